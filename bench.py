@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark: ADT pack+unpack GB/s (% of HBM peak) and weight-sync ms/iter.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config alexnet]
+
+One STEP = one weight-distribution pass of the whole synthetic weight set:
+  N = 1: pack every layer at its AWP width with the l2-norm fused (one launch)
+         + unpack every layer into the FP32 replica (one launch);
+  N > 1: each rank packs its shard (norm fused), ncclAllGather of the packed
+         bytes, every rank unpacks the full set (sharded.ShardedWeightSync).
+value = algorithmic bytes of all ranks / time = (Σ(4+r)n + N·Σ(r+4)n) / t,
+which at N = 1 is the pack+unpack round trip 2·Σ(4+r)n / t.
+
+Default workload: BASELINE.json configs[1] — AlexNet's 8 weight tensors
+(61,090,496 weights) at widths 8/16/24/32/8/16/24/32 bits by layer index,
+N(0, 0.1²) synthetic FP32 weights generated on the device (seed 0).
+The working set (244 MB FP32 + 149 MB packed + 244 MB replica) exceeds the
+126 MB L2, so no explicit flush is needed between steps.
+
+`--impl reference` times the reference CPU implementation (the oracle port of
+weightpack's pack_parallel / unpack / l2_norm, oracle/weightpack_oracle.py)
+on the host cores, rank 0 only, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADT pack+unpack GB/s (% HBM peak); weight-sync ms/iter at 1/2/4/8 GPUs"
+UNIT = "GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="alexnet", choices=["lenet", "alexnet", "vgg16", "resnet50", "1b"])
+    ap.add_argument("--bits", type=int, default=None, help="uniform width (default: the config's widths)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--quiet-extra", action="store_true", help="skip per-kernel event timing")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(args):
+    from paper_2004_02297_b200 import workloads
+    from paper_2004_02297_b200.codec import bits_to_round_to
+    counts = workloads.counts_of(args.config)
+    bits = workloads.default_bits(args.config, args.bits)
+    return counts, bits, [bits_to_round_to(b) for b in bits]
+
+
+def workload_name(args, bits):
+    b = "/".join(str(x) for x in bits) if len(set(bits)) > 1 else str(bits[0])
+    return f"{args.config} weight set, per-layer widths {b} bits"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------- reference (CPU)
+def cpu_reference_step(sample, rs, threads):
+    """One step of the reference CPU path on `sample` (list of float32 arrays):
+    pack_parallel + unpack + l2_norm per layer (weightpack codec.py:156-197,
+    precision.py:25-28, as restated in oracle/weightpack_oracle.py)."""
+    from oracle import weightpack_oracle as O
+    for w, r in zip(sample, rs):
+        p = O.pack_parallel(w, r, threads)
+        O.unpack(p, w.size, r)
+        O.l2_norm(w)
+
+
+def cpu_sample(counts, per_layer):
+    import numpy as np
+    rng = np.random.default_rng(0)
+    return [rng.standard_normal(min(n, per_layer), dtype=np.float32) * np.float32(0.1) for n in counts]
+
+
+def run_cpu_baseline(counts, rs, per_layer, reps):
+    sample = cpu_sample(counts, per_layer)
+    threads = len(os.sched_getaffinity(0))
+    byts = 2 * sum((4 + r) * w.size for w, r in zip(sample, rs))
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        cpu_reference_step(sample, rs, threads)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": byts / best / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first min(n, {per_layer}) weights of each layer ({sum(w.size for w in sample)} weights), "
+                      f"pack_parallel({threads} threads)+unpack+l2_norm, best of {reps}",
+            "seconds_per_pass": best}
+
+
+def main_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    counts, bits, rs = workload(args)
+    per_layer = 1 << 18
+    sample = cpu_sample(counts, per_layer)
+    threads = len(os.sched_getaffinity(0))
+    byts = 2 * sum((4 + r) * w.size for w, r in zip(sample, rs))
+    for _ in range(args.warmup):
+        cpu_reference_step(sample, rs, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_reference_step(sample, rs, threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = byts / dt / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic N(0,0.1^2) float32, seed 0",
+        "config": {"workload": workload_name(args, bits), "sample_weights": sum(w.size for w in sample)},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"first min(n, {per_layer}) weights of each layer per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2004_02297_b200 as adt
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    from paper_2004_02297_b200.precision import FixedPrecision
+
+    counts, bits, rs = workload(args)
+    L = len(counts)
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    masters = [torch.randn(n, generator=g, device=dev) * 0.1 for n in counts]
+    replicas = [torch.empty_like(m) for m in masters]
+
+    class Fixed(FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    sched = Fixed(L, 32)
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        layout = PackedLayout.plan(counts, rs)
+        packed = torch.empty(layout.nbytes, dtype=torch.uint8, device=dev)
+        ptab = engine.SegmentTable(masters, layout)
+        utab = engine.SegmentTable(replicas, layout)
+        sumsq = torch.empty(L, dtype=torch.float64, device=dev)
+
+        def do_pack():
+            engine.pack(ptab, packed, sumsq)
+
+        def do_unpack():
+            engine.unpack(utab, packed)
+
+        pack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
+        unpack_bytes = pack_bytes
+        kernels_per_step = 2
+    else:
+        from paper_2004_02297_b200.sharded import ShardedWeightSync
+        sync = ShardedWeightSync(masters, sched, replicas)
+        plan = sync.plan
+
+        def do_pack():
+            S = plan.send_bytes
+            engine.pack(sync.pack_table, sync.send[:S], sync.tail)
+            dist.all_gather_into_tensor(sync.recv[:S * world], sync.send[:S])
+
+        def do_unpack():
+            engine.unpack(sync.unpack_table, sync.recv[:plan.send_bytes * world])
+
+        pack_bytes = sum((pc.hi - pc.lo) * (4 + plan.round_tos[pc.layer]) for pc in plan.pieces[rank])
+        unpack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
+        kernels_per_step = 2
+
+    def step():
+        do_pack()
+        do_unpack()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    mids = [] if args.quiet_extra else [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                                          torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(local) as clocks:
+        e_start.record(stream)
+        for k in range(K):
+            if mids:
+                mids[k][0].record(stream)
+            do_pack()
+            if mids:
+                mids[k][1].record(stream)
+            do_unpack()
+            if mids:
+                mids[k][2].record(stream)
+        e_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e_start.elapsed_time(e_end) / K
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_bytes = (sum((4 + r) * n for n, r in zip(counts, rs))            # pack: every weight once (sharded)
+                   + world * sum((4 + r) * n for n, r in zip(counts, rs)))  # unpack: every rank, full set
+    value = total_bytes / (ms * 1e-3) / 1e9
+
+    pk = up = None
+    if mids:
+        pk = sum(a.elapsed_time(b) for a, b, _ in mids) / K
+        up = sum(b.elapsed_time(c) for _, b, c in mids) / K
+    hbm, peak_kind = peaks()
+    roofline = None
+    if pk is not None:
+        if world == 1:
+            dom, dur, byts = ("adt_unpack_kernel", up, unpack_bytes) if up >= pk else ("adt_pack_kernel", pk, pack_bytes)
+        else:
+            dom, dur, byts = "adt_unpack_kernel", up, unpack_bytes
+        achieved = byts / (dur * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": traffic_of(dom, args), "kernel": dom, "peak_source": f"{peak_kind} hbm_gbs (burst copy)",
+                    "pack_ms": pk, "unpack_ms": up,
+                    "pack_GBps": pack_bytes / (pk * 1e-3) / 1e9, "unpack_GBps": unpack_bytes / (up * 1e-3) / 1e9}
+
+    # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(args, masters, rs, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(counts, rs, per_layer=1 << 22, reps=2)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic N(0,0.1^2) float32 generated on device, seed 0",
+            "config": {"workload": workload_name(args, bits), "weights": sum(counts), "layers": L,
+                       "packed_payload_bytes": sum(n * r for n, r in zip(counts, rs)),
+                       "algorithmic_bytes_per_step": total_bytes,
+                       "l2": "working set (FP32 master + packed + FP32 replica) > 126 MB L2; no flush",
+                       "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
+            "sync_ms_per_iter": ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traffic_of(kernel, args):
+    """dram bytes per launch from a committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(args.config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def run_e2e(args, dev_masters, rs, dev):
+    """Same metric through the public API (WeightSync) with HOST buffers: every
+    step copies the FP32 masters from pinned host memory (H2D), packs (norms
+    fused) and unpacks through WeightSync.step, and reads the per-layer norms
+    back to the host (D2H) — the AWP observation."""
+    import torch
+    import paper_2004_02297_b200 as adt
+    from paper_2004_02297_b200.precision import FixedPrecision
+    host = [m.cpu().pin_memory() for m in dev_masters]
+    masters = [torch.empty_like(m) for m in dev_masters]
+
+    class Fixed(FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    sync = adt.WeightSync(masters, Fixed(len(masters), 32))
+    h2d = sum(h.numel() * 4 for h in host)
+    d2h = 8 * len(masters)
+
+    def one():
+        for m, h in zip(masters, host):
+            m.copy_(h, non_blocking=True)
+        sync.launch(fused_norm=True)
+        sync._read_norms()  # D2H of the L float64 sums + host sync
+
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    byts = sync.layout.roundtrip_bytes()
+    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": dt * 1e3, "note": "WeightSync.step path from pinned host FP32 masters; wall clock"}
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        main_reference(a)
+    else:
+        main_ours(a)

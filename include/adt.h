@@ -1,0 +1,105 @@
+/*
+ * adt.h — C ABI of the B200 ADT codec (Approximate Data Transfer, arXiv:2004.02297).
+ *
+ * The reference (`weightpack`, pure Python) has no native boundary; its drop-in
+ * surface is the Python API re-exported at /root/reference/pkg/src/weightpack/__init__.py:5-25.
+ * Each entry point below replaces the reference function cited beside it; the
+ * Python package `paper_2004_02297_b200` binds them through ctypes (see
+ * INTEGRATION.md for the binding a maintainer would add to `weightpack`).
+ *
+ * Rules of the boundary:
+ *   - plain pointers and sizes only; all buffers are caller-allocated device
+ *     memory (or mapped pinned host memory where stated); the library never
+ *     allocates;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream) and returns an int status: 0 = ADT_OK,
+ *     negative = error (see adt_strerror); the library never aborts;
+ *   - thread-safe: no mutable globals besides a per-device attribute cache.
+ *
+ * Packed layout (codec.py:76-107): layer l's payload is
+ * count_l * round_to_l bytes at byte `offset` of the packed buffer; weight i of
+ * the layer occupies payload bytes [i*r, (i+1)*r), most-significant byte first
+ * (the top r bytes of the IEEE-754 word, big-endian). Offsets must be 16-byte
+ * aligned (pad between layers is not part of any payload).
+ */
+#ifndef ADT_H
+#define ADT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADT_ABI_VERSION 1
+
+/* status codes */
+#define ADT_OK 0
+#define ADT_ERR_ROUND_TO (-1)   /* round_to outside [1, 4]            -> ValueError (codec.py:52-57) */
+#define ADT_ERR_ALIGN (-2)      /* weights/packed/offset not 16-B aligned */
+#define ADT_ERR_ARG (-3)        /* NULL pointer with nonzero count, nseg < 0, overflow */
+#define ADT_ERR_NO_DEVICE (-4)  /* no CUDA device / driver */
+#define ADT_ERR_CUDA_BASE (-1000) /* -(1000 + cudaError_t) for CUDA runtime errors */
+
+/* Weights per tile: the unit of work of one CTA and of one norm partial. */
+#define ADT_TILE_WEIGHTS 4096
+
+/* One layer (a "segment" of the packed stream). */
+typedef struct adt_segment {
+    void *weights;      /* FP32 words of the layer, 16-B aligned. pack: read; unpack: written */
+    uint64_t count;     /* number of weights (may be 0) */
+    uint64_t offset;    /* byte offset of this layer's payload in the packed buffer, 16-B aligned */
+    int32_t round_to;   /* bytes kept per weight, 1..4 (codec.py:52-57; bits_to_round_to codec.py:60-67) */
+    int32_t reserved;   /* must be 0 */
+} adt_segment;
+
+/* ABI version (ADT_ABI_VERSION). */
+int adt_abi_version(void);
+
+/* Human-readable text for a status code (static storage). */
+const char *adt_strerror(int status);
+
+/* Number of tiles (= norm partials) a pack/sumsq over `segs` uses; size
+ * `tile_partials` (doubles) to at least this. Host-only, no device work. */
+int adt_tile_count(const adt_segment *segs, int nseg, uint64_t *ntiles);
+
+/*
+ * Multi-tensor pack.  Replaces codec.pack / pack_vectorized / pack_parallel
+ * (codec.py:116-180) applied to every layer, and — when `seg_sumsq` is non-NULL —
+ * fuses precision.l2_norm (precision.py:25-28): seg_sumsq[l] receives the float64
+ * sum of squares of layer l (sqrt it for the norm), reduced in a fixed order so
+ * results are bit-identical run to run.  When seg_sumsq != NULL, `tile_partials`
+ * (adt_tile_count doubles) and `seg_counters` (nseg uint32, zero-initialised once
+ * by the caller; the kernel leaves them zero) are required scratch.
+ */
+int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed,
+             double *seg_sumsq, double *tile_partials, uint32_t *seg_counters,
+             void *stream);
+
+/*
+ * Multi-tensor unpack.  Replaces codec.unpack (codec.py:183-197) applied to
+ * every layer: writes count_l FP32 words to segs[l].weights, the kept bytes in
+ * the high bytes and zeros below.  `packed` may be device memory or mapped
+ * (pinned, cudaHostAlloc) host memory — the latter is the zero-copy
+ * host->device path (packed weights crossing from CPU master
+ * weights to the GPU).
+ */
+int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *stream);
+
+/*
+ * Norm-only pass (no packed output): seg_sumsq[l] = float64 sum of squares of
+ * layer l.  Replaces precision.l2_norm (precision.py:25-28) for the batch whose
+ * norm is not fused into a pack (the last observation of a run, training.py:246-254).
+ */
+int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq,
+              double *tile_partials, uint32_t *seg_counters, void *stream);
+
+/* Number of SMs of the current device (cached). */
+int adt_device_sm_count(int *sm_count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADT_H */

@@ -1,0 +1,121 @@
+"""ctypes binding of the in-tree C-ABI library `libadt.so` (include/adt.h).
+
+There is no CPU fallback: if the library is missing, or no CUDA device is
+present when a compute entry point is called, the call raises. Status codes
+map to the reference's exception types (ValueError for a bad round_to,
+codec.py:52-57) or RuntimeError for CUDA failures.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libadt.so")
+
+ADT_OK = 0
+ADT_ERR_ROUND_TO = -1
+ADT_ERR_ALIGN = -2
+ADT_ERR_ARG = -3
+ADT_ERR_NO_DEVICE = -4
+ADT_ERR_CUDA_BASE = -1000
+TILE_WEIGHTS = 4096
+ABI_VERSION = 1
+
+EXPORTS = ("adt_abi_version", "adt_strerror", "adt_tile_count", "adt_pack", "adt_unpack",
+           "adt_sumsq", "adt_device_sm_count")
+
+
+class Segment(ctypes.Structure):
+    """adt_segment (include/adt.h)."""
+
+    _fields_ = [
+        ("weights", ctypes.c_void_p),
+        ("count", ctypes.c_uint64),
+        ("offset", ctypes.c_uint64),
+        ("round_to", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class AdtError(RuntimeError):
+    """A CUDA or argument failure reported by libadt."""
+
+    def __init__(self, status: int, text: str):
+        super().__init__(f"libadt status {status}: {text}")
+        self.status = status
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libadt.so once; raise loudly if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the sm_100a library first "
+                "(python -m paper_2004_02297_b200._build, or __graft_entry__.build()). "
+                "There is no CPU fallback.")
+        lib = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        seg_p = P(Segment)
+        vp = ctypes.c_void_p
+        lib.adt_abi_version.restype = ctypes.c_int
+        lib.adt_abi_version.argtypes = []
+        lib.adt_strerror.restype = ctypes.c_char_p
+        lib.adt_strerror.argtypes = [ctypes.c_int]
+        lib.adt_tile_count.restype = ctypes.c_int
+        lib.adt_tile_count.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_uint64)]
+        lib.adt_pack.restype = ctypes.c_int
+        lib.adt_pack.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp, vp]
+        lib.adt_unpack.restype = ctypes.c_int
+        lib.adt_unpack.argtypes = [seg_p, ctypes.c_int, vp, vp]
+        lib.adt_sumsq.restype = ctypes.c_int
+        lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
+        lib.adt_device_sm_count.restype = ctypes.c_int
+        lib.adt_device_sm_count.argtypes = [P(ctypes.c_int)]
+        if lib.adt_abi_version() != ABI_VERSION:
+            raise ImportError(f"libadt ABI {lib.adt_abi_version()} != expected {ABI_VERSION}; rebuild")
+        _lib = lib
+        return lib
+
+
+def strerror(status: int) -> str:
+    return load().adt_strerror(status).decode()
+
+
+def check(status: int) -> None:
+    """Map a libadt status to the reference's exception types."""
+    if status == ADT_OK:
+        return
+    text = strerror(status)
+    if status == ADT_ERR_ROUND_TO:
+        raise ValueError(text)
+    raise AdtError(status, text)
+
+
+def segment_array(segs) -> ctypes.Array:
+    """[(ptr, count, offset, round_to), ...] -> adt_segment[]."""
+    arr = (Segment * max(1, len(segs)))()
+    for i, (ptr, count, offset, r) in enumerate(segs):
+        arr[i].weights = ptr
+        arr[i].count = count
+        arr[i].offset = offset
+        arr[i].round_to = r
+        arr[i].reserved = 0
+    return arr
+
+
+def tile_count(seg_arr, nseg: int) -> int:
+    out = ctypes.c_uint64(0)
+    check(load().adt_tile_count(seg_arr, nseg, ctypes.byref(out)))
+    return int(out.value)

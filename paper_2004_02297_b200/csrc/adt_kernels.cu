@@ -1,0 +1,482 @@
+// adt_kernels.cu — sm_100a kernels and the C ABI (include/adt.h) of the ADT codec.
+//
+// What the reference computes (pure NumPy, /root/reference/pkg/src/weightpack):
+//   pack    codec.py:116-180  keep the top r bytes of every FP32 word, MSB first
+//   unpack  codec.py:183-197  kept bytes -> word MSBs, low bytes zero
+//   norm    precision.py:25-28 float64 l2-norm of a layer's master weights
+//
+// B200 design: the path is pure byte movement, HBM-bound
+// (pack reads 4n and writes r*n bytes; unpack the reverse), so the kernels are
+// built around coalesced 128-bit traffic, not tensor cores:
+//   * multi-tensor: one launch walks a per-layer descriptor table passed by
+//     value in kernel parameter space (__grid_constant__, up to 256 layers per
+//     launch); each CTA owns one 4096-weight tile of one layer and finds its
+//     layer with a uniform binary search over the tile prefix table;
+//   * byte compaction with PRMT (__byte_perm): r = 1, 2, 4 are warp-coalesced
+//     32/64/128-bit stores straight from registers; r = 3 (12 bytes per 4
+//     weights) is staged through shared memory and written as 16-byte vectors;
+//   * the layer's float64 sum of squares is fused into the pack pass (every
+//     weight is read once); partials are per tile and the last CTA of a layer
+//     reduces them in a fixed order, so norms are run-to-run bit-identical
+//     (no floating-point atomics).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <limits.h>
+
+#include "adt.h"
+
+namespace {
+
+constexpr int kThreads = 256;                      // 8 warps per CTA
+constexpr int kVec = 4;                            // float4 groups per thread per tile
+constexpr int kTile = kThreads * kVec * 4;         // weights per tile
+static_assert(kTile == ADT_TILE_WEIGHTS, "tile size is part of the ABI");
+
+template <int MAXSEG>
+struct Table {
+    const uint8_t *packed_in;   // unpack source (device or mapped host)
+    uint8_t *packed_out;        // pack destination
+    double *seg_sumsq;          // per-layer result (chunk-relative)
+    double *partials;           // per-tile scratch (chunk-relative)
+    uint32_t *counters;         // per-layer completion counters (chunk-relative)
+    int nseg;
+    uint32_t tile_begin[MAXSEG + 1];
+    uint64_t count[MAXSEG];
+    uint64_t offset[MAXSEG];
+    uintptr_t weights[MAXSEG];
+    uint8_t round_to[MAXSEG];
+};
+
+// ----------------------------------------------------------- byte compaction
+// Word w of the layer is little-endian in memory (byte 3 = MSB). The payload
+// wants the MSBs first: for 4 consecutive words a,b,c,d and r kept bytes the
+// payload is a3..a(4-r) b3.. c3.. d3.. — r 32-bit payload words per 4 weights.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    return __byte_perm(a, b, sel);
+}
+
+__device__ __forceinline__ void pack_r1(const uint4 &v, uint32_t *o) {
+    o[0] = prmt(prmt(v.x, v.y, 0x0073), prmt(v.z, v.w, 0x0073), 0x5410);
+}
+__device__ __forceinline__ void pack_r2(const uint4 &v, uint32_t *o) {
+    o[0] = prmt(v.x, v.y, 0x6723);
+    o[1] = prmt(v.z, v.w, 0x6723);
+}
+__device__ __forceinline__ void pack_r3(const uint4 &v, uint32_t *o) {
+    o[0] = prmt(v.x, v.y, 0x7123);
+    o[1] = prmt(v.y, v.z, 0x6712);
+    o[2] = prmt(v.z, v.w, 0x5671);
+}
+__device__ __forceinline__ void pack_r4(const uint4 &v, uint32_t *o) {
+    o[0] = prmt(v.x, 0, 0x0123);
+    o[1] = prmt(v.y, 0, 0x0123);
+    o[2] = prmt(v.z, 0, 0x0123);
+    o[3] = prmt(v.w, 0, 0x0123);
+}
+__device__ __forceinline__ void pack_any(int r, const uint4 &v, uint32_t *o) {
+    switch (r) {
+        case 1: pack_r1(v, o); break;
+        case 2: pack_r2(v, o); break;
+        case 3: pack_r3(v, o); break;
+        default: pack_r4(v, o); break;
+    }
+}
+
+__device__ __forceinline__ uint4 unpack_r1(uint32_t p) {
+    return make_uint4(prmt(p, 0, 0x0444), prmt(p, 0, 0x1444), prmt(p, 0, 0x2444), prmt(p, 0, 0x3444));
+}
+__device__ __forceinline__ uint4 unpack_r2(uint32_t p, uint32_t q) {
+    return make_uint4(prmt(p, 0, 0x0144), prmt(p, 0, 0x2344), prmt(q, 0, 0x0144), prmt(q, 0, 0x2344));
+}
+__device__ __forceinline__ uint4 unpack_r3(uint32_t p, uint32_t q, uint32_t s) {
+    return make_uint4(prmt(p, 0, 0x0124), prmt(p, q, 0x3450) & 0xFFFFFF00u,
+                      prmt(q, s, 0x2340) & 0xFFFFFF00u, prmt(s, 0, 0x1234));
+}
+__device__ __forceinline__ uint4 unpack_r4(const uint4 &p) {
+    return make_uint4(prmt(p.x, 0, 0x0123), prmt(p.y, 0, 0x0123), prmt(p.z, 0, 0x0123), prmt(p.w, 0, 0x0123));
+}
+__device__ __forceinline__ uint4 unpack_words(int r, const uint32_t *w) {
+    switch (r) {
+        case 1: return unpack_r1(w[0]);
+        case 2: return unpack_r2(w[0], w[1]);
+        case 3: return unpack_r3(w[0], w[1], w[2]);
+        default: return unpack_r4(make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
+// ------------------------------------------------------------------ helpers
+template <int MAXSEG>
+__device__ __forceinline__ int find_segment(const Table<MAXSEG> &T, uint32_t tile) {
+    // last s with tile_begin[s] <= tile (zero-tile layers are never selected)
+    int lo = 0, hi = T.nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (T.tile_begin[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ double sq_acc(double acc, uint32_t w) {
+    const double d = static_cast<double>(__uint_as_float(w));  // exact widening
+    return fma(d, d, acc);                                    // exact square, rounded add
+}
+
+// Fixed-order CTA reduction; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double *red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+    }
+    return s;
+}
+
+// Tile partial -> (last CTA of the layer) fixed-order layer total.
+template <int MAXSEG>
+__device__ __forceinline__ void norm_epilogue(const Table<MAXSEG> &T, int s, uint32_t tile, double acc) {
+    __shared__ double red[kThreads / 32];
+    __shared__ int last;
+    const double part = block_sum(acc, red);
+    if (threadIdx.x == 0) {
+        T.partials[tile] = part;
+        __threadfence();
+        const uint32_t ntiles = T.tile_begin[s + 1] - T.tile_begin[s];
+        last = (atomicAdd(&T.counters[s], 1u) == ntiles - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double a = 0.0;
+    for (uint32_t i = T.tile_begin[s] + threadIdx.x; i < T.tile_begin[s + 1]; i += kThreads)
+        a += __ldcg(&T.partials[i]);
+    __syncthreads();  // red reuse
+    const double total = block_sum(a, red);
+    if (threadIdx.x == 0) {
+        T.seg_sumsq[s] = total;
+        T.counters[s] = 0u;  // re-arm for the next stream-ordered call
+    }
+}
+
+template <int MAXSEG>
+__device__ __forceinline__ void zero_empty_layers(const Table<MAXSEG> &T) {
+    if (blockIdx.x != 0) return;
+    for (int i = threadIdx.x; i < T.nseg; i += kThreads)
+        if (T.count[i] == 0) T.seg_sumsq[i] = 0.0;
+}
+
+// ---------------------------------------------------------------- pack pass
+// WRITE=false is the norm-only pass (adt_sumsq).
+template <int MAXSEG, bool NORM, bool WRITE>
+__global__ void __launch_bounds__(kThreads)
+adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
+    __shared__ __align__(16) uint32_t stage[kTile];   // r*kTile/4 words used (r = 3 or tails)
+    const uint32_t tile = blockIdx.x;
+    const int s = find_segment(T, tile);
+    const uint64_t n = T.count[s];
+    const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
+    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n - e0));
+    const int r = T.round_to[s];
+    const int t = threadIdx.x;
+    const uint4 *src = reinterpret_cast<const uint4 *>(T.weights[s]) + e0 / 4;
+
+    uint4 v[kVec];
+    if (m == kTile) {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) v[k] = __ldcs(src + k * kThreads + t);
+    } else {
+        const uint32_t *src1 = reinterpret_cast<const uint32_t *>(src);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            const uint32_t i = (k * kThreads + t) * 4;
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
+            v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+
+    if (NORM) zero_empty_layers(T);
+    double acc = 0.0;
+    if (NORM) {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            acc = sq_acc(acc, v[k].x);
+            acc = sq_acc(acc, v[k].y);
+            acc = sq_acc(acc, v[k].z);
+            acc = sq_acc(acc, v[k].w);
+        }
+    }
+
+    if (WRITE) {
+        uint8_t *dst = T.packed_out + T.offset[s] + e0 * r;
+        if (m == kTile && r != 3) {
+            // direct warp-coalesced stores from registers
+            if (r == 1) {
+                uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+#pragma unroll
+                for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); d[k * kThreads + t] = o[0]; }
+            } else if (r == 2) {
+                uint2 *d = reinterpret_cast<uint2 *>(dst);
+#pragma unroll
+                for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); d[k * kThreads + t] = make_uint2(o[0], o[1]); }
+            } else {
+                uint4 *d = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+                for (int k = 0; k < kVec; ++k) { uint32_t o[4]; pack_r4(v[k], o); d[k * kThreads + t] = make_uint4(o[0], o[1], o[2], o[3]); }
+            }
+        } else {
+            // stage r words per float4 group in shared memory, then 16-byte stores
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) {
+                uint32_t o[4];
+                pack_any(r, v[k], o);
+                uint32_t *p = stage + (k * kThreads + t) * r;
+                for (int j = 0; j < r; ++j) p[j] = o[j];
+            }
+            __syncthreads();
+            const uint32_t nbytes = m * r;
+            const uint32_t n16 = nbytes / 16;
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
+            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+            for (uint32_t i = t; i < n16; i += kThreads) d4[i] = s4[i];
+            const uint8_t *s1 = reinterpret_cast<const uint8_t *>(stage);
+            for (uint32_t i = n16 * 16 + t; i < nbytes; i += kThreads) dst[i] = s1[i];
+        }
+    }
+
+    if (NORM) norm_epilogue(T, s, tile, acc);
+}
+
+// -------------------------------------------------------------- unpack pass
+template <int MAXSEG>
+__global__ void __launch_bounds__(kThreads)
+adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
+    __shared__ __align__(16) uint32_t stage[kTile];
+    const uint32_t tile = blockIdx.x;
+    const int s = find_segment(T, tile);
+    const uint64_t n = T.count[s];
+    const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
+    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n - e0));
+    const int r = T.round_to[s];
+    const int t = threadIdx.x;
+    const uint8_t *src = T.packed_in + T.offset[s] + e0 * r;
+    uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
+
+    if (m == kTile && r != 3) {
+        if (r == 1) {
+            const uint32_t *p = reinterpret_cast<const uint32_t *>(src);
+            uint32_t w[kVec];
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + k * kThreads + t);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) dst[k * kThreads + t] = unpack_r1(w[k]);
+        } else if (r == 2) {
+            const uint2 *p = reinterpret_cast<const uint2 *>(src);
+            uint2 w[kVec];
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + k * kThreads + t);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) dst[k * kThreads + t] = unpack_r2(w[k].x, w[k].y);
+        } else {
+            const uint4 *p = reinterpret_cast<const uint4 *>(src);
+            uint4 w[kVec];
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + k * kThreads + t);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) dst[k * kThreads + t] = unpack_r4(w[k]);
+        }
+        return;
+    }
+
+    // staged path: r = 3 tiles and every layer's ragged last tile
+    const uint32_t nbytes = m * r;
+    const uint32_t n16 = nbytes / 16;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *st4 = reinterpret_cast<uint4 *>(stage);
+    for (uint32_t i = t; i < n16; i += kThreads) st4[i] = __ldcs(s4 + i);
+    uint8_t *st1 = reinterpret_cast<uint8_t *>(stage);
+    for (uint32_t i = n16 * 16 + t; i < nbytes; i += kThreads) st1[i] = src[i];
+    __syncthreads();
+    uint32_t *dst1 = reinterpret_cast<uint32_t *>(dst);
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+        const uint32_t g = k * kThreads + t;   // float4 group within the tile
+        if (g * 4 >= m) break;
+        const uint4 o = unpack_words(r, stage + g * r);
+        if (g * 4 + 4 <= m) {
+            dst[g] = o;
+        } else {
+            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+            for (uint32_t j = 0; g * 4 + j < m; ++j) dst1[g * 4 + j] = ow[j];
+        }
+    }
+}
+
+// ----------------------------------------------------------------- host side
+enum class Pass { Pack, PackNorm, Norm, Unpack };
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? ADT_OK : ADT_ERR_CUDA_BASE - static_cast<int>(e); }
+
+int validate(const adt_segment *segs, int nseg, const void *packed, bool need_packed) {
+    if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
+    bool any = false;
+    for (int i = 0; i < nseg; ++i) {
+        const adt_segment &g = segs[i];
+        if (g.round_to < 1 || g.round_to > 4) return ADT_ERR_ROUND_TO;
+        if (g.reserved != 0) return ADT_ERR_ARG;
+        if (g.count == 0) continue;
+        any = true;
+        if (g.weights == nullptr) return ADT_ERR_ARG;
+        if (reinterpret_cast<uintptr_t>(g.weights) % 16 || g.offset % 16) return ADT_ERR_ALIGN;
+        if (g.count > (UINT64_MAX - g.offset) / 4) return ADT_ERR_ARG;
+        if ((g.count + kTile - 1) / kTile > static_cast<uint64_t>(INT_MAX)) return ADT_ERR_ARG;
+    }
+    if (any && need_packed) {
+        if (packed == nullptr) return ADT_ERR_ARG;
+        if (reinterpret_cast<uintptr_t>(packed) % 16) return ADT_ERR_ALIGN;
+    }
+    return ADT_OK;
+}
+
+template <int MAXSEG>
+int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
+                 double *seg_sumsq, double *partials, uint32_t *counters, uint32_t ntiles,
+                 cudaStream_t stream) {
+    Table<MAXSEG> T;
+    T.packed_in = pin;
+    T.packed_out = pout;
+    T.seg_sumsq = seg_sumsq;
+    T.partials = partials;
+    T.counters = counters;
+    T.nseg = nseg;
+    uint32_t acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+        T.tile_begin[i] = acc;
+        acc += static_cast<uint32_t>((segs[i].count + kTile - 1) / kTile);
+        T.count[i] = segs[i].count;
+        T.offset[i] = segs[i].offset;
+        T.weights[i] = reinterpret_cast<uintptr_t>(segs[i].weights);
+        T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
+    }
+    T.tile_begin[nseg] = acc;
+    if (ntiles == 0) {
+        if (pass == Pass::PackNorm || pass == Pass::Norm)
+            return cuda_status(cudaMemsetAsync(seg_sumsq, 0, sizeof(double) * nseg, stream));
+        return ADT_OK;
+    }
+    const dim3 grid(ntiles), block(kThreads);
+    switch (pass) {
+        case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T); break;
+        case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T); break;
+        case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T); break;
+        case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T); break;
+    }
+    return cuda_status(cudaGetLastError());
+}
+
+constexpr int kSmallSeg = 16;
+constexpr int kLargeSeg = 256;
+
+int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
+        double *seg_sumsq, double *partials, uint32_t *counters, void *stream_v) {
+    const bool norm = pass == Pass::PackNorm || pass == Pass::Norm;
+    if (norm && nseg > 0 && (seg_sumsq == nullptr || partials == nullptr || counters == nullptr))
+        return ADT_ERR_ARG;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+    uint64_t partial_base = 0;
+    int base = 0;
+    while (base < nseg) {
+        // greedy chunk: <= kLargeSeg layers and < 2^31 tiles per launch
+        int cnt = 0;
+        uint64_t tiles = 0;
+        while (base + cnt < nseg && cnt < kLargeSeg) {
+            const uint64_t t = (segs[base + cnt].count + kTile - 1) / kTile;
+            if (cnt > 0 && tiles + t > static_cast<uint64_t>(INT_MAX)) break;
+            tiles += t;
+            ++cnt;
+        }
+        double *ss = norm ? seg_sumsq + base : nullptr;
+        double *pp = norm ? partials + partial_base : nullptr;
+        uint32_t *cc = norm ? counters + base : nullptr;
+        const int st = cnt <= kSmallSeg
+            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, pin, pout, ss, pp, cc, static_cast<uint32_t>(tiles), stream)
+            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, pin, pout, ss, pp, cc, static_cast<uint32_t>(tiles), stream);
+        if (st != ADT_OK) return st;
+        partial_base += tiles;
+        base += cnt;
+    }
+    return ADT_OK;
+}
+
+}  // namespace
+
+// -------------------------------------------------------------------- C ABI
+extern "C" {
+
+int adt_abi_version(void) { return ADT_ABI_VERSION; }
+
+const char *adt_strerror(int status) {
+    switch (status) {
+        case ADT_OK: return "ok";
+        case ADT_ERR_ROUND_TO: return "round_to must be an integer in [1, 4]";
+        case ADT_ERR_ALIGN: return "weights, packed buffer and layer offsets must be 16-byte aligned";
+        case ADT_ERR_ARG: return "invalid argument (null pointer, negative count or size overflow)";
+        case ADT_ERR_NO_DEVICE: return "no CUDA device available";
+        default:
+            if (status <= ADT_ERR_CUDA_BASE)
+                return cudaGetErrorString(static_cast<cudaError_t>(ADT_ERR_CUDA_BASE - status));
+            return "unknown adt status";
+    }
+}
+
+int adt_tile_count(const adt_segment *segs, int nseg, uint64_t *ntiles) {
+    if (ntiles == nullptr || nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
+    uint64_t t = 0;
+    for (int i = 0; i < nseg; ++i) t += (segs[i].count + kTile - 1) / kTile;
+    *ntiles = t;
+    return ADT_OK;
+}
+
+int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed, double *seg_sumsq,
+             double *tile_partials, uint32_t *seg_counters, void *stream) {
+    const int v = validate(segs, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    return run(seg_sumsq ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, packed, seg_sumsq,
+               tile_partials, seg_counters, stream);
+}
+
+int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *stream) {
+    const int v = validate(segs, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    return run(Pass::Unpack, segs, nseg, packed, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *tile_partials,
+              uint32_t *seg_counters, void *stream) {
+    const int v = validate(segs, nseg, nullptr, false);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && seg_sumsq == nullptr) return ADT_ERR_ARG;
+    return run(Pass::Norm, segs, nseg, nullptr, nullptr, seg_sumsq, tile_partials, seg_counters, stream);
+}
+
+int adt_device_sm_count(int *sm_count) {
+    if (sm_count == nullptr) return ADT_ERR_ARG;
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return ADT_ERR_NO_DEVICE;
+    if (dev >= 0 && dev < 64 && cache[dev] > 0) { *sm_count = cache[dev]; return ADT_OK; }
+    int v = 0;
+    e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (dev >= 0 && dev < 64) cache[dev] = v;
+    *sm_count = v;
+    return ADT_OK;
+}
+
+}  // extern "C"

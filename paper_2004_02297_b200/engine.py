@@ -1,0 +1,130 @@
+"""Device engine: multi-tensor pack / unpack / norm launches through libadt.
+
+Everything here is stream-ordered on the caller's (or torch's current) CUDA
+stream; buffers are torch tensors so the caching allocator owns lifetimes and
+the C side allocates nothing (include/adt.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .layout import PackedLayout
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2004_02297_b200 needs a CUDA device (B200, sm_100a); there is no CPU path")
+    _lib.load()
+
+
+def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _check_weight(t: torch.Tensor, count: int, what: str) -> int:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what}: expected a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{what}: expected float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+    if t.numel() != count:
+        raise ValueError(f"{what}: {t.numel()} weights, layout says {count}")
+    ptr = t.data_ptr()
+    if count and ptr % 16:
+        raise ValueError(f"{what}: data pointer not 16-byte aligned")
+    return ptr
+
+
+class SegmentTable:
+    """A prepared adt_segment[] over fixed weight tensors and a layout.
+
+    Building the table costs Python time proportional to the layer count, so
+    long-lived callers (WeightSync, bench) build it once and reuse it.
+    """
+
+    def __init__(self, weights: Sequence[torch.Tensor], layout: PackedLayout):
+        if len(weights) != layout.num_layers:
+            raise ValueError(f"{len(weights)} tensors for a {layout.num_layers}-layer layout")
+        self.layout = layout
+        self.tensors = list(weights)  # keep alive
+        segs = []
+        for i, (t, n, off, r) in enumerate(zip(weights, layout.counts, layout.offsets, layout.round_tos)):
+            segs.append((_check_weight(t, n, f"layer {i}"), n, off, r))
+        self.nseg = len(segs)
+        self.array = _lib.segment_array(segs)
+        self.ntiles = _lib.tile_count(self.array, self.nseg)
+
+
+class _Scratch:
+    """Per (device, stream) norm scratch: tile partials + zeroed layer counters."""
+
+    _lock = threading.Lock()
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, device: torch.device, stream: int, ntiles: int, nseg: int):
+        key = (device.index, stream)
+        with cls._lock:
+            cur = cls._cache.get(key)
+            if cur is None or cur[0].numel() < max(1, ntiles) or cur[1].numel() < max(1, nseg):
+                parts = torch.empty(max(1, ntiles, cur[0].numel() if cur else 0), dtype=torch.float64, device=device)
+                ctr = torch.zeros(max(1, nseg, cur[1].numel() if cur else 0), dtype=torch.int32, device=device)
+                cur = (parts, ctr)
+                cls._cache[key] = cur
+            return cur
+
+
+def _device_of(table: SegmentTable) -> torch.device:
+    for t in table.tensors:
+        return t.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def pack(table: SegmentTable, packed: torch.Tensor, sumsq: torch.Tensor | None = None,
+         stream: torch.cuda.Stream | None = None) -> None:
+    """adt_pack: every layer of `table` into `packed` (uint8, >= layout.nbytes);
+    with `sumsq` (float64[L]) the per-layer sums of squares are fused in."""
+    if packed.dtype != torch.uint8 or not packed.is_cuda or packed.numel() < table.layout.payload_end:
+        raise ValueError("packed must be a CUDA uint8 tensor covering every layer's payload")
+    sh = stream_handle(stream)
+    if sumsq is None:
+        _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), None, None, None, sh))
+        return
+    if sumsq.dtype != torch.float64 or not sumsq.is_cuda or sumsq.numel() < table.nseg:
+        raise ValueError("sumsq must be a CUDA float64 tensor with one entry per layer")
+    parts, ctr = _Scratch.get(packed.device, sh, table.ntiles, table.nseg)
+    _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), sumsq.data_ptr(),
+                                    parts.data_ptr(), ctr.data_ptr(), sh))
+
+
+def unpack(table: SegmentTable, packed: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_unpack: `packed` (CUDA, or pinned host = zero-copy) into the table's tensors."""
+    if packed.dtype != torch.uint8 or packed.numel() < table.layout.payload_end:
+        raise ValueError("packed must be a uint8 tensor covering every layer's payload")
+    if not packed.is_cuda and not packed.is_pinned():
+        raise ValueError("packed must live on the device or in pinned (page-locked) host memory")
+    _lib.check(_lib.load().adt_unpack(table.array, table.nseg, packed.data_ptr(), stream_handle(stream)))
+
+
+def sumsq(table: SegmentTable, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_sumsq: float64 sum of squares of every layer (norm-only pass)."""
+    if out.dtype != torch.float64 or not out.is_cuda or out.numel() < table.nseg:
+        raise ValueError("out must be a CUDA float64 tensor with one entry per layer")
+    sh = stream_handle(stream)
+    parts, ctr = _Scratch.get(out.device, sh, table.ntiles, table.nseg)
+    _lib.check(_lib.load().adt_sumsq(table.array, table.nseg, out.data_ptr(), parts.data_ptr(),
+                                     ctr.data_ptr(), sh))
+
+
+def sm_count() -> int:
+    v = ctypes.c_int(0)
+    _lib.check(_lib.load().adt_device_sm_count(ctypes.byref(v)))
+    return int(v.value)

@@ -1,0 +1,117 @@
+"""Per-step weight distribution with ADT + AWP on one device.
+
+Reference caller contract (training.py:207-254):
+  batch b: pack every layer of the FP32 master at the controller's current
+  widths -> each worker unpacks its replica -> ... -> update master ->
+  l2-norm of every post-update master layer -> observe_batch -> widths for b+1.
+
+B200 flow (one pack launch with the norm fused, one unpack launch):
+  step(b): pack W_b at the widths in force (norm of W_b fused into the same
+  read), unpack into the replicas, then read the L float64 sums back, observe
+  them (this is the reference's end-of-batch-(b-1) observation of the
+  post-update master W_b), and if any width escalated, re-plan and re-pack /
+  re-unpack at the new widths. Escalations are rare (at most
+  log2-ish (32-initial)/step per layer per run), so the common step is exactly
+  two kernel launches and one 8·L-byte device->host read, with results
+  byte-identical to the reference's order. step(0) observes nothing (the
+  reference's first observation is of the post-update-0 master), and
+  observe_final() runs a norm-only pass for the last post-update master.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+
+from . import engine
+from .layout import PackedLayout
+from .precision import FixedPrecision, PrecisionController
+
+
+@dataclass
+class SyncResult:
+    round_tos: list[int]             # widths the replicas were produced with this step
+    trace: list[tuple] = field(default_factory=list)  # TRACE_HEADER rows observed this step
+    repacked: bool = False           # a width escalated and the step was redone
+
+
+class WeightSync:
+    """Masters (CUDA float32 tensors, one per layer) -> packed bytes -> replicas."""
+
+    def __init__(self, masters: Sequence[torch.Tensor], schedule=None,
+                 replicas: Sequence[torch.Tensor] | None = None):
+        engine.require_cuda()
+        self.masters = [m.detach().reshape(-1) for m in masters]
+        for i, m in enumerate(self.masters):
+            if not m.is_cuda or m.dtype != torch.float32 or not m.is_contiguous():
+                raise TypeError(f"master layer {i}: need a contiguous CUDA float32 tensor")
+        self.counts = [m.numel() for m in self.masters]
+        self.schedule = schedule if schedule is not None else FixedPrecision(len(self.masters), 32)
+        if self.schedule.num_layers != len(self.masters):
+            raise ValueError("schedule layer count differs from the number of master tensors")
+        self.adaptive = isinstance(self.schedule, PrecisionController)
+        dev = self.masters[0].device if self.masters else torch.device("cuda")
+        if replicas is None:
+            replicas = [torch.empty_like(m) for m in self.masters]
+        self.replicas = [r.reshape(-1) for r in replicas]
+        self.sumsq = torch.zeros(len(self.masters), dtype=torch.float64, device=dev)
+        self._host_sumsq = torch.empty(len(self.masters), dtype=torch.float64, pin_memory=True)
+        self.device = dev
+        self.layout = None
+        self.packed = None
+        self._plan(self.schedule.round_tos())
+
+    def _plan(self, round_tos):
+        self.layout = PackedLayout.plan(self.counts, round_tos)
+        if self.packed is None or self.packed.numel() < self.layout.nbytes:
+            # capacity for every width up to 4 bytes: re-plans never reallocate
+            cap = PackedLayout.plan(self.counts, [4] * len(self.counts)).nbytes
+            self.packed = torch.empty(max(16, cap), dtype=torch.uint8, device=self.device)
+        self.pack_table = engine.SegmentTable(self.masters, self.layout)
+        self.unpack_table = engine.SegmentTable(self.replicas, self.layout)
+
+    @property
+    def round_tos(self) -> list[int]:
+        return list(self.layout.round_tos)
+
+    def launch(self, fused_norm: bool, stream=None) -> None:
+        """The device work of one step: pack (+ fused norms), unpack. No host sync."""
+        engine.pack(self.pack_table, self.packed, self.sumsq if fused_norm else None, stream)
+        engine.unpack(self.unpack_table, self.packed, stream)
+
+    def _read_norms(self) -> list[float]:
+        self._host_sumsq.copy_(self.sumsq, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return [math.sqrt(v) for v in self._host_sumsq.tolist()]
+
+    def step(self, batch: int = 0, observe: bool | None = None) -> SyncResult:
+        """One batch of weight distribution (see module doc for the ordering)."""
+        if observe is None:
+            observe = self.adaptive and batch > 0
+        used = self.round_tos
+        self.launch(fused_norm=observe)
+        res = SyncResult(round_tos=used)
+        if not observe:
+            return res
+        res.trace = self.schedule.observe_all(self._read_norms(), batch=batch - 1)
+        new = self.schedule.round_tos()
+        if new != used:
+            self._plan(new)
+            self.launch(fused_norm=False)
+            res.round_tos = new
+            res.repacked = True
+        return res
+
+    def observe_final(self, batch: int) -> list[tuple]:
+        """Norm-only pass over the masters (the observation after the last
+        update, training.py:246-254); returns its trace rows labelled `batch`."""
+        engine.sumsq(self.pack_table, self.sumsq)
+        return self.schedule.observe_all(self._read_norms(), batch=batch)
+
+    def norms(self) -> list[float]:
+        """Current per-layer l2 norms of the masters (norm-only pass)."""
+        engine.sumsq(self.pack_table, self.sumsq)
+        return self._read_norms()

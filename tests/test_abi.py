@@ -1,0 +1,69 @@
+"""C-ABI checks that need no GPU: the in-tree library loads, exports every
+entry point include/adt.h declares, and validates arguments before touching
+the device (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "adt.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(adt_\w+)\s*\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2004_02297_b200 import _lib
+    return _lib
+
+
+def test_header_declares_the_expected_surface():
+    assert declared_functions() == sorted(
+        ["adt_abi_version", "adt_strerror", "adt_tile_count", "adt_pack", "adt_unpack", "adt_sumsq",
+         "adt_device_sm_count"])
+
+
+def test_library_exports_every_declared_symbol(lib):
+    handle = lib.load()
+    for name in declared_functions():
+        assert hasattr(handle, name), name
+    assert set(lib.EXPORTS) == set(declared_functions())
+    assert handle.adt_abi_version() == lib.ABI_VERSION
+
+
+def test_library_is_sm100a_only():
+    so = os.path.join(ROOT, "paper_2004_02297_b200", "libadt.so")
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_strerror_and_tile_count(lib):
+    assert lib.strerror(0) == "ok"
+    assert "round_to" in lib.strerror(lib.ADT_ERR_ROUND_TO)
+    segs = lib.segment_array([(0, 0, 0, 1), (16, 4097, 16, 3), (32, 4096, 12304, 4)])
+    assert lib.tile_count(segs, 3) == 0 + 2 + 1
+
+
+def test_validation_happens_before_any_device_work(lib):
+    h = lib.load()
+    bad_r = lib.segment_array([(16, 10, 0, 5)])
+    assert h.adt_pack(bad_r, 1, 16, None, None, None, None) == lib.ADT_ERR_ROUND_TO
+    with pytest.raises(ValueError):
+        lib.check(lib.ADT_ERR_ROUND_TO)
+    misaligned = lib.segment_array([(8, 10, 0, 2)])
+    assert h.adt_pack(misaligned, 1, 16, None, None, None, None) == lib.ADT_ERR_ALIGN
+    bad_off = lib.segment_array([(16, 10, 8, 2)])
+    assert h.adt_unpack(bad_off, 1, 16, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_unpack(lib.segment_array([(16, 10, 0, 2)]), 1, 0, None) == lib.ADT_ERR_ARG
+    assert h.adt_pack(None, -1, 0, None, None, None, None) == lib.ADT_ERR_ARG
+    # norm pass without scratch
+    assert h.adt_sumsq(lib.segment_array([(16, 10, 0, 2)]), 1, None, None, None, None) == lib.ADT_ERR_ARG

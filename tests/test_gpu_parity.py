@@ -1,0 +1,248 @@
+"""GPU parity: the sm_100a path vs the reference's golden vectors and the oracle.
+
+Bar (BASELINE.json north_star): packed bytes and unpacked words bit-exact,
+AWP widths identical, norms within 1e-6 relative (the reference's summation
+order lives in OpenBLAS ddot and is not pinned; ours is fixed, so we also
+assert run-to-run bit identity).
+"""
+
+import hashlib
+import io
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import weightpack_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+NORM_RTOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def adt():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2004_02297_b200 as adt
+    return adt
+
+
+def test_library_is_the_in_tree_build(adt):
+    from paper_2004_02297_b200 import _lib
+    lib = _lib.load()
+    assert lib._name.endswith("paper_2004_02297_b200/libadt.so")
+    from paper_2004_02297_b200 import engine
+    assert engine.sm_count() >= 100
+
+
+# ------------------------------------------------- golden (reference-run) vectors
+def test_pack_matches_golden(adt, golden_codec):
+    for c in golden_codec:
+        x = c["words"].view(np.float32)
+        want = c["payload"].tobytes()
+        for fn in (lambda: adt.pack(x, c["r"]), lambda: adt.pack_vectorized(x, c["r"]),
+                   lambda: adt.pack_parallel(x, c["r"], 3)):
+            blk = fn()
+            assert blk.payload == want, c["name"]
+            assert blk.weight_count == c["words"].size
+
+
+def test_unpack_matches_golden(adt, golden_codec):
+    for c in golden_codec:
+        blk = adt.PackedBlock(c["r"], c["words"].size, c["payload"].tobytes())
+        got = adt.unpack(blk)
+        assert isinstance(got, np.ndarray) and got.dtype == np.float32 and got.flags.writeable
+        assert np.array_equal(got.view(np.uint32), c["unpacked"]), c["name"]
+
+
+def test_device_payload_path(adt, golden_codec):
+    for c in golden_codec[::7]:
+        t = torch.from_numpy(c["words"].astype(np.uint32).view(np.float32).copy()).cuda()
+        blk = adt.pack(t, c["r"])
+        assert blk.on_device
+        assert blk.payload_bytes() == c["payload"].tobytes()
+        out = adt.unpack(blk)
+        assert out.is_cuda
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), c["unpacked"])
+
+
+def test_reference_kats(adt):
+    # test_codec.py:66-147
+    assert adt.pack([1.0], 3).payload == bytes([0x3F, 0x80, 0x00])
+    assert adt.pack([-2.0], 1).payload == bytes([0xC0])
+    assert adt.pack([np.float32(3.14159274)], 2).payload == bytes([0x40, 0x49])
+    m = np.array([0x11223344, 0x55667788, 0x99AABBCC, 0xDDEEFF00], np.uint32).view(np.float32).reshape(2, 2)
+    assert adt.pack(m, 1).payload == bytes([0x11, 0x55, 0x99, 0xDD])
+    assert adt.unpack(adt.PackedBlock(1, 1, bytes([0x3F]))).tolist() == [0.5]
+    assert adt.unpack(adt.PackedBlock(2, 1, bytes([0x40, 0x49]))).tolist() == [3.140625]
+    snan = np.array([0x7F800001], np.uint32).view(np.float32)
+    assert adt.unpack(adt.pack(snan, 3)).tolist() == [float("inf")]
+    e = adt.pack([], 2)
+    assert e.payload == b"" and e.weight_count == 0
+    assert adt.unpack(e).size == 0
+
+
+def test_errors_map_to_reference_types(adt):
+    for bad in (0, 5, 2.5):
+        with pytest.raises(ValueError):
+            adt.pack([1.0], bad)
+    with pytest.raises(ValueError):
+        adt.pack_parallel([1.0], 2, 0)
+    with pytest.raises(adt.MalformedBlock):
+        adt.PackedBlock(2, 3, bytes(5))
+
+
+def test_transposed_and_float64_inputs_follow_reference_cast(adt):
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((33, 17))
+    for x in (a, a.T, a.astype(np.float32).T):
+        for r in (1, 3, 4):
+            assert adt.pack(x, r).payload == O.pack_scalar(x, r)
+
+
+# ------------------------------------------------------------- laws at scale
+@pytest.mark.parametrize("r", [1, 2, 3, 4])
+def test_mask_law_and_idempotence_1e6(adt, r):
+    """test_acceptance.py:71-83 (criterion 1) and test_codec.py:163-171, on device."""
+    rng = np.random.default_rng(7)
+    words = np.concatenate([rng.integers(0, 1 << 32, 10**6, dtype=np.uint32),
+                            np.array(O.SPECIAL_WORDS, np.uint32)])
+    t = torch.from_numpy(words.view(np.float32).copy()).cuda()
+    blk = adt.pack(t, r)
+    assert blk.payload_bytes() == O.pack_vectorized(words.view(np.float32), r)
+    back = adt.unpack(blk)
+    want = torch.from_numpy((words & np.uint32(O.keep_mask(r))).view(np.int32).copy()).cuda()
+    assert torch.equal(back.view(torch.int32), want)
+    assert adt.pack(back, r) == blk
+
+
+LENGTHS = [0, 1, 3, 4, 5, 15, 16, 17, 4095, 4096, 4097, 8191, 8193, 12289, 65537, 100003]
+
+
+def test_multi_tensor_ragged_mixed_widths(adt):
+    rng = np.random.default_rng(11)
+    hosts = [rng.integers(0, 1 << 32, n, dtype=np.uint32).view(np.float32) for n in LENGTHS]
+    rs = [(i % 4) + 1 for i in range(len(hosts))]
+    devs = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+    packed, layout, ss = adt.pack_many(devs, rs, with_norms=True)
+    assert all(o % 16 == 0 for o in layout.offsets)
+    for i, (h, r) in enumerate(zip(hosts, rs)):
+        lo, hi = layout.span(i)
+        assert packed[lo:hi].cpu().numpy().tobytes() == O.pack_vectorized(h, r), (i, LENGTHS[i], r)
+    outs = adt.unpack_many(packed, layout)
+    for h, r, o in zip(hosts, rs, outs):
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+    blocks = adt.blocks_of(packed, layout)
+    assert [b.weight_count for b in blocks] == LENGTHS
+
+
+def test_multi_tensor_beyond_one_launch_table(adt):
+    """> 256 layers forces several launches; results must not change."""
+    rng = np.random.default_rng(5)
+    counts = [int(c) for c in rng.integers(0, 9000, 300)]
+    hosts = [(rng.standard_normal(n, dtype=np.float32) * np.float32(0.1)) for n in counts]
+    rs = [int(x) for x in rng.integers(1, 5, len(counts))]
+    devs = [torch.from_numpy(h).cuda() for h in hosts]
+    packed, layout, ss = adt.pack_many(devs, rs, with_norms=True)
+    ss = ss.cpu().numpy()
+    for i, (h, r) in enumerate(zip(hosts, rs)):
+        lo, hi = layout.span(i)
+        assert packed[lo:hi].cpu().numpy().tobytes() == O.pack_vectorized(h, r)
+        assert ss[i] == pytest.approx(O.sumsq(h), rel=1e-12, abs=0)
+
+
+# -------------------------------------------------------------------- norms
+def test_norms_match_golden(adt, golden_norms):
+    for x, want in golden_norms:
+        got = adt.l2_norm(x)
+        if want == 0.0:
+            assert got == 0.0
+        else:
+            assert abs(got - want) <= NORM_RTOL * want
+
+
+def test_fused_norm_bit_identical_across_runs_and_widths(adt):
+    rng = np.random.default_rng(0)
+    hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in (1000, 4096 * 37 + 5, 1 << 20)]
+    devs = [torch.from_numpy(h).cuda() for h in hosts]
+    runs = []
+    for rs in ([1, 2, 3], [4, 4, 4], [3, 1, 2]):
+        _, _, ss = adt.pack_many(devs, rs, with_norms=True)
+        runs.append(ss.cpu().numpy().tobytes())
+    assert len(set(runs)) == 1
+    ss = np.frombuffer(runs[0], np.float64)
+    for h, s in zip(hosts, ss):
+        assert math.sqrt(s) == pytest.approx(O.l2_norm(h), rel=1e-12)
+
+
+# ---------------------------------------------------------------- container
+def test_container_roundtrip_device_block(adt):
+    t = torch.randn(1001, device="cuda")
+    blk = adt.pack(t, 3)
+    buf = io.BytesIO()
+    n = adt.write_stream(buf, blk)
+    assert n == 14 + 3003
+    buf.seek(0)
+    back = adt.read_stream(buf)
+    assert back == blk
+    assert buf.getvalue() == O.write_container(3, 1001, O.pack_vectorized(t.cpu().numpy(), 3))
+
+
+# --------------------------------------------------------- pinned zero-copy
+def test_unpack_from_pinned_host(adt):
+    from paper_2004_02297_b200 import engine
+    rng = np.random.default_rng(2)
+    counts, rs = [5000, 4096, 77], [2, 3, 1]
+    hosts = [rng.integers(0, 1 << 32, n, dtype=np.uint32).view(np.float32) for n in counts]
+    layout = adt.PackedLayout.plan(counts, rs)
+    buf = np.zeros(layout.nbytes, np.uint8)
+    for i, (h, r) in enumerate(zip(hosts, rs)):
+        lo, hi = layout.span(i)
+        buf[lo:hi] = np.frombuffer(O.pack_vectorized(h, r), np.uint8)
+    pinned = torch.from_numpy(buf).pin_memory()
+    outs = [torch.empty(n, dtype=torch.float32, device="cuda") for n in counts]
+    engine.unpack(engine.SegmentTable(outs, layout), pinned)
+    torch.cuda.synchronize()
+    for h, r, o in zip(hosts, rs, outs):
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+
+
+# ------------------------------------------------------- AWP flow (config 1)
+def test_lenet_awp_walk_matches_reference(adt, golden_lenet):
+    """200 batches of the seeded LeNet walk through
+    WeightSync (fused norms, repack on escalation) vs the reference's run."""
+    steps = int(golden_lenet["steps"])
+    walk = list(O.lenet_walk(steps, seed=7))
+    L = len(walk[0][1])
+    cfg = adt.PrecisionConfig(threshold=-2e-3, interval=int(golden_lenet["interval"]), step_bits=8, initial_bits=8)
+    ctl = adt.PrecisionController(L, cfg)
+    masters = [torch.from_numpy(w.copy()).cuda() for w in walk[0][1]]
+    sync = adt.WeightSync(masters, ctl)
+    trace = []
+    for t in range(steps):
+        for m, w in zip(masters, walk[t][1]):
+            m.copy_(torch.from_numpy(w))
+        res = sync.step(batch=t)
+        trace += res.trace
+        assert res.round_tos == list(golden_lenet["widths"][t]), t
+        lo_hi = [sync.layout.span(i) for i in range(L)]
+        host_packed = sync.packed.cpu().numpy()
+        for i in range(L):
+            pay = host_packed[lo_hi[i][0]:lo_hi[i][1]].tobytes()
+            assert hashlib.sha256(pay).digest() == golden_lenet["payload_sha"][t, i].tobytes(), (t, i)
+            rep = sync.replicas[i].cpu().numpy()
+            assert hashlib.sha256(rep.tobytes()).digest() == golden_lenet["unpacked_sha"][t, i].tobytes(), (t, i)
+    for m, w in zip(masters, walk[steps][1]):
+        m.copy_(torch.from_numpy(w))
+    trace += sync.observe_final(batch=steps - 1)
+    assert len(trace) == steps * L
+    for k, (b, layer, norm, delta, counter, bits) in enumerate(trace):
+        t, i = divmod(k, L)
+        assert (b, layer) == (t, i)
+        assert bits == golden_lenet["bits"][t, i] and counter == golden_lenet["counter"][t, i], (t, i)
+        assert abs(norm - golden_lenet["norms"][t, i]) <= NORM_RTOL * golden_lenet["norms"][t, i]
+        gd = golden_lenet["delta"][t, i]
+        assert (delta is None and math.isnan(gd)) or abs(delta - gd) <= 1e-6 * max(abs(gd), 1e-3)
+
