@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <limits.h>
+#include <stdlib.h>
 
 #include "adt.h"
 
@@ -317,10 +318,79 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
     }
 }
 
+}  // namespace
+
+#include "adt_tma.cuh"
+
+namespace {
+
 // ----------------------------------------------------------------- host side
 enum class Pass { Pack, PackNorm, Norm, Unpack };
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? ADT_OK : ADT_ERR_CUDA_BASE - static_cast<int>(e); }
+
+// Kernel family: the persistent TMA pipeline (default) or the one-tile-per-CTA
+// register kernels (ADT_KERNEL=simple), kept for A/B measurements.
+bool use_simple_kernels() {
+    static const int v = [] {
+        const char *e = getenv("ADT_KERNEL");
+        return (e != nullptr && e[0] == 's') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
+int sm_count_cached(int *out) {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return ADT_ERR_NO_DEVICE;
+    if (dev >= 0 && dev < 64 && cache[dev] > 0) { *out = cache[dev]; return ADT_OK; }
+    int v = 0;
+    e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (dev >= 0 && dev < 64) cache[dev] = v;
+    *out = v;
+    return ADT_OK;
+}
+
+template <typename K>
+cudaError_t allow_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
+template <int MAXSEG>
+int launch_tma(Pass pass, const Table<MAXSEG> &T, uint32_t ntiles, cudaStream_t stream) {
+    int sms = 0;
+    const int st = sm_count_cached(&sms);
+    if (st != ADT_OK) return st;
+    const uint32_t grid = min(ntiles, static_cast<uint32_t>(2 * sms));
+    const size_t smem = sizeof(tma::Smem);
+    cudaError_t e = cudaSuccess;
+    switch (pass) {
+        case Pass::Pack: {
+            auto k = tma::adt_pack_tma_kernel<MAXSEG, false, true>;
+            e = allow_smem(k, smem);
+            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+        } break;
+        case Pass::PackNorm: {
+            auto k = tma::adt_pack_tma_kernel<MAXSEG, true, true>;
+            e = allow_smem(k, smem);
+            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+        } break;
+        case Pass::Norm: {
+            auto k = tma::adt_pack_tma_kernel<MAXSEG, true, false>;
+            e = allow_smem(k, smem);
+            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+        } break;
+        case Pass::Unpack: {
+            auto k = tma::adt_unpack_tma_kernel<MAXSEG>;
+            e = allow_smem(k, smem);
+            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+        } break;
+    }
+    if (e != cudaSuccess) return cuda_status(e);
+    return cuda_status(cudaGetLastError());
+}
 
 int validate(const adt_segment *segs, int nseg, const void *packed, bool need_packed) {
     if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
@@ -369,6 +439,7 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pi
             return cuda_status(cudaMemsetAsync(seg_sumsq, 0, sizeof(double) * nseg, stream));
         return ADT_OK;
     }
+    if (!use_simple_kernels()) return launch_tma<MAXSEG>(pass, T, ntiles, stream);
     const dim3 grid(ntiles), block(kThreads);
     switch (pass) {
         case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T); break;
@@ -466,17 +537,7 @@ int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *tile
 
 int adt_device_sm_count(int *sm_count) {
     if (sm_count == nullptr) return ADT_ERR_ARG;
-    static int cache[64] = {0};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return ADT_ERR_NO_DEVICE;
-    if (dev >= 0 && dev < 64 && cache[dev] > 0) { *sm_count = cache[dev]; return ADT_OK; }
-    int v = 0;
-    e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return cuda_status(e);
-    if (dev >= 0 && dev < 64) cache[dev] = v;
-    *sm_count = v;
-    return ADT_OK;
+    return sm_count_cached(sm_count);
 }
 
 }  // extern "C"

@@ -88,3 +88,15 @@ def test_lenet_walk_matches_golden(golden_lenet):
             b = c.observe_layer(i, float(golden_lenet["norms"][t, i]))
             assert b == golden_lenet["bits"][t, i]
             assert c.counter[i] == golden_lenet["counter"][t, i]
+
+
+def test_c_oracle_matches_golden(golden_codec, golden_norms):
+    from oracle import c_oracle as C
+    for c in golden_codec:
+        x = c["words"].view(np.float32)
+        assert C.pack(x, c["r"]) == c["payload"].tobytes(), c["name"]
+        got = C.unpack(c["payload"].tobytes(), c["words"].size, c["r"])
+        assert np.array_equal(got.view(np.uint32), c["unpacked"]), c["name"]
+    for x, want in golden_norms:
+        got = math.sqrt(C.sumsq(x))
+        assert got == pytest.approx(want, rel=1e-12) or got == want == 0.0
