@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--quiet-extra", action="store_true", help="skip per-kernel event timing")
+    ap.add_argument("--no-norm", action="store_true", help="A/B only: pack without the fused l2-norm")
     return ap.parse_args()
 
 
@@ -237,7 +238,7 @@ def main_ours(args):
         sumsq = torch.empty(L, dtype=torch.float64, device=dev)
 
         def do_pack():
-            engine.pack(ptab, packed, sumsq)
+            engine.pack(ptab, packed, None if args.no_norm else sumsq)
 
         def do_unpack():
             engine.unpack(utab, packed)

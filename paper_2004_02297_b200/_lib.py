@@ -13,7 +13,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libadt.so")
+# ADT_LIB may point at an in-tree build variant (scripts/build_variants.sh) for A/B runs.
+LIB_PATH = os.environ.get("ADT_LIB") or os.path.join(PKG, "libadt.so")
 
 ADT_OK = 0
 ADT_ERR_ROUND_TO = -1

@@ -363,7 +363,7 @@ int launch_tma(Pass pass, const Table<MAXSEG> &T, uint32_t ntiles, cudaStream_t 
     int sms = 0;
     const int st = sm_count_cached(&sms);
     if (st != ADT_OK) return st;
-    const uint32_t grid = min(ntiles, static_cast<uint32_t>(2 * sms));
+    const uint32_t grid = min(ntiles, static_cast<uint32_t>(tma::kCtasPerSm * sms));
     const size_t smem = sizeof(tma::Smem);
     cudaError_t e = cudaSuccess;
     switch (pass) {

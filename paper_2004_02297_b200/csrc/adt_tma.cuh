@@ -20,7 +20,14 @@ namespace tma {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kBlock = kConsumers + 32;
-constexpr int kStages = 4;
+#ifndef ADT_TMA_STAGES
+#define ADT_TMA_STAGES 4
+#endif
+#ifndef ADT_TMA_CTAS
+#define ADT_TMA_CTAS 2
+#endif
+constexpr int kStages = ADT_TMA_STAGES;   // ring depth per CTA
+constexpr int kCtasPerSm = ADT_TMA_CTAS;   // persistent CTAs per SM
 constexpr int kGroups = kTile / 4;                       // float4 groups per tile (1024)
 constexpr int kWarpGroups = kGroups / kConsumerWarps;    // 128
 constexpr int kStageBytes = kTile * 4;                   // one FP32 tile (>= any packed tile)
@@ -31,6 +38,7 @@ struct Smem {
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     double red[2][kConsumerWarps];
+    unsigned char fin[256];                              // layers this CTA finalises (<= kLargeSeg)
 };
 
 __device__ __forceinline__ uint32_t saddr(const void *p) {
@@ -78,35 +86,64 @@ __device__ __forceinline__ TileInfo tile_info(const Table<MAXSEG> &T, uint32_t t
     return ti;
 }
 
-// Per-tile norm epilogue inside the persistent loop (consumer threads only).
-template <int MAXSEG>
-__device__ __forceinline__ void norm_tile(const Table<MAXSEG> &T, Smem &S, int s, uint32_t tile, int k, double acc) {
+// Per-tile norm partial inside the persistent loop (consumer threads only):
+// a fixed-order warp + CTA reduction, one plain store per tile. No fence and
+// no atomic here — those would put an L2 round trip behind every tile.
+__device__ __forceinline__ void norm_tile(double *partials, Smem &S, uint32_t tile, int k, double acc) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
     if (lane == 0) S.red[k & 1][warp] = acc;
     consumer_sync(1);
-    if (warp != 0) return;
-    int last = 0;
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         double part = 0.0;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) part += S.red[k & 1][w];
-        T.partials[tile] = part;
-        __threadfence();
-        const uint32_t ntiles = T.tile_begin[s + 1] - T.tile_begin[s];
-        last = (atomicAdd(&T.counters[s], 1u) == ntiles - 1);
+        partials[tile] = part;
     }
-    last = __shfl_sync(0xFFFFFFFFu, last, 0);
-    if (!last) return;
-    __threadfence();
-    double a = 0.0;
-    for (uint32_t i = T.tile_begin[s] + lane; i < T.tile_begin[s + 1]; i += 32) a += __ldcg(&T.partials[i]);
+}
+
+// Tiles t = b + k*G (k >= 0) that fall in [lo, hi).
+__device__ __forceinline__ uint32_t my_tiles_in(uint32_t lo, uint32_t hi, uint32_t b, uint32_t G) {
+    auto below = [&](uint32_t x) -> uint32_t { return x > b ? (x - b - 1) / G + 1 : 0u; };
+    return below(hi) - below(lo);
+}
+
+// End of a CTA's tile loop: ONE fence, then per layer one atomic adding the
+// number of this CTA's tiles in it; the CTA that completes a layer sums its
+// tile partials in tile order (fixed, independent of which CTA did which tile).
+template <int MAXSEG>
+__device__ __forceinline__ void norm_finish(const Table<MAXSEG> &T, Smem &S) {
+    consumer_sync(1);
+    if (threadIdx.x == 0) __threadfence();  // this CTA's partial stores (all by thread 0)
+    consumer_sync(1);
+    for (int s = threadIdx.x; s < T.nseg; s += kConsumers) {
+        const uint32_t lo = T.tile_begin[s], hi = T.tile_begin[s + 1];
+        const uint32_t mine = my_tiles_in(lo, hi, blockIdx.x, gridDim.x);
+        unsigned char fin = 0;
+        if (mine) fin = (atomicAdd(&T.counters[s], mine) + mine == hi - lo);
+        S.fin[s] = fin;
+    }
+    consumer_sync(1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int s = 0; s < T.nseg; ++s) {
+        if (!S.fin[s]) continue;  // uniform: every consumer reads the same flag
+        __threadfence();
+        double a = 0.0;
+        for (uint32_t i = T.tile_begin[s] + threadIdx.x; i < T.tile_begin[s + 1]; i += kConsumers)
+            a += __ldcg(&T.partials[i]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
-    if (lane == 0) {
-        T.seg_sumsq[s] = a;
-        T.counters[s] = 0u;
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
+        if (lane == 0) S.red[0][warp] = a;
+        consumer_sync(1);
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+#pragma unroll
+            for (int w = 0; w < kConsumerWarps; ++w) tot += S.red[0][w];
+            T.seg_sumsq[s] = tot;
+            T.counters[s] = 0u;  // re-arm for the next stream-ordered call
+        }
+        consumer_sync(1);
     }
 }
 
@@ -121,7 +158,7 @@ __device__ __forceinline__ void warp_copy_out(const uint32_t *ws, uint8_t *dst, 
 }
 
 template <int MAXSEG, bool NORM, bool WRITE>
-__global__ void __launch_bounds__(kBlock, 2)
+__global__ void __launch_bounds__(kBlock, kCtasPerSm)
 adt_pack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
@@ -236,12 +273,13 @@ adt_pack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
                 __syncwarp();
             }
         }
-        if (NORM) norm_tile(T, S, ti.s, tile, k, acc);
+        if (NORM) norm_tile(T.partials, S, tile, k, acc);
     }
+    if (NORM) norm_finish(T, S);
 }
 
 template <int MAXSEG>
-__global__ void __launch_bounds__(kBlock, 2)
+__global__ void __launch_bounds__(kBlock, kCtasPerSm)
 adt_unpack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
