@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 1
+#define ADT_ABI_VERSION 2
 
 /* status codes */
 #define ADT_OK 0
@@ -70,12 +70,12 @@ int adt_tile_count(const adt_segment *segs, int nseg, uint64_t *ntiles);
  * fuses precision.l2_norm (precision.py:25-28): seg_sumsq[l] receives the float64
  * sum of squares of layer l (sqrt it for the norm), reduced in a fixed order so
  * results are bit-identical run to run.  When seg_sumsq != NULL, `tile_partials`
- * (adt_tile_count doubles) and `seg_counters` (nseg uint32, zero-initialised once
- * by the caller; the kernel leaves them zero) are required scratch.
+ * (adt_tile_count doubles) is required scratch: the pack pass stores one float64
+ * partial per 4096-weight tile and a small finalize kernel (launched behind it as
+ * a programmatic dependent) sums each layer's partials in tile order.
  */
 int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed,
-             double *seg_sumsq, double *tile_partials, uint32_t *seg_counters,
-             void *stream);
+             double *seg_sumsq, double *tile_partials, void *stream);
 
 /*
  * Multi-tensor unpack.  Replaces codec.unpack (codec.py:183-197) applied to
@@ -93,7 +93,7 @@ int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *s
  * norm is not fused into a pack (the last observation of a run, training.py:246-254).
  */
 int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq,
-              double *tile_partials, uint32_t *seg_counters, void *stream);
+              double *tile_partials, void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

@@ -23,7 +23,7 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_tile_count", "adt_pack", "adt_unpack",
            "adt_sumsq", "adt_device_sm_count")
@@ -77,11 +77,11 @@ def load() -> ctypes.CDLL:
         lib.adt_tile_count.restype = ctypes.c_int
         lib.adt_tile_count.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_uint64)]
         lib.adt_pack.restype = ctypes.c_int
-        lib.adt_pack.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp, vp]
+        lib.adt_pack.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack.restype = ctypes.c_int
         lib.adt_unpack.argtypes = [seg_p, ctypes.c_int, vp, vp]
         lib.adt_sumsq.restype = ctypes.c_int
-        lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
+        lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_device_sm_count.restype = ctypes.c_int
         lib.adt_device_sm_count.argtypes = [P(ctypes.c_int)]
         if lib.adt_abi_version() != ABI_VERSION:

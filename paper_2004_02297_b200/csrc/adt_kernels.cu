@@ -40,7 +40,6 @@ struct Table {
     uint8_t *packed_out;        // pack destination
     double *seg_sumsq;          // per-layer result (chunk-relative)
     double *partials;           // per-tile scratch (chunk-relative)
-    uint32_t *counters;         // per-layer completion counters (chunk-relative)
     int nseg;
     uint32_t tile_begin[MAXSEG + 1];
     uint64_t count[MAXSEG];
@@ -118,9 +117,21 @@ __device__ __forceinline__ int find_segment(const Table<MAXSEG> &T, uint32_t til
     return lo;
 }
 
+// float32 -> float64 widening on the integer pipe. cvt.f64.f32 (F2F) issues on
+// the XU pipe, which ncu showed as the pack+norm bottleneck (58.6% XU, see
+// profiles/r01_v1_*); rebuilding the double from the float's bits is exact for
+// normal numbers, and zeros / subnormals / inf / NaN (rare) fall back to F2F.
+__device__ __forceinline__ double widen(uint32_t w) {
+    const uint32_t a = w & 0x7FFFFFFFu;           // |x| (the square ignores the sign)
+    if (a - 0x00800000u < 0x7F000000u) {          // 0 < exponent < 255
+        return __hiloint2double(static_cast<int>((a >> 3) + (896u << 20)), static_cast<int>(a << 29));
+    }
+    return a == 0u ? 0.0 : static_cast<double>(__uint_as_float(a));
+}
+
 __device__ __forceinline__ double sq_acc(double acc, uint32_t w) {
-    const double d = static_cast<double>(__uint_as_float(w));  // exact widening
-    return fma(d, d, acc);                                    // exact square, rounded add
+    const double d = widen(w);  // exact
+    return fma(d, d, acc);      // exact square, rounded add
 }
 
 // Fixed-order CTA reduction; result valid in thread 0.
@@ -137,37 +148,29 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
     return s;
 }
 
-// Tile partial -> (last CTA of the layer) fixed-order layer total.
-template <int MAXSEG>
-__device__ __forceinline__ void norm_epilogue(const Table<MAXSEG> &T, int s, uint32_t tile, double acc) {
+// Tile partial: fixed-order CTA reduction, one plain store. The per-layer
+// totals are summed by adt_norm_finalize_kernel (no fences or atomics here:
+// a per-CTA fence + L2 atomic kept every CTA resident ~1 us longer).
+__device__ __forceinline__ void tile_partial(double *partials, uint32_t tile, double acc) {
     __shared__ double red[kThreads / 32];
-    __shared__ int last;
     const double part = block_sum(acc, red);
-    if (threadIdx.x == 0) {
-        T.partials[tile] = part;
-        __threadfence();
-        const uint32_t ntiles = T.tile_begin[s + 1] - T.tile_begin[s];
-        last = (atomicAdd(&T.counters[s], 1u) == ntiles - 1);
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    double a = 0.0;
-    for (uint32_t i = T.tile_begin[s] + threadIdx.x; i < T.tile_begin[s + 1]; i += kThreads)
-        a += __ldcg(&T.partials[i]);
-    __syncthreads();  // red reuse
-    const double total = block_sum(a, red);
-    if (threadIdx.x == 0) {
-        T.seg_sumsq[s] = total;
-        T.counters[s] = 0u;  // re-arm for the next stream-ordered call
-    }
+    if (threadIdx.x == 0) partials[tile] = part;
 }
 
+// Per layer (one CTA each): sum its tile partials in tile order -> seg_sumsq.
+// Launched right behind the pack pass (programmatic dependent launch).
 template <int MAXSEG>
-__device__ __forceinline__ void zero_empty_layers(const Table<MAXSEG> &T) {
-    if (blockIdx.x != 0) return;
-    for (int i = threadIdx.x; i < T.nseg; i += kThreads)
-        if (T.count[i] == 0) T.seg_sumsq[i] = 0.0;
+__global__ void __launch_bounds__(kThreads)
+adt_norm_finalize_kernel(const __grid_constant__ Table<MAXSEG> T) {
+#if __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+    __shared__ double red[kThreads / 32];
+    const int s = blockIdx.x;
+    double a = 0.0;
+    for (uint32_t i = T.tile_begin[s] + threadIdx.x; i < T.tile_begin[s + 1]; i += kThreads) a += T.partials[i];
+    const double total = block_sum(a, red);
+    if (threadIdx.x == 0) T.seg_sumsq[s] = total;  // 0.0 for empty layers
 }
 
 // ---------------------------------------------------------------- pack pass
@@ -201,7 +204,6 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
         }
     }
 
-    if (NORM) zero_empty_layers(T);
     double acc = 0.0;
     if (NORM) {
 #pragma unroll
@@ -250,7 +252,7 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
         }
     }
 
-    if (NORM) norm_epilogue(T, s, tile, acc);
+    if (NORM) tile_partial(T.partials, tile, acc);
 }
 
 // -------------------------------------------------------------- unpack pass
@@ -329,12 +331,13 @@ enum class Pass { Pack, PackNorm, Norm, Unpack };
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? ADT_OK : ADT_ERR_CUDA_BASE - static_cast<int>(e); }
 
-// Kernel family: the persistent TMA pipeline (default) or the one-tile-per-CTA
-// register kernels (ADT_KERNEL=simple), kept for A/B measurements.
-bool use_simple_kernels() {
+// Kernel family: one-tile-per-CTA register kernels (default; measured fastest,
+// profiles/r01_*) or the persistent TMA bulk-copy pipeline (ADT_KERNEL=tma),
+// kept for A/B measurements.
+bool use_tma_kernels() {
     static const int v = [] {
         const char *e = getenv("ADT_KERNEL");
-        return (e != nullptr && e[0] == 's') ? 1 : 0;
+        return (e != nullptr && e[0] == 't') ? 1 : 0;
     }();
     return v != 0;
 }
@@ -359,37 +362,49 @@ cudaError_t allow_smem(K kernel, size_t bytes) {
 }
 
 template <int MAXSEG>
-int launch_tma(Pass pass, const Table<MAXSEG> &T, uint32_t ntiles, cudaStream_t stream) {
+cudaError_t launch_tma(Pass pass, const Table<MAXSEG> &T, uint32_t ntiles, cudaStream_t stream) {
     int sms = 0;
-    const int st = sm_count_cached(&sms);
-    if (st != ADT_OK) return st;
+    if (sm_count_cached(&sms) != ADT_OK) return cudaErrorNoDevice;
     const uint32_t grid = min(ntiles, static_cast<uint32_t>(tma::kCtasPerSm * sms));
     const size_t smem = sizeof(tma::Smem);
     cudaError_t e = cudaSuccess;
     switch (pass) {
         case Pass::Pack: {
             auto k = tma::adt_pack_tma_kernel<MAXSEG, false, true>;
-            e = allow_smem(k, smem);
-            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+            if ((e = allow_smem(k, smem)) == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
         } break;
         case Pass::PackNorm: {
             auto k = tma::adt_pack_tma_kernel<MAXSEG, true, true>;
-            e = allow_smem(k, smem);
-            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+            if ((e = allow_smem(k, smem)) == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
         } break;
         case Pass::Norm: {
             auto k = tma::adt_pack_tma_kernel<MAXSEG, true, false>;
-            e = allow_smem(k, smem);
-            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+            if ((e = allow_smem(k, smem)) == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
         } break;
         case Pass::Unpack: {
             auto k = tma::adt_unpack_tma_kernel<MAXSEG>;
-            e = allow_smem(k, smem);
-            if (e == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
+            if ((e = allow_smem(k, smem)) == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
         } break;
     }
-    if (e != cudaSuccess) return cuda_status(e);
-    return cuda_status(cudaGetLastError());
+    return e;
+}
+
+// Finalize launched as a programmatic dependent of the pack pass: its launch
+// is processed while the pack drains; griddepcontrol.wait in the kernel
+// orders its reads after the pack's partial stores.
+template <int MAXSEG>
+cudaError_t launch_finalize(const Table<MAXSEG> &T, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(T.nseg);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, adt_norm_finalize_kernel<MAXSEG>, T);
 }
 
 int validate(const adt_segment *segs, int nseg, const void *packed, bool need_packed) {
@@ -415,14 +430,12 @@ int validate(const adt_segment *segs, int nseg, const void *packed, bool need_pa
 
 template <int MAXSEG>
 int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
-                 double *seg_sumsq, double *partials, uint32_t *counters, uint32_t ntiles,
-                 cudaStream_t stream) {
+                 double *seg_sumsq, double *partials, uint32_t ntiles, cudaStream_t stream) {
     Table<MAXSEG> T;
     T.packed_in = pin;
     T.packed_out = pout;
     T.seg_sumsq = seg_sumsq;
     T.partials = partials;
-    T.counters = counters;
     T.nseg = nseg;
     uint32_t acc = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -434,30 +447,33 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pi
         T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
     }
     T.tile_begin[nseg] = acc;
-    if (ntiles == 0) {
-        if (pass == Pass::PackNorm || pass == Pass::Norm)
-            return cuda_status(cudaMemsetAsync(seg_sumsq, 0, sizeof(double) * nseg, stream));
-        return ADT_OK;
+    const bool norm = pass == Pass::PackNorm || pass == Pass::Norm;
+    cudaError_t e = cudaSuccess;
+    if (ntiles > 0) {
+        if (use_tma_kernels()) {
+            e = launch_tma<MAXSEG>(pass, T, ntiles, stream);
+        } else {
+            const dim3 grid(ntiles), block(kThreads);
+            switch (pass) {
+                case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T); break;
+                case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T); break;
+                case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T); break;
+                case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T); break;
+            }
+            e = cudaGetLastError();
+        }
     }
-    if (!use_simple_kernels()) return launch_tma<MAXSEG>(pass, T, ntiles, stream);
-    const dim3 grid(ntiles), block(kThreads);
-    switch (pass) {
-        case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T); break;
-        case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T); break;
-        case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T); break;
-        case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T); break;
-    }
-    return cuda_status(cudaGetLastError());
+    if (e == cudaSuccess && norm && nseg > 0) e = launch_finalize<MAXSEG>(T, stream);
+    return cuda_status(e);
 }
 
 constexpr int kSmallSeg = 16;
 constexpr int kLargeSeg = 256;
 
 int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
-        double *seg_sumsq, double *partials, uint32_t *counters, void *stream_v) {
+        double *seg_sumsq, double *partials, void *stream_v) {
     const bool norm = pass == Pass::PackNorm || pass == Pass::Norm;
-    if (norm && nseg > 0 && (seg_sumsq == nullptr || partials == nullptr || counters == nullptr))
-        return ADT_ERR_ARG;
+    if (norm && nseg > 0 && (seg_sumsq == nullptr || partials == nullptr)) return ADT_ERR_ARG;
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
     uint64_t partial_base = 0;
     int base = 0;
@@ -473,10 +489,9 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_
         }
         double *ss = norm ? seg_sumsq + base : nullptr;
         double *pp = norm ? partials + partial_base : nullptr;
-        uint32_t *cc = norm ? counters + base : nullptr;
         const int st = cnt <= kSmallSeg
-            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, pin, pout, ss, pp, cc, static_cast<uint32_t>(tiles), stream)
-            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, pin, pout, ss, pp, cc, static_cast<uint32_t>(tiles), stream);
+            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), stream)
+            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), stream);
         if (st != ADT_OK) return st;
         partial_base += tiles;
         base += cnt;
@@ -514,25 +529,24 @@ int adt_tile_count(const adt_segment *segs, int nseg, uint64_t *ntiles) {
 }
 
 int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed, double *seg_sumsq,
-             double *tile_partials, uint32_t *seg_counters, void *stream) {
+             double *tile_partials, void *stream) {
     const int v = validate(segs, nseg, packed, true);
     if (v != ADT_OK) return v;
     return run(seg_sumsq ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, packed, seg_sumsq,
-               tile_partials, seg_counters, stream);
+               tile_partials, stream);
 }
 
 int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *stream) {
     const int v = validate(segs, nseg, packed, true);
     if (v != ADT_OK) return v;
-    return run(Pass::Unpack, segs, nseg, packed, nullptr, nullptr, nullptr, nullptr, stream);
+    return run(Pass::Unpack, segs, nseg, packed, nullptr, nullptr, nullptr, stream);
 }
 
-int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *tile_partials,
-              uint32_t *seg_counters, void *stream) {
+int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *tile_partials, void *stream) {
     const int v = validate(segs, nseg, nullptr, false);
     if (v != ADT_OK) return v;
     if (nseg > 0 && seg_sumsq == nullptr) return ADT_ERR_ARG;
-    return run(Pass::Norm, segs, nseg, nullptr, nullptr, seg_sumsq, tile_partials, seg_counters, stream);
+    return run(Pass::Norm, segs, nseg, nullptr, nullptr, seg_sumsq, tile_partials, stream);
 }
 
 int adt_device_sm_count(int *sm_count) {

@@ -12,7 +12,8 @@
 // lane l handles groups 128w + l + 32j, j = 0..3 (coalesced at every width).
 // r = 3 (12 bytes per group) and ragged tails go through a per-warp staging
 // buffer so global stores stay 16-byte vectors, synchronised by __syncwarp
-// only. The fused float64 norm uses one 256-thread named barrier per tile.
+// only. The fused float64 norm uses one 256-thread named barrier per tile and
+// stores one partial per tile (summed by adt_norm_finalize_kernel).
 #pragma once
 
 namespace tma {
@@ -38,7 +39,6 @@ struct Smem {
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     double red[2][kConsumerWarps];
-    unsigned char fin[256];                              // layers this CTA finalises (<= kLargeSeg)
 };
 
 __device__ __forceinline__ uint32_t saddr(const void *p) {
@@ -103,50 +103,6 @@ __device__ __forceinline__ void norm_tile(double *partials, Smem &S, uint32_t ti
     }
 }
 
-// Tiles t = b + k*G (k >= 0) that fall in [lo, hi).
-__device__ __forceinline__ uint32_t my_tiles_in(uint32_t lo, uint32_t hi, uint32_t b, uint32_t G) {
-    auto below = [&](uint32_t x) -> uint32_t { return x > b ? (x - b - 1) / G + 1 : 0u; };
-    return below(hi) - below(lo);
-}
-
-// End of a CTA's tile loop: ONE fence, then per layer one atomic adding the
-// number of this CTA's tiles in it; the CTA that completes a layer sums its
-// tile partials in tile order (fixed, independent of which CTA did which tile).
-template <int MAXSEG>
-__device__ __forceinline__ void norm_finish(const Table<MAXSEG> &T, Smem &S) {
-    consumer_sync(1);
-    if (threadIdx.x == 0) __threadfence();  // this CTA's partial stores (all by thread 0)
-    consumer_sync(1);
-    for (int s = threadIdx.x; s < T.nseg; s += kConsumers) {
-        const uint32_t lo = T.tile_begin[s], hi = T.tile_begin[s + 1];
-        const uint32_t mine = my_tiles_in(lo, hi, blockIdx.x, gridDim.x);
-        unsigned char fin = 0;
-        if (mine) fin = (atomicAdd(&T.counters[s], mine) + mine == hi - lo);
-        S.fin[s] = fin;
-    }
-    consumer_sync(1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int s = 0; s < T.nseg; ++s) {
-        if (!S.fin[s]) continue;  // uniform: every consumer reads the same flag
-        __threadfence();
-        double a = 0.0;
-        for (uint32_t i = T.tile_begin[s] + threadIdx.x; i < T.tile_begin[s + 1]; i += kConsumers)
-            a += __ldcg(&T.partials[i]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
-        if (lane == 0) S.red[0][warp] = a;
-        consumer_sync(1);
-        if (threadIdx.x == 0) {
-            double tot = 0.0;
-#pragma unroll
-            for (int w = 0; w < kConsumerWarps; ++w) tot += S.red[0][w];
-            T.seg_sumsq[s] = tot;
-            T.counters[s] = 0u;  // re-arm for the next stream-ordered call
-        }
-        consumer_sync(1);
-    }
-}
-
 // Copy `nbytes` (clipped to the warp's span) from the warp's staging buffer.
 __device__ __forceinline__ void warp_copy_out(const uint32_t *ws, uint8_t *dst, uint32_t nbytes, int lane) {
     const uint32_t n16 = nbytes / 16;
@@ -193,9 +149,6 @@ adt_pack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     }
 
     // -------------------------------------------------- consumers
-    if (NORM && blockIdx.x == 0)
-        for (int i = threadIdx.x; i < T.nseg; i += kConsumers)
-            if (T.count[i] == 0) T.seg_sumsq[i] = 0.0;
     uint32_t *ws = S.wstage[warp];
     int k = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
@@ -275,7 +228,6 @@ adt_pack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
         }
         if (NORM) norm_tile(T.partials, S, tile, k, acc);
     }
-    if (NORM) norm_finish(T, S);
 }
 
 template <int MAXSEG>

@@ -64,20 +64,18 @@ class SegmentTable:
 
 
 class _Scratch:
-    """Per (device, stream) norm scratch: tile partials + zeroed layer counters."""
+    """Per (device, stream) norm scratch: one float64 partial per tile."""
 
     _lock = threading.Lock()
     _cache: dict = {}
 
     @classmethod
-    def get(cls, device: torch.device, stream: int, ntiles: int, nseg: int):
+    def get(cls, device: torch.device, stream: int, ntiles: int) -> torch.Tensor:
         key = (device.index, stream)
         with cls._lock:
             cur = cls._cache.get(key)
-            if cur is None or cur[0].numel() < max(1, ntiles) or cur[1].numel() < max(1, nseg):
-                parts = torch.empty(max(1, ntiles, cur[0].numel() if cur else 0), dtype=torch.float64, device=device)
-                ctr = torch.zeros(max(1, nseg, cur[1].numel() if cur else 0), dtype=torch.int32, device=device)
-                cur = (parts, ctr)
+            if cur is None or cur.numel() < max(1, ntiles):
+                cur = torch.empty(max(1, ntiles), dtype=torch.float64, device=device)
                 cls._cache[key] = cur
             return cur
 
@@ -96,13 +94,13 @@ def pack(table: SegmentTable, packed: torch.Tensor, sumsq: torch.Tensor | None =
         raise ValueError("packed must be a CUDA uint8 tensor covering every layer's payload")
     sh = stream_handle(stream)
     if sumsq is None:
-        _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), None, None, None, sh))
+        _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), None, None, sh))
         return
     if sumsq.dtype != torch.float64 or not sumsq.is_cuda or sumsq.numel() < table.nseg:
         raise ValueError("sumsq must be a CUDA float64 tensor with one entry per layer")
-    parts, ctr = _Scratch.get(packed.device, sh, table.ntiles, table.nseg)
+    parts = _Scratch.get(packed.device, sh, table.ntiles)
     _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), sumsq.data_ptr(),
-                                    parts.data_ptr(), ctr.data_ptr(), sh))
+                                    parts.data_ptr(), sh))
 
 
 def unpack(table: SegmentTable, packed: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
@@ -119,9 +117,8 @@ def sumsq(table: SegmentTable, out: torch.Tensor, stream: torch.cuda.Stream | No
     if out.dtype != torch.float64 or not out.is_cuda or out.numel() < table.nseg:
         raise ValueError("out must be a CUDA float64 tensor with one entry per layer")
     sh = stream_handle(stream)
-    parts, ctr = _Scratch.get(out.device, sh, table.ntiles, table.nseg)
-    _lib.check(_lib.load().adt_sumsq(table.array, table.nseg, out.data_ptr(), parts.data_ptr(),
-                                     ctr.data_ptr(), sh))
+    parts = _Scratch.get(out.device, sh, table.ntiles)
+    _lib.check(_lib.load().adt_sumsq(table.array, table.nseg, out.data_ptr(), parts.data_ptr(), sh))
 
 
 def sm_count() -> int:

@@ -10,10 +10,10 @@ for l in open('$1'):
   r=d.get('roofline') or {}
   print('$2', round(d['value'],1), round(r.get('pack_GBps',0)), round(r.get('unpack_GBps',0)), d['clocks']['sm_mhz'])
 "; }
-for v in simple default "$@"; do
+for v in default tma "$@"; do
   for nn in "" "--no-norm"; do
     case $v in
-      simple) env="ADT_KERNEL=simple";;
+      tma) env="ADT_KERNEL=tma";;
       default) env="";;
       *) env="ADT_LIB=$PWD/paper_2004_02297_b200/variants/libadt_$v.so";;
     esac

@@ -56,14 +56,14 @@ def test_strerror_and_tile_count(lib):
 def test_validation_happens_before_any_device_work(lib):
     h = lib.load()
     bad_r = lib.segment_array([(16, 10, 0, 5)])
-    assert h.adt_pack(bad_r, 1, 16, None, None, None, None) == lib.ADT_ERR_ROUND_TO
+    assert h.adt_pack(bad_r, 1, 16, None, None, None) == lib.ADT_ERR_ROUND_TO
     with pytest.raises(ValueError):
         lib.check(lib.ADT_ERR_ROUND_TO)
     misaligned = lib.segment_array([(8, 10, 0, 2)])
-    assert h.adt_pack(misaligned, 1, 16, None, None, None, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_pack(misaligned, 1, 16, None, None, None) == lib.ADT_ERR_ALIGN
     bad_off = lib.segment_array([(16, 10, 8, 2)])
     assert h.adt_unpack(bad_off, 1, 16, None) == lib.ADT_ERR_ALIGN
     assert h.adt_unpack(lib.segment_array([(16, 10, 0, 2)]), 1, 0, None) == lib.ADT_ERR_ARG
-    assert h.adt_pack(None, -1, 0, None, None, None, None) == lib.ADT_ERR_ARG
+    assert h.adt_pack(None, -1, 0, None, None, None) == lib.ADT_ERR_ARG
     # norm pass without scratch
-    assert h.adt_sumsq(lib.segment_array([(16, 10, 0, 2)]), 1, None, None, None, None) == lib.ADT_ERR_ARG
+    assert h.adt_sumsq(lib.segment_array([(16, 10, 0, 2)]), 1, None, None, None) == lib.ADT_ERR_ARG
