@@ -158,19 +158,44 @@ __device__ __forceinline__ void tile_partial(double *partials, uint32_t tile, do
 }
 
 // Per layer (one CTA each): sum its tile partials in tile order -> seg_sumsq.
-// Launched right behind the pack pass (programmatic dependent launch).
+// Launched right behind the pack pass (programmatic dependent launch). Each
+// of the 1024 threads owns a contiguous run of partials and issues all its
+// loads before adding (the first version's strided dependent loop cost ~6 us
+// for AlexNet's 9216-tile fc6, profiles/r01_v3_*); runs then combine in a
+// fixed warp/CTA order, so the result depends only on the tile count.
+constexpr int kFinThreads = 1024;
 template <int MAXSEG>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kFinThreads)
 adt_norm_finalize_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #if __CUDA_ARCH__ >= 900
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-    __shared__ double red[kThreads / 32];
+    __shared__ double red[kFinThreads / 32];
     const int s = blockIdx.x;
+    const uint32_t lo = T.tile_begin[s], n = T.tile_begin[s + 1] - lo;
+    const uint32_t per = (n + kFinThreads - 1) / kFinThreads;
+    const uint32_t b = min(n, threadIdx.x * per), e = min(n, b + per);
+    const double *p = T.partials + lo;
     double a = 0.0;
-    for (uint32_t i = T.tile_begin[s] + threadIdx.x; i < T.tile_begin[s + 1]; i += kThreads) a += T.partials[i];
-    const double total = block_sum(a, red);
-    if (threadIdx.x == 0) T.seg_sumsq[s] = total;  // 0.0 for empty layers
+    uint32_t i = b;
+    for (; i + 8 <= e; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = p[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a += x[j];
+    }
+    for (; i < e; ++i) a += p[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+#pragma unroll
+        for (int w = 0; w < kFinThreads / 32; ++w) tot += red[w];
+        T.seg_sumsq[s] = tot;  // 0.0 for empty layers
+    }
 }
 
 // ---------------------------------------------------------------- pack pass
@@ -197,10 +222,14 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #pragma unroll
         for (int k = 0; k < kVec; ++k) {
             const uint32_t i = (k * kThreads + t) * 4;
-            uint32_t w[4];
+            if (i + 4 <= m) {
+                v[k] = __ldcs(src + k * kThreads + t);
+            } else {
+                uint32_t w[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
-            v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+                for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
+                v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
         }
     }
 
@@ -396,7 +425,7 @@ template <int MAXSEG>
 cudaError_t launch_finalize(const Table<MAXSEG> &T, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(T.nseg);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kFinThreads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
