@@ -230,45 +230,24 @@ def main_ours(args):
     sched = Fixed(L, 32)
     stream = torch.cuda.current_stream()
 
+    # The timed step is the product's own step: WeightSync.launch (N = 1) or
+    # ShardedWeightSync.launch (N > 1) — pack with the norm fused, [gather],
+    # unpack. `mid` events split pack from unpack for the per-kernel numbers.
     if world == 1:
-        layout = PackedLayout.plan(counts, rs)
-        packed = torch.empty(layout.nbytes, dtype=torch.uint8, device=dev)
-        ptab = engine.SegmentTable(masters, layout)
-        utab = engine.SegmentTable(replicas, layout)
-        sumsq = torch.empty(L, dtype=torch.float64, device=dev)
-
-        def do_pack():
-            engine.pack(ptab, packed, None if args.no_norm else sumsq)
-
-        def do_unpack():
-            engine.unpack(utab, packed)
-
+        sync = adt.WeightSync(masters, sched, replicas)
         pack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
         unpack_bytes = pack_bytes
-        kernels_per_step = 2
     else:
         from paper_2004_02297_b200.sharded import ShardedWeightSync
         sync = ShardedWeightSync(masters, sched, replicas)
         plan = sync.plan
-
-        def do_pack():
-            S = plan.send_bytes
-            engine.pack(sync.pack_table, sync.send[:S], sync.tail)
-            dist.all_gather_into_tensor(sync.recv[:S * world], sync.send[:S])
-
-        def do_unpack():
-            engine.unpack(sync.unpack_table, sync.recv[:plan.send_bytes * world])
-
         pack_bytes = sum((pc.hi - pc.lo) * (4 + plan.round_tos[pc.layer]) for pc in plan.pieces[rank])
         unpack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
-        kernels_per_step = 2
-
-    def step():
-        do_pack()
-        do_unpack()
+    kernels_per_step = 2 + (0 if args.no_norm else 1)  # pack, unpack, norm finalize
+    fused = not args.no_norm
 
     for _ in range(args.warmup):
-        step()
+        sync.launch(fused)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -284,12 +263,10 @@ def main_ours(args):
         for k in range(K):
             if mids:
                 mids[k][0].record(stream)
-            do_pack()
-            if mids:
-                mids[k][1].record(stream)
-            do_unpack()
-            if mids:
+                sync.launch(fused, mid_event=mids[k][1])
                 mids[k][2].record(stream)
+            else:
+                sync.launch(fused)
         e_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 2
+#define ADT_ABI_VERSION 3
 
 /* status codes */
 #define ADT_OK 0
@@ -42,8 +42,10 @@ extern "C" {
 #define ADT_ERR_NO_DEVICE (-4)  /* no CUDA device / driver */
 #define ADT_ERR_CUDA_BASE (-1000) /* -(1000 + cudaError_t) for CUDA runtime errors */
 
-/* Weights per tile: the unit of work of one CTA and of one norm partial. */
+/* Weights per tile: the unit of work of one CTA. */
 #define ADT_TILE_WEIGHTS 4096
+/* float64 norm partials per tile (one per 512-weight warp slice). */
+#define ADT_PARTIALS_PER_TILE 8
 
 /* One layer (a "segment" of the packed stream). */
 typedef struct adt_segment {
@@ -60,22 +62,31 @@ int adt_abi_version(void);
 /* Human-readable text for a status code (static storage). */
 const char *adt_strerror(int status);
 
-/* Number of tiles (= norm partials) a pack/sumsq over `segs` uses; size
- * `tile_partials` (doubles) to at least this. Host-only, no device work. */
-int adt_tile_count(const adt_segment *segs, int nseg, uint64_t *ntiles);
+/* Number of float64 norm partials a pack/sumsq over `segs` writes
+ * (ADT_PARTIALS_PER_TILE per 4096-weight tile); size `partials` to at least
+ * this. Host-only, no device work. */
+int adt_partials_count(const adt_segment *segs, int nseg, uint64_t *npartials);
 
 /*
  * Multi-tensor pack.  Replaces codec.pack / pack_vectorized / pack_parallel
- * (codec.py:116-180) applied to every layer, and — when `seg_sumsq` is non-NULL —
- * fuses precision.l2_norm (precision.py:25-28): seg_sumsq[l] receives the float64
- * sum of squares of layer l (sqrt it for the norm), reduced in a fixed order so
- * results are bit-identical run to run.  When seg_sumsq != NULL, `tile_partials`
- * (adt_tile_count doubles) is required scratch: the pack pass stores one float64
- * partial per 4096-weight tile and a small finalize kernel (launched behind it as
- * a programmatic dependent) sums each layer's partials in tile order.
+ * (codec.py:116-180) applied to every layer, and fuses precision.l2_norm
+ * (precision.py:25-28) into the same read of the weights:
+ *   partials  != NULL: the pass also stores float64 sums of squares, one per
+ *                      512-weight warp slice (adt_partials_count doubles);
+ *   seg_sumsq != NULL: (needs partials) a small finalize kernel is launched
+ *                      behind the pass (programmatic dependent launch) and
+ *                      writes seg_sumsq[l] = layer l's sum of squares, summed
+ *                      in a fixed (tile, warp) order: bit-identical run to run.
+ * Callers that want the finalize off the critical path pass seg_sumsq = NULL
+ * and call adt_norm_finalize on another stream (see sync.WeightSync).
  */
 int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed,
-             double *seg_sumsq, double *tile_partials, void *stream);
+             double *seg_sumsq, double *partials, void *stream);
+
+/* seg_sumsq[l] = fixed-order sum of layer l's partials written by adt_pack /
+ * adt_sumsq over the same `segs`. */
+int adt_norm_finalize(const adt_segment *segs, int nseg, double *partials,
+                      double *seg_sumsq, void *stream);
 
 /*
  * Multi-tensor unpack.  Replaces codec.unpack (codec.py:183-197) applied to
@@ -93,7 +104,7 @@ int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *s
  * norm is not fused into a pack (the last observation of a run, training.py:246-254).
  */
 int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq,
-              double *tile_partials, void *stream);
+              double *partials, void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

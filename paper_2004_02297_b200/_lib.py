@@ -23,10 +23,11 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 2
+ABI_VERSION = 3
+PARTIALS_PER_TILE = 8
 
-EXPORTS = ("adt_abi_version", "adt_strerror", "adt_tile_count", "adt_pack", "adt_unpack",
-           "adt_sumsq", "adt_device_sm_count")
+EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
+           "adt_unpack", "adt_sumsq", "adt_device_sm_count")
 
 
 class Segment(ctypes.Structure):
@@ -74,8 +75,10 @@ def load() -> ctypes.CDLL:
         lib.adt_abi_version.argtypes = []
         lib.adt_strerror.restype = ctypes.c_char_p
         lib.adt_strerror.argtypes = [ctypes.c_int]
-        lib.adt_tile_count.restype = ctypes.c_int
-        lib.adt_tile_count.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_uint64)]
+        lib.adt_partials_count.restype = ctypes.c_int
+        lib.adt_partials_count.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_uint64)]
+        lib.adt_norm_finalize.restype = ctypes.c_int
+        lib.adt_norm_finalize.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_pack.restype = ctypes.c_int
         lib.adt_pack.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack.restype = ctypes.c_int
@@ -116,7 +119,7 @@ def segment_array(segs) -> ctypes.Array:
     return arr
 
 
-def tile_count(seg_arr, nseg: int) -> int:
+def partials_count(seg_arr, nseg: int) -> int:
     out = ctypes.c_uint64(0)
-    check(load().adt_tile_count(seg_arr, nseg, ctypes.byref(out)))
+    check(load().adt_partials_count(seg_arr, nseg, ctypes.byref(out)))
     return int(out.value)

@@ -148,17 +148,21 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
     return s;
 }
 
-// Tile partial: fixed-order CTA reduction, one plain store. The per-layer
-// totals are summed by adt_norm_finalize_kernel (no fences or atomics here:
-// a per-CTA fence + L2 atomic kept every CTA resident ~1 us longer).
-__device__ __forceinline__ void tile_partial(double *partials, uint32_t tile, double acc) {
-    __shared__ double red[kThreads / 32];
-    const double part = block_sum(acc, red);
-    if (threadIdx.x == 0) partials[tile] = part;
+// Norm partials: ONE float64 per warp per tile (kWarpsPerTile per tile), a
+// fixed-order shuffle reduction and one plain store by lane 0 — no CTA barrier,
+// fence or atomic on the pack path (an earlier per-CTA fence + L2 atomic kept
+// every CTA resident ~1 us longer, profiles/r01_v1_*). adt_norm_finalize_kernel
+// sums a layer's partials in (tile, warp) order.
+constexpr int kWarpsPerTile = kThreads / 32;
+__device__ __forceinline__ void warp_partial(double *partials, uint32_t tile, double acc) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
+    if ((threadIdx.x & 31) == 0) partials[tile * kWarpsPerTile + (threadIdx.x >> 5)] = acc;
 }
 
-// Per layer (one CTA each): sum its tile partials in tile order -> seg_sumsq.
-// Launched right behind the pack pass (programmatic dependent launch). Each
+// Per layer (one CTA each): sum its partials in (tile, warp) order -> seg_sumsq.
+// Launched behind the pack pass (programmatic dependent launch) or on a side
+// stream by the caller (adt_norm_finalize). Each
 // of the 1024 threads owns a contiguous run of partials and issues all its
 // loads before adding (the first version's strided dependent loop cost ~6 us
 // for AlexNet's 9216-tile fc6, profiles/r01_v3_*); runs then combine in a
@@ -172,7 +176,7 @@ adt_norm_finalize_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #endif
     __shared__ double red[kFinThreads / 32];
     const int s = blockIdx.x;
-    const uint32_t lo = T.tile_begin[s], n = T.tile_begin[s + 1] - lo;
+    const uint32_t lo = T.tile_begin[s] * kWarpsPerTile, n = (T.tile_begin[s + 1] - T.tile_begin[s]) * kWarpsPerTile;
     const uint32_t per = (n + kFinThreads - 1) / kFinThreads;
     const uint32_t b = min(n, threadIdx.x * per), e = min(n, b + per);
     const double *p = T.partials + lo;
@@ -281,7 +285,7 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
         }
     }
 
-    if (NORM) tile_partial(T.partials, tile, acc);
+    if (NORM) warp_partial(T.partials, tile, acc);
 }
 
 // -------------------------------------------------------------- unpack pass
@@ -356,7 +360,7 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 namespace {
 
 // ----------------------------------------------------------------- host side
-enum class Pass { Pack, PackNorm, Norm, Unpack };
+enum class Pass { Pack, PackNorm, Norm, Unpack, Finalize };
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? ADT_OK : ADT_ERR_CUDA_BASE - static_cast<int>(e); }
 
@@ -414,6 +418,7 @@ cudaError_t launch_tma(Pass pass, const Table<MAXSEG> &T, uint32_t ntiles, cudaS
             auto k = tma::adt_unpack_tma_kernel<MAXSEG>;
             if ((e = allow_smem(k, smem)) == cudaSuccess) k<<<grid, tma::kBlock, smem, stream>>>(T, ntiles);
         } break;
+        case Pass::Finalize: break;
     }
     return e;
 }
@@ -459,7 +464,7 @@ int validate(const adt_segment *segs, int nseg, const void *packed, bool need_pa
 
 template <int MAXSEG>
 int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
-                 double *seg_sumsq, double *partials, uint32_t ntiles, cudaStream_t stream) {
+                 double *seg_sumsq, double *partials, uint32_t ntiles, bool finalize, cudaStream_t stream) {
     Table<MAXSEG> T;
     T.packed_in = pin;
     T.packed_out = pout;
@@ -476,9 +481,8 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pi
         T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
     }
     T.tile_begin[nseg] = acc;
-    const bool norm = pass == Pass::PackNorm || pass == Pass::Norm;
     cudaError_t e = cudaSuccess;
-    if (ntiles > 0) {
+    if (ntiles > 0 && pass != Pass::Finalize) {
         if (use_tma_kernels()) {
             e = launch_tma<MAXSEG>(pass, T, ntiles, stream);
         } else {
@@ -488,26 +492,27 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pi
                 case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T); break;
                 case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T); break;
                 case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T); break;
+                case Pass::Finalize: break;
             }
             e = cudaGetLastError();
         }
     }
-    if (e == cudaSuccess && norm && nseg > 0) e = launch_finalize<MAXSEG>(T, stream);
+    if (e == cudaSuccess && finalize && nseg > 0) e = launch_finalize<MAXSEG>(T, stream);
     return cuda_status(e);
 }
 
 constexpr int kSmallSeg = 16;
 constexpr int kLargeSeg = 256;
 
+// Greedy chunking (<= kLargeSeg layers, < 2^31 tiles per launch); the partial
+// offsets of a chunk depend only on `segs`, so a separate finalize call
+// (adt_norm_finalize) walks exactly the chunks the pack pass wrote.
 int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
-        double *seg_sumsq, double *partials, void *stream_v) {
-    const bool norm = pass == Pass::PackNorm || pass == Pass::Norm;
-    if (norm && nseg > 0 && (seg_sumsq == nullptr || partials == nullptr)) return ADT_ERR_ARG;
+        double *seg_sumsq, double *partials, bool finalize, void *stream_v) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
     uint64_t partial_base = 0;
     int base = 0;
     while (base < nseg) {
-        // greedy chunk: <= kLargeSeg layers and < 2^31 tiles per launch
         int cnt = 0;
         uint64_t tiles = 0;
         while (base + cnt < nseg && cnt < kLargeSeg) {
@@ -516,13 +521,13 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_
             tiles += t;
             ++cnt;
         }
-        double *ss = norm ? seg_sumsq + base : nullptr;
-        double *pp = norm ? partials + partial_base : nullptr;
+        double *ss = seg_sumsq ? seg_sumsq + base : nullptr;
+        double *pp = partials ? partials + partial_base : nullptr;
         const int st = cnt <= kSmallSeg
-            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), stream)
-            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), stream);
+            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream)
+            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream);
         if (st != ADT_OK) return st;
-        partial_base += tiles;
+        partial_base += tiles * kWarpsPerTile;
         base += cnt;
     }
     return ADT_OK;
@@ -549,33 +554,39 @@ const char *adt_strerror(int status) {
     }
 }
 
-int adt_tile_count(const adt_segment *segs, int nseg, uint64_t *ntiles) {
-    if (ntiles == nullptr || nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
+int adt_partials_count(const adt_segment *segs, int nseg, uint64_t *npartials) {
+    if (npartials == nullptr || nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
     uint64_t t = 0;
     for (int i = 0; i < nseg; ++i) t += (segs[i].count + kTile - 1) / kTile;
-    *ntiles = t;
+    *npartials = t * kWarpsPerTile;
     return ADT_OK;
 }
 
 int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed, double *seg_sumsq,
-             double *tile_partials, void *stream) {
+             double *partials, void *stream) {
     const int v = validate(segs, nseg, packed, true);
     if (v != ADT_OK) return v;
-    return run(seg_sumsq ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, packed, seg_sumsq,
-               tile_partials, stream);
+    if (nseg > 0 && seg_sumsq != nullptr && partials == nullptr) return ADT_ERR_ARG;
+    return run(partials ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, packed, seg_sumsq, partials,
+               seg_sumsq != nullptr, stream);
+}
+
+int adt_norm_finalize(const adt_segment *segs, int nseg, double *partials, double *seg_sumsq, void *stream) {
+    if (nseg < 0 || (nseg > 0 && (segs == nullptr || partials == nullptr || seg_sumsq == nullptr))) return ADT_ERR_ARG;
+    return run(Pass::Finalize, segs, nseg, nullptr, nullptr, seg_sumsq, partials, true, stream);
 }
 
 int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *stream) {
     const int v = validate(segs, nseg, packed, true);
     if (v != ADT_OK) return v;
-    return run(Pass::Unpack, segs, nseg, packed, nullptr, nullptr, nullptr, stream);
+    return run(Pass::Unpack, segs, nseg, packed, nullptr, nullptr, nullptr, false, stream);
 }
 
-int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *tile_partials, void *stream) {
+int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *partials, void *stream) {
     const int v = validate(segs, nseg, nullptr, false);
     if (v != ADT_OK) return v;
-    if (nseg > 0 && seg_sumsq == nullptr) return ADT_ERR_ARG;
-    return run(Pass::Norm, segs, nseg, nullptr, nullptr, seg_sumsq, tile_partials, stream);
+    if (nseg > 0 && (seg_sumsq == nullptr || partials == nullptr)) return ADT_ERR_ARG;
+    return run(Pass::Norm, segs, nseg, nullptr, nullptr, seg_sumsq, partials, true, stream);
 }
 
 int adt_device_sm_count(int *sm_count) {

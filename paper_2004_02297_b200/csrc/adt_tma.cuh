@@ -12,8 +12,8 @@
 // lane l handles groups 128w + l + 32j, j = 0..3 (coalesced at every width).
 // r = 3 (12 bytes per group) and ragged tails go through a per-warp staging
 // buffer so global stores stay 16-byte vectors, synchronised by __syncwarp
-// only. The fused float64 norm uses one 256-thread named barrier per tile and
-// stores one partial per tile (summed by adt_norm_finalize_kernel).
+// only. The fused float64 norm stores one partial per warp per tile (summed by
+// adt_norm_finalize_kernel).
 #pragma once
 
 namespace tma {
@@ -86,21 +86,12 @@ __device__ __forceinline__ TileInfo tile_info(const Table<MAXSEG> &T, uint32_t t
     return ti;
 }
 
-// Per-tile norm partial inside the persistent loop (consumer threads only):
-// a fixed-order warp + CTA reduction, one plain store per tile. No fence and
-// no atomic here — those would put an L2 round trip behind every tile.
-__device__ __forceinline__ void norm_tile(double *partials, Smem &S, uint32_t tile, int k, double acc) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Per-warp norm partial, indexed (tile, warp) like the register kernels'
+// (warp w here covers the tile's contiguous groups [128w, 128w+128)).
+__device__ __forceinline__ void norm_tile(double *partials, uint32_t tile, double acc) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
-    if (lane == 0) S.red[k & 1][warp] = acc;
-    consumer_sync(1);
-    if (threadIdx.x == 0) {
-        double part = 0.0;
-#pragma unroll
-        for (int w = 0; w < kConsumerWarps; ++w) part += S.red[k & 1][w];
-        partials[tile] = part;
-    }
+    if ((threadIdx.x & 31) == 0) partials[tile * kConsumerWarps + (threadIdx.x >> 5)] = acc;
 }
 
 // Copy `nbytes` (clipped to the warp's span) from the warp's staging buffer.
@@ -226,7 +217,7 @@ adt_pack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
                 __syncwarp();
             }
         }
-        if (NORM) norm_tile(T.partials, S, tile, k, acc);
+        if (NORM) norm_tile(T.partials, tile, acc);
     }
 }
 

@@ -60,22 +60,22 @@ class SegmentTable:
             segs.append((_check_weight(t, n, f"layer {i}"), n, off, r))
         self.nseg = len(segs)
         self.array = _lib.segment_array(segs)
-        self.ntiles = _lib.tile_count(self.array, self.nseg)
+        self.npartials = _lib.partials_count(self.array, self.nseg)
 
 
 class _Scratch:
-    """Per (device, stream) norm scratch: one float64 partial per tile."""
+    """Per (device, stream) norm scratch: the float64 partials of one pass."""
 
     _lock = threading.Lock()
     _cache: dict = {}
 
     @classmethod
-    def get(cls, device: torch.device, stream: int, ntiles: int) -> torch.Tensor:
+    def get(cls, device: torch.device, stream: int, n: int) -> torch.Tensor:
         key = (device.index, stream)
         with cls._lock:
             cur = cls._cache.get(key)
-            if cur is None or cur.numel() < max(1, ntiles):
-                cur = torch.empty(max(1, ntiles), dtype=torch.float64, device=device)
+            if cur is None or cur.numel() < max(1, n):
+                cur = torch.empty(max(1, n), dtype=torch.float64, device=device)
                 cls._cache[key] = cur
             return cur
 
@@ -87,20 +87,34 @@ def _device_of(table: SegmentTable) -> torch.device:
 
 
 def pack(table: SegmentTable, packed: torch.Tensor, sumsq: torch.Tensor | None = None,
-         stream: torch.cuda.Stream | None = None) -> None:
-    """adt_pack: every layer of `table` into `packed` (uint8, >= layout.nbytes);
-    with `sumsq` (float64[L]) the per-layer sums of squares are fused in."""
+         stream: torch.cuda.Stream | None = None, partials: torch.Tensor | None = None) -> None:
+    """adt_pack: every layer of `table` into `packed` (uint8, covering every payload).
+
+    sumsq (float64[L])       -> per-layer sums of squares fused in (finalize on the same stream);
+    partials only (no sumsq) -> the pass stores its norm partials for a later
+                                finalize(...) on another stream.
+    """
     if packed.dtype != torch.uint8 or not packed.is_cuda or packed.numel() < table.layout.payload_end:
         raise ValueError("packed must be a CUDA uint8 tensor covering every layer's payload")
     sh = stream_handle(stream)
-    if sumsq is None:
-        _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), None, None, sh))
-        return
+    if sumsq is not None and (sumsq.dtype != torch.float64 or not sumsq.is_cuda or sumsq.numel() < table.nseg):
+        raise ValueError("sumsq must be a CUDA float64 tensor with one entry per layer")
+    if partials is None and sumsq is not None:
+        partials = _Scratch.get(packed.device, sh, table.npartials)
+    if partials is not None and (partials.dtype != torch.float64 or partials.numel() < table.npartials):
+        raise ValueError("partials must be a float64 tensor of table.npartials entries")
+    _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(),
+                                    sumsq.data_ptr() if sumsq is not None else None,
+                                    partials.data_ptr() if partials is not None else None, sh))
+
+
+def finalize(table: SegmentTable, partials: torch.Tensor, sumsq: torch.Tensor,
+             stream: torch.cuda.Stream | None = None) -> None:
+    """adt_norm_finalize: per-layer fixed-order sums of a pack pass's partials."""
     if sumsq.dtype != torch.float64 or not sumsq.is_cuda or sumsq.numel() < table.nseg:
         raise ValueError("sumsq must be a CUDA float64 tensor with one entry per layer")
-    parts = _Scratch.get(packed.device, sh, table.ntiles)
-    _lib.check(_lib.load().adt_pack(table.array, table.nseg, packed.data_ptr(), sumsq.data_ptr(),
-                                    parts.data_ptr(), sh))
+    _lib.check(_lib.load().adt_norm_finalize(table.array, table.nseg, partials.data_ptr(), sumsq.data_ptr(),
+                                             stream_handle(stream)))
 
 
 def unpack(table: SegmentTable, packed: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
@@ -117,7 +131,7 @@ def sumsq(table: SegmentTable, out: torch.Tensor, stream: torch.cuda.Stream | No
     if out.dtype != torch.float64 or not out.is_cuda or out.numel() < table.nseg:
         raise ValueError("out must be a CUDA float64 tensor with one entry per layer")
     sh = stream_handle(stream)
-    parts = _Scratch.get(out.device, sh, table.ntiles)
+    parts = _Scratch.get(out.device, sh, table.npartials)
     _lib.check(_lib.load().adt_sumsq(table.array, table.nseg, out.data_ptr(), parts.data_ptr(), sh))
 
 

@@ -162,13 +162,16 @@ class ShardedWeightSync:
     def round_tos(self) -> list[int]:
         return list(self.plan.round_tos)
 
-    def launch(self, fused_norm: bool) -> None:
+    def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
+        """pack shard (norm finalized into the send tail) -> ncclAllGather -> unpack."""
         S = self.plan.send_bytes
         send = self.send[:S]
         recv = self.recv[:S * self.world]
         engine.pack(self.pack_table, send, self.tail if fused_norm else None)
         if self.world > 1:
             self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        if mid_event is not None:
+            mid_event.record(torch.cuda.current_stream())
         engine.unpack(self.unpack_table, recv)
 
     def _norms(self) -> list[float]:

@@ -59,6 +59,12 @@ class WeightSync:
         self.replicas = [r.reshape(-1) for r in replicas]
         self.sumsq = torch.zeros(len(self.masters), dtype=torch.float64, device=dev)
         self._host_sumsq = torch.empty(len(self.masters), dtype=torch.float64, pin_memory=True)
+        # The norm finalize (a tiny per-layer reduction of the pack's partials)
+        # runs on a side stream, concurrently with the unpack.
+        self._side = torch.cuda.Stream(device=dev)
+        self._fin_done = torch.cuda.Event()
+        self._fin_pending = False
+        self._partials = None
         self.device = dev
         self.layout = None
         self.packed = None
@@ -72,19 +78,35 @@ class WeightSync:
             self.packed = torch.empty(max(16, cap), dtype=torch.uint8, device=self.device)
         self.pack_table = engine.SegmentTable(self.masters, self.layout)
         self.unpack_table = engine.SegmentTable(self.replicas, self.layout)
+        if self._partials is None or self._partials.numel() < self.pack_table.npartials:
+            self._partials = torch.empty(max(1, self.pack_table.npartials), dtype=torch.float64, device=self.device)
 
     @property
     def round_tos(self) -> list[int]:
         return list(self.layout.round_tos)
 
-    def launch(self, fused_norm: bool, stream=None) -> None:
-        """The device work of one step: pack (+ fused norms), unpack. No host sync."""
-        engine.pack(self.pack_table, self.packed, self.sumsq if fused_norm else None, stream)
-        engine.unpack(self.unpack_table, self.packed, stream)
+    def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
+        """The device work of one step on the current stream, no host sync:
+        pack (+ norm partials), [side stream: finalize -> self.sumsq], unpack."""
+        main = torch.cuda.current_stream()
+        if fused_norm:
+            if self._fin_pending:
+                main.wait_event(self._fin_done)  # previous finalize done reading the partials
+            engine.pack(self.pack_table, self.packed, None, main, partials=self._partials)
+            self._side.wait_stream(main)
+            engine.finalize(self.pack_table, self._partials, self.sumsq, self._side)
+            self._fin_done.record(self._side)
+            self._fin_pending = True
+        else:
+            engine.pack(self.pack_table, self.packed, None, main)
+        if mid_event is not None:
+            mid_event.record(main)
+        engine.unpack(self.unpack_table, self.packed, main)
 
     def _read_norms(self) -> list[float]:
-        self._host_sumsq.copy_(self.sumsq, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        with torch.cuda.stream(self._side):  # queued behind the finalize
+            self._host_sumsq.copy_(self.sumsq, non_blocking=True)
+        self._side.synchronize()
         return [math.sqrt(v) for v in self._host_sumsq.tolist()]
 
     def step(self, batch: int = 0, observe: bool | None = None) -> SyncResult:
@@ -105,13 +127,19 @@ class WeightSync:
             res.repacked = True
         return res
 
+    def _norm_pass(self) -> list[float]:
+        main = torch.cuda.current_stream()
+        if self._fin_pending:
+            main.wait_event(self._fin_done)
+        engine.sumsq(self.pack_table, self.sumsq)
+        self._side.wait_stream(main)
+        return self._read_norms()
+
     def observe_final(self, batch: int) -> list[tuple]:
         """Norm-only pass over the masters (the observation after the last
         update, training.py:246-254); returns its trace rows labelled `batch`."""
-        engine.sumsq(self.pack_table, self.sumsq)
-        return self.schedule.observe_all(self._read_norms(), batch=batch)
+        return self.schedule.observe_all(self._norm_pass(), batch=batch)
 
     def norms(self) -> list[float]:
         """Current per-layer l2 norms of the masters (norm-only pass)."""
-        engine.sumsq(self.pack_table, self.sumsq)
-        return self._read_norms()
+        return self._norm_pass()

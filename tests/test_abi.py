@@ -26,8 +26,8 @@ def lib():
 
 def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
-        ["adt_abi_version", "adt_strerror", "adt_tile_count", "adt_pack", "adt_unpack", "adt_sumsq",
-         "adt_device_sm_count"])
+        ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
+         "adt_sumsq", "adt_device_sm_count"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -46,11 +46,11 @@ def test_library_is_sm100a_only():
     assert not re.search(r"sm_(?!100a)\d+", out)
 
 
-def test_strerror_and_tile_count(lib):
+def test_strerror_and_partials_count(lib):
     assert lib.strerror(0) == "ok"
     assert "round_to" in lib.strerror(lib.ADT_ERR_ROUND_TO)
     segs = lib.segment_array([(0, 0, 0, 1), (16, 4097, 16, 3), (32, 4096, 12304, 4)])
-    assert lib.tile_count(segs, 3) == 0 + 2 + 1
+    assert lib.partials_count(segs, 3) == (0 + 2 + 1) * lib.PARTIALS_PER_TILE
 
 
 def test_validation_happens_before_any_device_work(lib):
@@ -65,5 +65,8 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_unpack(bad_off, 1, 16, None) == lib.ADT_ERR_ALIGN
     assert h.adt_unpack(lib.segment_array([(16, 10, 0, 2)]), 1, 0, None) == lib.ADT_ERR_ARG
     assert h.adt_pack(None, -1, 0, None, None, None) == lib.ADT_ERR_ARG
+    # sums requested without partials scratch
+    assert h.adt_pack(lib.segment_array([(16, 10, 0, 2)]), 1, 16, 16, None, None) == lib.ADT_ERR_ARG
+    assert h.adt_norm_finalize(lib.segment_array([(16, 10, 0, 2)]), 1, None, 16, None) == lib.ADT_ERR_ARG
     # norm pass without scratch
     assert h.adt_sumsq(lib.segment_array([(16, 10, 0, 2)]), 1, None, None, None) == lib.ADT_ERR_ARG
