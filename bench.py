@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--quiet-extra", action="store_true", help="skip per-kernel event timing")
     ap.add_argument("--no-norm", action="store_true", help="A/B only: pack without the fused l2-norm")
+    ap.add_argument("--eager", action="store_true", help="launch each step eagerly instead of from CUDA graphs")
     return ap.parse_args()
 
 
@@ -245,9 +246,10 @@ def main_ours(args):
         unpack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
     kernels_per_step = 2 + (0 if args.no_norm else 1)  # pack, unpack, norm finalize
     fused = not args.no_norm
+    run_step = sync.launch if (args.eager or world > 1) else sync.launch_graphed
 
     for _ in range(args.warmup):
-        sync.launch(fused)
+        run_step(fused)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -263,10 +265,10 @@ def main_ours(args):
         for k in range(K):
             if mids:
                 mids[k][0].record(stream)
-                sync.launch(fused, mid_event=mids[k][1])
+                run_step(fused, mid_event=mids[k][1])
                 mids[k][2].record(stream)
             else:
-                sync.launch(fused)
+                run_step(fused)
         e_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:

@@ -427,7 +427,7 @@ cudaError_t launch_tma(Pass pass, const Table<MAXSEG> &T, uint32_t ntiles, cudaS
 // is processed while the pack drains; griddepcontrol.wait in the kernel
 // orders its reads after the pack's partial stores.
 template <int MAXSEG>
-cudaError_t launch_finalize(const Table<MAXSEG> &T, cudaStream_t stream) {
+cudaError_t launch_finalize(const Table<MAXSEG> &T, bool pdl, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(T.nseg);
     cfg.blockDim = dim3(kFinThreads);
@@ -437,7 +437,7 @@ cudaError_t launch_finalize(const Table<MAXSEG> &T, cudaStream_t stream) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, adt_norm_finalize_kernel<MAXSEG>, T);
 }
 
@@ -497,7 +497,9 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pi
             e = cudaGetLastError();
         }
     }
-    if (e == cudaSuccess && finalize && nseg > 0) e = launch_finalize<MAXSEG>(T, stream);
+    // PDL only directly behind this call's own pack pass; a standalone
+    // adt_norm_finalize (often on another stream) is an ordinary launch.
+    if (e == cudaSuccess && finalize && nseg > 0) e = launch_finalize<MAXSEG>(T, pass != Pass::Finalize, stream);
     return cuda_status(e);
 }
 

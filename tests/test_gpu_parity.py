@@ -246,3 +246,21 @@ def test_lenet_awp_walk_matches_reference(adt, golden_lenet):
         gd = golden_lenet["delta"][t, i]
         assert (delta is None and math.isnan(gd)) or abs(delta - gd) <= 1e-6 * max(abs(gd), 1e-3)
 
+
+
+def test_graphed_step_matches_eager(adt):
+    """WeightSync.launch_graphed (two CUDA graphs, finalize on a side branch)
+    == eager launch: same packed bytes, replicas and norm bits."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    masters = [torch.randn(n, generator=g, device="cuda") * 0.1 for n in (64, 4096 * 5 + 3, 1 << 18, 10)]
+    sched = adt.FixedPrecision(len(masters), 24)
+    a = adt.WeightSync(masters, sched)
+    a.launch(fused_norm=True)
+    eager = (a.packed.clone(), [r.clone() for r in a.replicas], a._read_norms())
+    b = adt.WeightSync(masters, sched)
+    for _ in range(3):
+        b.launch_graphed(fused_norm=True)
+    torch.cuda.synchronize()
+    assert torch.equal(b.packed[:b.layout.nbytes], eager[0][:a.layout.nbytes])
+    assert all(torch.equal(x, y) for x, y in zip(b.replicas, eager[1]))
+    assert b._read_norms() == eager[2]
