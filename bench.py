@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--quiet-extra", action="store_true", help="skip per-kernel event timing")
     ap.add_argument("--no-norm", action="store_true", help="A/B only: pack without the fused l2-norm")
     ap.add_argument("--eager", action="store_true", help="launch each step eagerly instead of from CUDA graphs")
+    ap.add_argument("--no-h2d", action="store_true", help="skip the pinned host->device comparison")
     return ap.parse_args()
 
 
@@ -304,6 +305,13 @@ def main_ours(args):
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, masters, rs, dev)
 
+    h2d = None
+    if not args.no_h2d and world == 1:
+        h2d = run_h2d(sync)
+    fp32_gather = None
+    if world > 1:
+        fp32_gather = run_fp32_allgather(counts, world, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(counts, rs, per_layer=1 << 22, reps=2)
@@ -320,7 +328,7 @@ def main_ours(args):
                        "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
-            "sync_ms_per_iter": ms,
+            "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -336,6 +344,70 @@ def traffic_of(kernel, args):
         return d.get(args.config, {}).get(kernel)
     except Exception:
         return None
+
+
+def _time_ms(fn, reps):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def run_h2d(sync, reps=10):
+    """The paper's CPU-master setting: weights cross from
+    pinned host memory to the GPU. Compares, on the same layer set,
+      raw FP32 H2D (4n bytes)                      — the uncompressed baseline,
+      packed H2D memcpy (Σn·r bytes) + unpack       — ADT, two steps,
+      zero-copy unpack reading mapped pinned memory — ADT, one kernel (K5).
+    The host packed stream is the device pack's output copied to pinned
+    memory beforehand (setup, untimed)."""
+    import torch
+    from paper_2004_02297_b200 import engine
+    lay = sync.layout
+    host_packed = torch.empty(lay.nbytes, dtype=torch.uint8, pin_memory=True)
+    host_packed.copy_(sync.packed[:lay.nbytes])
+    dev_packed = torch.empty(lay.nbytes, dtype=torch.uint8, device=sync.device)
+    host_fp32 = [m.cpu().pin_memory() for m in sync.masters]
+    reps_ = [torch.empty_like(m) for m in sync.masters]
+    table = engine.SegmentTable(sync.replicas, lay)
+
+    def raw():
+        for d, h in zip(reps_, host_fp32):
+            d.copy_(h, non_blocking=True)
+
+    def copy_unpack():
+        dev_packed.copy_(host_packed, non_blocking=True)
+        engine.unpack(table, dev_packed)
+
+    def zero_copy():
+        engine.unpack(table, host_packed)
+
+    t_raw, t_cu, t_zc = _time_ms(raw, reps), _time_ms(copy_unpack, reps), _time_ms(zero_copy, reps)
+    raw_b, pk_b = lay.raw_bytes, lay.total_payload_bytes
+    return {"raw_fp32_ms": t_raw, "adt_copy_unpack_ms": t_cu, "adt_zero_copy_unpack_ms": t_zc,
+            "raw_fp32_GBps": raw_b / t_raw / 1e6, "packed_bytes": pk_b, "raw_bytes": raw_b,
+            "payload_ratio": raw_b / pk_b, "speedup_vs_fp32": t_raw / min(t_cu, t_zc)}
+
+
+def run_fp32_allgather(counts, world, dev, reps=20):
+    """Baseline at N > 1: ncclAllGather of the raw FP32 weights (4n bytes)."""
+    import torch
+    import torch.distributed as dist
+    per = -(-4 * sum(counts) // world)
+    per = (per + 15) // 16 * 16
+    send = torch.empty(per, dtype=torch.uint8, device=dev)
+    recv = torch.empty(per * world, dtype=torch.uint8, device=dev)
+    ms = _time_ms(lambda: dist.all_gather_into_tensor(recv, send), reps)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"ms": ms, "bytes_per_rank": per, "busbw_GBps": per * (world - 1) / (ms * 1e-3) / 1e9}
 
 
 def run_e2e(args, dev_masters, rs, dev):

@@ -175,3 +175,16 @@ def test_product_path_refuses_without_cuda():
         adt.pack(np.zeros(4, np.float32), 2)
     with pytest.raises(RuntimeError, match="CUDA"):
         adt.l2_norm(np.zeros(4, np.float32))
+
+
+def test_wire_accounting_matches_reference_ledger_arithmetic():
+    # test_transfer.py:43-51 (1000 w @ r=3 -> 3014 wire) and :137-144 (mean r = 4/3 -> ~3x)
+    from paper_2004_02297_b200 import transfer
+    rec = transfer.send_weights_bytes(adt.PackedBlock(3, 1000, bytes(3000)), layer=0, bias_bytes=40)
+    assert (rec.wire_bytes, rec.raw_bytes, rec.weight_wire_bytes, rec.weight_raw_bytes) == (3054, 4040, 3014, 4000)
+    lay = PackedLayout.plan([10_000] * 3, [1, 1, 2])
+    recs = transfer.layout_records(lay)
+    assert 2.8 <= transfer.weight_stream_ratio(recs) <= 3.2
+    assert [r.weight_wire_bytes for r in recs] == [14 + 10_000, 14 + 10_000, 14 + 20_000]
+    with pytest.raises(ValueError):
+        transfer.weight_stream_ratio([])
