@@ -203,31 +203,94 @@ adt_norm_finalize_kernel(const __grid_constant__ Table<MAXSEG> T) {
 }
 
 // ---------------------------------------------------------------- pack pass
+// Mapping: warp w owns the tile's float4 groups [128w, 128w+128) (512 weights),
+// lane l handles groups 128w + 32j + l (j = 0..3): every load and every
+// direct store instruction of a warp is one contiguous, coalesced span.
+// r = 3 (12 bytes per group) and ragged last tiles go through a per-warp
+// shared-memory staging area and leave as 16-byte vectors; only __syncwarp is
+// needed, so no warp ever waits for another (no CTA barriers in the pack).
+constexpr int kWarpGroups = kTile / 4 / kWarpsPerTile;       // 128
+constexpr int kWarpStageWords = kWarpGroups * 4;              // <= r words per group, r <= 4
+
+// Float64 sum of squares of the 16 words a thread holds. Fast path (all
+// normal numbers, checked with two unsigned min/max per word): rebuild each
+// double from the float's bits on the integer pipe, no per-word branch.
+// Otherwise (zero / subnormal / inf / NaN present): per-word widen().
+__device__ __forceinline__ double sumsq16(const uint4 (&v)[kVec]) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+        const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t a = w[j] & 0x7FFFFFFFu;
+            lo = min(lo, a);
+            hi = max(hi, a);
+        }
+    }
+    double acc = 0.0;
+    if (lo >= 0x00800000u && hi < 0x7F800000u) {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t a = w[j] & 0x7FFFFFFFu;
+                const double d = __hiloint2double(static_cast<int>((a >> 3) + (896u << 20)),
+                                                  static_cast<int>(w[j] << 29));
+                acc = fma(d, d, acc);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            acc = sq_acc(acc, v[k].x);
+            acc = sq_acc(acc, v[k].y);
+            acc = sq_acc(acc, v[k].z);
+            acc = sq_acc(acc, v[k].w);
+        }
+    }
+    return acc;
+}
+
+// Copy `nbytes` from a warp's staging words to global, 16-byte vectors first.
+__device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *dst, uint32_t nbytes, int lane) {
+    const uint32_t n16 = nbytes / 16;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(ws);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    for (uint32_t i = lane; i < n16; i += 32) d4[i] = s4[i];
+    const uint8_t *s1 = reinterpret_cast<const uint8_t *>(ws);
+    for (uint32_t i = n16 * 16 + lane; i < nbytes; i += 32) dst[i] = s1[i];
+}
+
 // WRITE=false is the norm-only pass (adt_sumsq).
+#ifndef ADT_PACK_MIN_BLOCKS
+#define ADT_PACK_MIN_BLOCKS 5   // resident CTAs/SM the register budget must allow (A/B: scripts/build_variants.sh)
+#endif
 template <int MAXSEG, bool NORM, bool WRITE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, ADT_PACK_MIN_BLOCKS)
 adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
-    __shared__ __align__(16) uint32_t stage[kTile];   // r*kTile/4 words used (r = 3 or tails)
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     const uint32_t tile = blockIdx.x;
     const int s = find_segment(T, tile);
-    const uint64_t n = T.count[s];
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
-    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n - e0));
+    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
     const int r = T.round_to[s];
-    const int t = threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t g0 = warp * kWarpGroups + lane;                 // group of j = 0
     const uint4 *src = reinterpret_cast<const uint4 *>(T.weights[s]) + e0 / 4;
 
     uint4 v[kVec];
     if (m == kTile) {
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) v[k] = __ldcs(src + k * kThreads + t);
+        for (int k = 0; k < kVec; ++k) v[k] = __ldcs(src + g0 + 32 * k);
     } else {
         const uint32_t *src1 = reinterpret_cast<const uint32_t *>(src);
 #pragma unroll
         for (int k = 0; k < kVec; ++k) {
-            const uint32_t i = (k * kThreads + t) * 4;
+            const uint32_t g = g0 + 32 * k, i = g * 4;
             if (i + 4 <= m) {
-                v[k] = __ldcs(src + k * kThreads + t);
+                v[k] = __ldcs(src + g);
             } else {
                 uint32_t w[4];
 #pragma unroll
@@ -237,118 +300,121 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
         }
     }
 
-    double acc = 0.0;
-    if (NORM) {
-#pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-            acc = sq_acc(acc, v[k].x);
-            acc = sq_acc(acc, v[k].y);
-            acc = sq_acc(acc, v[k].z);
-            acc = sq_acc(acc, v[k].w);
-        }
-    }
-
     if (WRITE) {
         uint8_t *dst = T.packed_out + T.offset[s] + e0 * r;
         if (m == kTile && r != 3) {
-            // direct warp-coalesced stores from registers
             if (r == 1) {
                 uint32_t *d = reinterpret_cast<uint32_t *>(dst);
 #pragma unroll
-                for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); d[k * kThreads + t] = o[0]; }
+                for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); d[g0 + 32 * k] = o[0]; }
             } else if (r == 2) {
                 uint2 *d = reinterpret_cast<uint2 *>(dst);
 #pragma unroll
-                for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); d[k * kThreads + t] = make_uint2(o[0], o[1]); }
+                for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); d[g0 + 32 * k] = make_uint2(o[0], o[1]); }
             } else {
                 uint4 *d = reinterpret_cast<uint4 *>(dst);
 #pragma unroll
-                for (int k = 0; k < kVec; ++k) { uint32_t o[4]; pack_r4(v[k], o); d[k * kThreads + t] = make_uint4(o[0], o[1], o[2], o[3]); }
+                for (int k = 0; k < kVec; ++k) { uint32_t o[4]; pack_r4(v[k], o); d[g0 + 32 * k] = make_uint4(o[0], o[1], o[2], o[3]); }
             }
         } else {
-            // stage r words per float4 group in shared memory, then 16-byte stores
+            uint32_t *ws = stage[warp];
+            if (r == 3) {
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) {
-                uint32_t o[4];
-                pack_any(r, v[k], o);
-                uint32_t *p = stage + (k * kThreads + t) * r;
-                for (int j = 0; j < r; ++j) p[j] = o[j];
+                for (int k = 0; k < kVec; ++k) {
+                    uint32_t o[3];
+                    pack_r3(v[k], o);
+                    uint32_t *p = ws + (lane + 32 * k) * 3;   // stride 3: conflict-free
+                    p[0] = o[0]; p[1] = o[1]; p[2] = o[2];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kVec; ++k) {
+                    uint32_t o[4];
+                    pack_any(r, v[k], o);
+                    uint32_t *p = ws + (lane + 32 * k) * r;
+                    p[0] = o[0];
+                    if (r > 1) p[1] = o[1];
+                    if (r > 2) p[2] = o[2];
+                    if (r > 3) p[3] = o[3];
+                }
             }
-            __syncthreads();
-            const uint32_t nbytes = m * r;
-            const uint32_t n16 = nbytes / 16;
-            const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
-            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-            for (uint32_t i = t; i < n16; i += kThreads) d4[i] = s4[i];
-            const uint8_t *s1 = reinterpret_cast<const uint8_t *>(stage);
-            for (uint32_t i = n16 * 16 + t; i < nbytes; i += kThreads) dst[i] = s1[i];
+            __syncwarp();
+            const uint32_t span = kWarpGroups * 4 * r;            // the warp's packed bytes
+            const uint32_t lo = warp * span, nbytes = m * r;
+            if (lo < nbytes) warp_store_bytes(ws, dst + lo, min(span, nbytes - lo), lane);
         }
     }
 
-    if (NORM) warp_partial(T.partials, tile, acc);
+    if (NORM) warp_partial(T.partials, tile, sumsq16(v));
 }
 
 // -------------------------------------------------------------- unpack pass
 template <int MAXSEG>
 __global__ void __launch_bounds__(kThreads)
 adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
-    __shared__ __align__(16) uint32_t stage[kTile];
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     const uint32_t tile = blockIdx.x;
     const int s = find_segment(T, tile);
-    const uint64_t n = T.count[s];
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
-    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n - e0));
+    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
     const int r = T.round_to[s];
-    const int t = threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t g0 = warp * kWarpGroups + lane;
     const uint8_t *src = T.packed_in + T.offset[s] + e0 * r;
     uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
 
     if (m == kTile && r != 3) {
+        uint4 out[kVec];
         if (r == 1) {
             const uint32_t *p = reinterpret_cast<const uint32_t *>(src);
             uint32_t w[kVec];
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + k * kThreads + t);
+            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + g0 + 32 * k);
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) dst[k * kThreads + t] = unpack_r1(w[k]);
+            for (int k = 0; k < kVec; ++k) out[k] = unpack_r1(w[k]);
         } else if (r == 2) {
             const uint2 *p = reinterpret_cast<const uint2 *>(src);
             uint2 w[kVec];
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + k * kThreads + t);
+            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + g0 + 32 * k);
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) dst[k * kThreads + t] = unpack_r2(w[k].x, w[k].y);
+            for (int k = 0; k < kVec; ++k) out[k] = unpack_r2(w[k].x, w[k].y);
         } else {
             const uint4 *p = reinterpret_cast<const uint4 *>(src);
             uint4 w[kVec];
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + k * kThreads + t);
+            for (int k = 0; k < kVec; ++k) w[k] = __ldcs(p + g0 + 32 * k);
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) dst[k * kThreads + t] = unpack_r4(w[k]);
+            for (int k = 0; k < kVec; ++k) out[k] = unpack_r4(w[k]);
         }
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) dst[g0 + 32 * k] = out[k];
         return;
     }
 
-    // staged path: r = 3 tiles and every layer's ragged last tile
-    const uint32_t nbytes = m * r;
-    const uint32_t n16 = nbytes / 16;
-    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-    uint4 *st4 = reinterpret_cast<uint4 *>(stage);
-    for (uint32_t i = t; i < n16; i += kThreads) st4[i] = __ldcs(s4 + i);
-    uint8_t *st1 = reinterpret_cast<uint8_t *>(stage);
-    for (uint32_t i = n16 * 16 + t; i < nbytes; i += kThreads) st1[i] = src[i];
-    __syncthreads();
+    // staged per warp: r = 3 tiles and every layer's ragged last tile
+    uint32_t *ws = stage[warp];
+    const uint32_t span = kWarpGroups * 4 * r, lo = warp * span, nbytes = m * r;
+    if (lo >= nbytes) return;
+    const uint32_t mine = min(span, nbytes - lo), n16 = mine / 16;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src + lo);
+    uint4 *w4 = reinterpret_cast<uint4 *>(ws);
+    for (uint32_t i = lane; i < n16; i += 32) w4[i] = __ldcs(s4 + i);
+    uint8_t *w1 = reinterpret_cast<uint8_t *>(ws);
+    for (uint32_t i = n16 * 16 + lane; i < mine; i += 32) w1[i] = src[lo + i];
+    __syncwarp();
     uint32_t *dst1 = reinterpret_cast<uint32_t *>(dst);
 #pragma unroll
     for (int k = 0; k < kVec; ++k) {
-        const uint32_t g = k * kThreads + t;   // float4 group within the tile
+        const uint32_t gl = lane + 32 * k, g = g0 + 32 * k;   // local / tile group
         if (g * 4 >= m) break;
-        const uint4 o = unpack_words(r, stage + g * r);
+        const uint4 o = unpack_words(r, ws + gl * r);
         if (g * 4 + 4 <= m) {
             dst[g] = o;
         } else {
-            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-            for (uint32_t j = 0; g * 4 + j < m; ++j) dst1[g * 4 + j] = ow[j];
+            if (g * 4 + 0 < m) dst1[g * 4 + 0] = o.x;
+            if (g * 4 + 1 < m) dst1[g * 4 + 1] = o.y;
+            if (g * 4 + 2 < m) dst1[g * 4 + 2] = o.z;
         }
     }
 }
