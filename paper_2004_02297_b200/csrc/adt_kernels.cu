@@ -265,7 +265,7 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
 
 // WRITE=false is the norm-only pass (adt_sumsq).
 #ifndef ADT_PACK_MIN_BLOCKS
-#define ADT_PACK_MIN_BLOCKS 5   // resident CTAs/SM the register budget must allow (A/B: scripts/build_variants.sh)
+#define ADT_PACK_MIN_BLOCKS 6   // resident CTAs/SM the register budget must allow (A/B: profiles/r01_ab_occupancy.md)
 #endif
 template <int MAXSEG, bool NORM, bool WRITE>
 __global__ void __launch_bounds__(kThreads, ADT_PACK_MIN_BLOCKS)
@@ -349,8 +349,11 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 }
 
 // -------------------------------------------------------------- unpack pass
+#ifndef ADT_UNPACK_MIN_BLOCKS
+#define ADT_UNPACK_MIN_BLOCKS 5
+#endif
 template <int MAXSEG>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
 adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     const uint32_t tile = blockIdx.x;
