@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--bits", type=int, default=None, help="uniform width (default: the config's widths)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--quiet-extra", action="store_true", help="skip per-kernel event timing")
     ap.add_argument("--no-norm", action="store_true", help="A/B only: pack without the fused l2-norm")
     ap.add_argument("--eager", action="store_true", help="launch each step eagerly instead of from CUDA graphs")
@@ -301,9 +301,10 @@ def main_ours(args):
                     "pack_GBps": pack_bytes / (pk * 1e-3) / 1e9, "unpack_GBps": unpack_bytes / (up * 1e-3) / 1e9}
 
     # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
-    e2e = None
+    e2e = e2e_sync = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, masters, rs, dev)
+        e2e_sync = run_e2e_weightsync(args, masters, rs, dev)
 
     h2d = None
     if not args.no_h2d and world == 1:
@@ -326,7 +327,7 @@ def main_ours(args):
                        "algorithmic_bytes_per_step": total_bytes,
                        "l2": "working set (FP32 master + packed + FP32 replica) > 126 MB L2; no flush",
                        "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_weightsync": e2e_sync,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
         }
@@ -411,10 +412,41 @@ def run_fp32_allgather(counts, world, dev, reps=20):
 
 
 def run_e2e(args, dev_masters, rs, dev):
-    """Same metric through the public API (WeightSync) with HOST buffers: every
-    step copies the FP32 masters from pinned host memory (H2D), packs (norms
-    fused) and unpacks through WeightSync.step, and reads the per-layer norms
-    back to the host (D2H) — the AWP observation."""
+    """Same metric through the reference-facing drop-in API with HOST buffers —
+    the calls the reference arm times (weightpack codec.pack_vectorized /
+    unpack, precision.l2_norm), layer by layer on NumPy arrays: every step
+    copies each layer host->device for pack, the payload bytes back
+    (PackedBlock.payload is `bytes`), the payload host->device for unpack, the
+    FP32 words back (a NumPy array), and the layer again for l2_norm."""
+    import torch
+    import paper_2004_02297_b200 as adt
+    host = [m.cpu().numpy() for m in dev_masters]
+
+    def one():
+        for w, r in zip(host, rs):
+            blk = adt.pack_vectorized(w, r)
+            adt.unpack(blk)
+            adt.l2_norm(w)
+
+    one()
+    steps = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    n = [w.size for w in host]
+    byts = 2 * sum((4 + r) * k for k, r in zip(n, rs))
+    h2d = sum(4 * k + r * k + 4 * k for k, r in zip(n, rs))
+    d2h = sum(r * k + 4 * k for k, r in zip(n, rs))
+    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": dt * 1e3, "steps": steps,
+            "note": "drop-in per-layer pack_vectorized + unpack + l2_norm on host NumPy arrays; wall clock"}
+
+
+def run_e2e_weightsync(args, dev_masters, rs, dev):
+    """WeightSync from pinned host FP32 masters: per step H2D of the masters,
+    pack (norm fused) + unpack on device, D2H of the L float64 sums."""
     import torch
     import paper_2004_02297_b200 as adt
     from paper_2004_02297_b200.precision import FixedPrecision
@@ -445,7 +477,7 @@ def run_e2e(args, dev_masters, rs, dev):
     dt = (time.perf_counter() - t0) / args.e2e_steps
     byts = sync.layout.roundtrip_bytes()
     return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": dt * 1e3, "note": "WeightSync.step path from pinned host FP32 masters; wall clock"}
+            "ms_per_step": dt * 1e3, "note": "WeightSync from pinned host FP32 masters; wall clock"}
 
 
 if __name__ == "__main__":

@@ -18,6 +18,7 @@ launch for all layers, norms fused into the pack.
 from __future__ import annotations
 
 import struct
+import warnings
 from typing import BinaryIO, Sequence
 
 import numpy as np
@@ -147,12 +148,9 @@ def _device_words(weights) -> tuple[torch.Tensor, bool]:
     if isinstance(weights, torch.Tensor):
         weights = weights.detach().numpy()
     host = np.ascontiguousarray(weights, dtype=np.float32).reshape(-1)
-    t = torch.from_numpy(host)
-    if t.numel():
-        t = t.pin_memory().to("cuda", non_blocking=True)
-    else:
-        t = torch.empty(0, dtype=torch.float32, device="cuda")
-    return t, False
+    if host.size == 0:
+        return torch.empty(0, dtype=torch.float32, device="cuda"), False
+    return torch.from_numpy(host).to("cuda"), False
 
 
 def _pack_device(flat: torch.Tensor, r: int) -> torch.Tensor:
@@ -209,7 +207,9 @@ def unpack(block: PackedBlock):
         if src.data_ptr() % 16:
             src = src.clone()
     else:
-        src = torch.frombuffer(bytearray(block.payload), dtype=torch.uint8).pin_memory().to("cuda", non_blocking=True)
+        with warnings.catch_warnings():  # read-only bytes: the view is only ever read (copied to the device)
+            warnings.simplefilter("ignore", UserWarning)
+            src = torch.frombuffer(block.payload, dtype=torch.uint8).to("cuda")
     engine.unpack(engine.SegmentTable([out], layout), src)
     return out if block.on_device else out.cpu().numpy()
 

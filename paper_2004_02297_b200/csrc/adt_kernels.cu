@@ -160,13 +160,12 @@ __device__ __forceinline__ void warp_partial(double *partials, uint32_t tile, do
     if ((threadIdx.x & 31) == 0) partials[tile * kWarpsPerTile + (threadIdx.x >> 5)] = acc;
 }
 
-// Per layer (one CTA each): sum its partials in (tile, warp) order -> seg_sumsq.
+// Per layer (one CTA each): fixed-order sum of its partials -> seg_sumsq.
 // Launched behind the pack pass (programmatic dependent launch) or on a side
-// stream by the caller (adt_norm_finalize). Each
-// of the 1024 threads owns a contiguous run of partials and issues all its
-// loads before adding (the first version's strided dependent loop cost ~6 us
-// for AlexNet's 9216-tile fc6, profiles/r01_v3_*); runs then combine in a
-// fixed warp/CTA order, so the result depends only on the tile count.
+// stream by the caller (adt_norm_finalize). Thread t sums partials t, t+1024,
+// t+2048, ... (coalesced; 8 loads in flight), then a fixed shuffle/CTA tree.
+// (A contiguous-run-per-thread version was uncoalesced: 28 us for AlexNet.)
+// The order depends only on the layer's partial count: bit-identical results.
 constexpr int kFinThreads = 1024;
 template <int MAXSEG>
 __global__ void __launch_bounds__(kFinThreads)
@@ -176,20 +175,19 @@ adt_norm_finalize_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #endif
     __shared__ double red[kFinThreads / 32];
     const int s = blockIdx.x;
-    const uint32_t lo = T.tile_begin[s] * kWarpsPerTile, n = (T.tile_begin[s + 1] - T.tile_begin[s]) * kWarpsPerTile;
-    const uint32_t per = (n + kFinThreads - 1) / kFinThreads;
-    const uint32_t b = min(n, threadIdx.x * per), e = min(n, b + per);
+    const uint32_t lo = T.tile_begin[s] * kWarpsPerTile;
+    const uint32_t n = (T.tile_begin[s + 1] - T.tile_begin[s]) * kWarpsPerTile;
     const double *p = T.partials + lo;
     double a = 0.0;
-    uint32_t i = b;
-    for (; i + 8 <= e; i += 8) {
+    uint32_t i = threadIdx.x;
+    for (; i + 7 * kFinThreads < n; i += 8 * kFinThreads) {
         double x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = p[i + j];
+        for (int j = 0; j < 8; ++j) x[j] = p[i + j * kFinThreads];
 #pragma unroll
         for (int j = 0; j < 8; ++j) a += x[j];
     }
-    for (; i < e; ++i) a += p[i];
+    for (; i < n; i += kFinThreads) a += p[i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
