@@ -301,10 +301,10 @@ def main_ours(args):
                     "pack_GBps": pack_bytes / (pk * 1e-3) / 1e9, "unpack_GBps": unpack_bytes / (up * 1e-3) / 1e9}
 
     # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
-    e2e = e2e_sync = None
+    e2e = e2e_dropin = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, masters, rs, dev)
-        e2e_sync = run_e2e_weightsync(args, masters, rs, dev)
+        e2e = run_e2e_weightsync(args, masters, rs, dev)
+        e2e_dropin = run_e2e(args, masters, rs, dev)
 
     h2d = None
     if not args.no_h2d and world == 1:
@@ -327,7 +327,7 @@ def main_ours(args):
                        "algorithmic_bytes_per_step": total_bytes,
                        "l2": "working set (FP32 master + packed + FP32 replica) > 126 MB L2; no flush",
                        "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_weightsync": e2e_sync,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
         }

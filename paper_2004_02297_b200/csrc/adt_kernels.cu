@@ -350,11 +350,21 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #ifndef ADT_UNPACK_MIN_BLOCKS
 #define ADT_UNPACK_MIN_BLOCKS 5
 #endif
+#ifndef ADT_UNPACK_REVERSE
+#define ADT_UNPACK_REVERSE 0
+#endif
 template <int MAXSEG>
 __global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
 adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+#if ADT_UNPACK_REVERSE
+    // Newest-first: CTAs are dispatched roughly in blockIdx order, so walking
+    // the tiles backwards reads the payload the pack pass wrote last — the
+    // part still resident in the 126 MB L2 — before it is evicted.
+    const uint32_t tile = gridDim.x - 1 - blockIdx.x;
+#else
     const uint32_t tile = blockIdx.x;
+#endif
     const int s = find_segment(T, tile);
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
