@@ -351,7 +351,7 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #define ADT_UNPACK_MIN_BLOCKS 5
 #endif
 #ifndef ADT_UNPACK_REVERSE
-#define ADT_UNPACK_REVERSE 0
+#define ADT_UNPACK_REVERSE 1   // A/B: AlexNet step 132.7 -> 127.2 us (profiles/r01_ab_unpack_order.md)
 #endif
 template <int MAXSEG>
 __global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
