@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-norm", action="store_true", help="A/B only: pack without the fused l2-norm")
     ap.add_argument("--eager", action="store_true", help="launch each step eagerly instead of from CUDA graphs")
     ap.add_argument("--no-h2d", action="store_true", help="skip the pinned host->device comparison")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: ncclAllGather of packed bytes, or fused peer-read gather-unpack (CUDA IPC)")
     return ap.parse_args()
 
 
@@ -241,7 +243,7 @@ def main_ours(args):
         unpack_bytes = pack_bytes
     else:
         from paper_2004_02297_b200.sharded import ShardedWeightSync
-        sync = ShardedWeightSync(masters, sched, replicas)
+        sync = ShardedWeightSync(masters, sched, replicas, transport=args.transport)
         plan = sync.plan
         pack_bytes = sum((pc.hi - pc.lo) * (4 + plan.round_tos[pc.layer]) for pc in plan.pieces[rank])
         unpack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))

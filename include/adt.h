@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 3
+#define ADT_ABI_VERSION 4
 
 /* status codes */
 #define ADT_OK 0
@@ -46,6 +46,8 @@ extern "C" {
 #define ADT_TILE_WEIGHTS 4096
 /* float64 norm partials per tile (one per 512-weight warp slice). */
 #define ADT_PARTIALS_PER_TILE 8
+/* Source buffers one adt_unpack_multi call may read (ranks of a node). */
+#define ADT_MAX_SOURCES 16
 
 /* One layer (a "segment" of the packed stream). */
 typedef struct adt_segment {
@@ -53,7 +55,7 @@ typedef struct adt_segment {
     uint64_t count;     /* number of weights (may be 0) */
     uint64_t offset;    /* byte offset of this layer's payload in the packed buffer, 16-B aligned */
     int32_t round_to;   /* bytes kept per weight, 1..4 (codec.py:52-57; bits_to_round_to codec.py:60-67) */
-    int32_t reserved;   /* must be 0 */
+    int32_t reserved;   /* 0; for adt_unpack_multi: index of the source buffer holding this payload */
 } adt_segment;
 
 /* ABI version (ADT_ABI_VERSION). */
@@ -97,6 +99,31 @@ int adt_norm_finalize(const adt_segment *segs, int nseg, double *partials,
  * weights to the GPU).
  */
 int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *stream);
+
+/*
+ * Gather-unpack: like adt_unpack, but layer l's payload is read from
+ * sources[segs[l].reserved] + segs[l].offset. The sources are the ranks' packed
+ * send buffers mapped into this process — peer device memory opened with
+ * adt_ipc_open (read over NVLink inside the kernel: the all-gather and the
+ * unpack are one pass) or local device/pinned buffers. nsrc <= ADT_MAX_SOURCES.
+ * Replaces the per-worker loop of training.py:214-225 (send_weights + unpack).
+ */
+int adt_unpack_multi(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
+                     void *stream);
+
+/* dst[q*bytes .. (q+1)*bytes) = sources[q][offset .. offset+bytes) for q < nsrc
+ * (small peer reads, e.g. every rank's norm tail). */
+int adt_copy_multi(uint8_t *dst, const uint8_t *const *sources, int nsrc, uint64_t offset, uint64_t bytes,
+                   void *stream);
+
+/* CUDA IPC plumbing for adt_unpack_multi (thin wrappers over cudaIpc*):
+ * handle size in bytes; export the allocation holding dev_ptr (*offset_out =
+ * dev_ptr's byte offset inside it); map a peer's allocation (peer access
+ * enabled lazily; add the exporter's offset); unmap it. */
+int adt_ipc_handle_bytes(void);
+int adt_ipc_get_handle(void *dev_ptr, void *handle_out, uint64_t *offset_out);
+int adt_ipc_open(const void *handle, void **dev_ptr_out);
+int adt_ipc_close(void *dev_ptr);
 
 /*
  * Norm-only pass (no packed output): seg_sumsq[l] = float64 sum of squares of

@@ -23,11 +23,13 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 3
+ABI_VERSION = 4
+MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
-           "adt_unpack", "adt_sumsq", "adt_device_sm_count")
+           "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
+           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_device_sm_count")
 
 
 class Segment(ctypes.Structure):
@@ -83,6 +85,18 @@ def load() -> ctypes.CDLL:
         lib.adt_pack.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack.restype = ctypes.c_int
         lib.adt_unpack.argtypes = [seg_p, ctypes.c_int, vp, vp]
+        lib.adt_unpack_multi.restype = ctypes.c_int
+        lib.adt_unpack_multi.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp]
+        lib.adt_copy_multi.restype = ctypes.c_int
+        lib.adt_copy_multi.argtypes = [vp, P(ctypes.c_void_p), ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp]
+        lib.adt_ipc_handle_bytes.restype = ctypes.c_int
+        lib.adt_ipc_handle_bytes.argtypes = []
+        lib.adt_ipc_get_handle.restype = ctypes.c_int
+        lib.adt_ipc_get_handle.argtypes = [vp, vp, P(ctypes.c_uint64)]
+        lib.adt_ipc_open.restype = ctypes.c_int
+        lib.adt_ipc_open.argtypes = [vp, P(ctypes.c_void_p)]
+        lib.adt_ipc_close.restype = ctypes.c_int
+        lib.adt_ipc_close.argtypes = [vp]
         lib.adt_sumsq.restype = ctypes.c_int
         lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_device_sm_count.restype = ctypes.c_int
@@ -108,14 +122,22 @@ def check(status: int) -> None:
 
 
 def segment_array(segs) -> ctypes.Array:
-    """[(ptr, count, offset, round_to), ...] -> adt_segment[]."""
+    """[(ptr, count, offset, round_to[, source]), ...] -> adt_segment[]."""
     arr = (Segment * max(1, len(segs)))()
-    for i, (ptr, count, offset, r) in enumerate(segs):
+    for i, seg in enumerate(segs):
+        ptr, count, offset, r = seg[:4]
         arr[i].weights = ptr
         arr[i].count = count
         arr[i].offset = offset
         arr[i].round_to = r
-        arr[i].reserved = 0
+        arr[i].reserved = seg[4] if len(seg) > 4 else 0
+    return arr
+
+
+def pointer_array(ptrs) -> ctypes.Array:
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
     return arr
 
 

@@ -24,6 +24,8 @@
 #include <stdint.h>
 #include <limits.h>
 #include <stdlib.h>
+#include <string.h>
+#include <dlfcn.h>
 
 #include "adt.h"
 
@@ -36,7 +38,7 @@ static_assert(kTile == ADT_TILE_WEIGHTS, "tile size is part of the ABI");
 
 template <int MAXSEG>
 struct Table {
-    const uint8_t *packed_in;   // unpack source (device or mapped host)
+    const uint8_t *srcs[ADT_MAX_SOURCES];  // unpack sources (device, peer-mapped or pinned host)
     uint8_t *packed_out;        // pack destination
     double *seg_sumsq;          // per-layer result (chunk-relative)
     double *partials;           // per-tile scratch (chunk-relative)
@@ -46,6 +48,7 @@ struct Table {
     uint64_t offset[MAXSEG];
     uintptr_t weights[MAXSEG];
     uint8_t round_to[MAXSEG];
+    uint8_t src_idx[MAXSEG];    // which srcs[] a layer's payload is read from (adt_unpack_multi)
 };
 
 // ----------------------------------------------------------- byte compaction
@@ -371,7 +374,7 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
     const int r = T.round_to[s];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g0 = warp * kWarpGroups + lane;
-    const uint8_t *src = T.packed_in + T.offset[s] + e0 * r;
+    const uint8_t *src = T.srcs[T.src_idx[s]] + T.offset[s] + e0 * r;
     uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
 
     if (m == kTile && r != 3) {
@@ -435,6 +438,18 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #include "adt_tma.cuh"
 
 namespace {
+
+// ------------------------------------------------------- small peer copies
+// dst[q*bytes + i] = srcs[q][offset + i]: gathers each rank's norm tail (a few
+// dozen bytes) out of its peer-mapped send buffer.
+struct SrcList {
+    const uint8_t *p[ADT_MAX_SOURCES];
+};
+__global__ void adt_copy_multi_param_kernel(uint8_t *dst, const __grid_constant__ SrcList S, uint64_t offset,
+                                            uint64_t bytes) {
+    const uint8_t *src = S.p[blockIdx.x] + offset;
+    for (uint64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[blockIdx.x * bytes + i] = src[i];
+}
 
 // ----------------------------------------------------------------- host side
 enum class Pass { Pack, PackNorm, Norm, Unpack, Finalize };
@@ -518,13 +533,15 @@ cudaError_t launch_finalize(const Table<MAXSEG> &T, bool pdl, cudaStream_t strea
     return cudaLaunchKernelEx(&cfg, adt_norm_finalize_kernel<MAXSEG>, T);
 }
 
-int validate(const adt_segment *segs, int nseg, const void *packed, bool need_packed) {
+// nsrc == 0: `reserved` must be 0 (single packed buffer); otherwise it names
+// the source buffer (adt_unpack_multi) and must be < nsrc.
+int validate(const adt_segment *segs, int nseg, const void *packed, bool need_packed, int nsrc = 0) {
     if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
     bool any = false;
     for (int i = 0; i < nseg; ++i) {
         const adt_segment &g = segs[i];
         if (g.round_to < 1 || g.round_to > 4) return ADT_ERR_ROUND_TO;
-        if (g.reserved != 0) return ADT_ERR_ARG;
+        if (nsrc == 0 ? g.reserved != 0 : (g.reserved < 0 || g.reserved >= nsrc)) return ADT_ERR_ARG;
         if (g.count == 0) continue;
         any = true;
         if (g.weights == nullptr) return ADT_ERR_ARG;
@@ -540,10 +557,11 @@ int validate(const adt_segment *segs, int nseg, const void *packed, bool need_pa
 }
 
 template <int MAXSEG>
-int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
-                 double *seg_sumsq, double *partials, uint32_t ntiles, bool finalize, cudaStream_t stream) {
+int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc,
+                 uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, bool finalize,
+                 cudaStream_t stream) {
     Table<MAXSEG> T;
-    T.packed_in = pin;
+    for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = (srcs != nullptr && i < nsrc) ? srcs[i] : nullptr;
     T.packed_out = pout;
     T.seg_sumsq = seg_sumsq;
     T.partials = partials;
@@ -556,6 +574,7 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pi
         T.offset[i] = segs[i].offset;
         T.weights[i] = reinterpret_cast<uintptr_t>(segs[i].weights);
         T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
+        T.src_idx[i] = static_cast<uint8_t>(pass == Pass::Unpack ? segs[i].reserved : 0);
     }
     T.tile_begin[nseg] = acc;
     cudaError_t e = cudaSuccess;
@@ -586,7 +605,7 @@ constexpr int kLargeSeg = 256;
 // Greedy chunking (<= kLargeSeg layers, < 2^31 tiles per launch); the partial
 // offsets of a chunk depend only on `segs`, so a separate finalize call
 // (adt_norm_finalize) walks exactly the chunks the pack pass wrote.
-int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_t *pout,
+int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc, uint8_t *pout,
         double *seg_sumsq, double *partials, bool finalize, void *stream_v) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
     uint64_t partial_base = 0;
@@ -603,8 +622,8 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *pin, uint8_
         double *ss = seg_sumsq ? seg_sumsq + base : nullptr;
         double *pp = partials ? partials + partial_base : nullptr;
         const int st = cnt <= kSmallSeg
-            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream)
-            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, pin, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream);
+            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream)
+            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream);
         if (st != ADT_OK) return st;
         partial_base += tiles * kWarpsPerTile;
         base += cnt;
@@ -646,26 +665,88 @@ int adt_pack(const adt_segment *segs, int nseg, uint8_t *packed, double *seg_sum
     const int v = validate(segs, nseg, packed, true);
     if (v != ADT_OK) return v;
     if (nseg > 0 && seg_sumsq != nullptr && partials == nullptr) return ADT_ERR_ARG;
-    return run(partials ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, packed, seg_sumsq, partials,
+    return run(partials ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, 0, packed, seg_sumsq, partials,
                seg_sumsq != nullptr, stream);
 }
 
 int adt_norm_finalize(const adt_segment *segs, int nseg, double *partials, double *seg_sumsq, void *stream) {
     if (nseg < 0 || (nseg > 0 && (segs == nullptr || partials == nullptr || seg_sumsq == nullptr))) return ADT_ERR_ARG;
-    return run(Pass::Finalize, segs, nseg, nullptr, nullptr, seg_sumsq, partials, true, stream);
+    return run(Pass::Finalize, segs, nseg, nullptr, 0, nullptr, seg_sumsq, partials, true, stream);
 }
 
 int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *stream) {
     const int v = validate(segs, nseg, packed, true);
     if (v != ADT_OK) return v;
-    return run(Pass::Unpack, segs, nseg, packed, nullptr, nullptr, nullptr, false, stream);
+    const uint8_t *srcs[1] = {packed};
+    return run(Pass::Unpack, segs, nseg, srcs, 1, nullptr, nullptr, nullptr, false, stream);
+}
+
+int adt_unpack_multi(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc, void *stream) {
+    if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nsrc; ++i)
+        if (reinterpret_cast<uintptr_t>(sources[i]) % 16) return ADT_ERR_ALIGN;
+    const int v = validate(segs, nseg, sources[0], false, nsrc);
+    if (v != ADT_OK) return v;
+    for (int i = 0; i < nseg; ++i)
+        if (segs[i].count > 0 && sources[segs[i].reserved] == nullptr) return ADT_ERR_ARG;
+    return run(Pass::Unpack, segs, nseg, sources, nsrc, nullptr, nullptr, nullptr, false, stream);
+}
+
+int adt_copy_multi(uint8_t *dst, const uint8_t *const *sources, int nsrc, uint64_t offset, uint64_t bytes,
+                   void *stream) {
+    if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr || dst == nullptr) return ADT_ERR_ARG;
+    SrcList S;
+    for (int i = 0; i < ADT_MAX_SOURCES; ++i) S.p[i] = i < nsrc ? sources[i] : nullptr;
+    for (int i = 0; i < nsrc; ++i)
+        if (S.p[i] == nullptr) return ADT_ERR_ARG;
+    if (bytes == 0) return ADT_OK;
+    adt_copy_multi_param_kernel<<<nsrc, 128, 0, static_cast<cudaStream_t>(stream)>>>(dst, S, offset, bytes);
+    return cuda_status(cudaGetLastError());
+}
+
+int adt_ipc_handle_bytes(void) { return static_cast<int>(sizeof(cudaIpcMemHandle_t)); }
+
+int adt_ipc_get_handle(void *dev_ptr, void *handle_out, uint64_t *offset_out) {
+    if (dev_ptr == nullptr || handle_out == nullptr || offset_out == nullptr) return ADT_ERR_ARG;
+    // The handle names the whole cudaMalloc allocation (a caching allocator may
+    // have carved dev_ptr out of a larger segment): report dev_ptr's offset in it.
+    // The allocation base comes from the driver (cuPointerGetAttribute, resolved
+    // with dlsym so the library still loads on machines without a driver).
+    using GetAttr = int (*)(void *, int, unsigned long long);
+    static GetAttr get_attr = [] {
+        void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        return h ? reinterpret_cast<GetAttr>(dlsym(h, "cuPointerGetAttribute")) : nullptr;
+    }();
+    if (get_attr == nullptr) return ADT_ERR_NO_DEVICE;
+    unsigned long long base = 0;
+    const int kRangeStart = 11;  // CU_POINTER_ATTRIBUTE_RANGE_START_ADDR
+    if (get_attr(&base, kRangeStart, reinterpret_cast<unsigned long long>(dev_ptr)) != 0 || base == 0)
+        return ADT_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+    if (e != cudaSuccess) return cuda_status(e);
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = reinterpret_cast<unsigned long long>(dev_ptr) - base;
+    return ADT_OK;
+}
+
+int adt_ipc_open(const void *handle, void **dev_ptr_out) {
+    if (handle == nullptr || dev_ptr_out == nullptr) return ADT_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    return cuda_status(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int adt_ipc_close(void *dev_ptr) {
+    if (dev_ptr == nullptr) return ADT_ERR_ARG;
+    return cuda_status(cudaIpcCloseMemHandle(dev_ptr));
 }
 
 int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *partials, void *stream) {
     const int v = validate(segs, nseg, nullptr, false);
     if (v != ADT_OK) return v;
     if (nseg > 0 && (seg_sumsq == nullptr || partials == nullptr)) return ADT_ERR_ARG;
-    return run(Pass::Norm, segs, nseg, nullptr, nullptr, seg_sumsq, partials, true, stream);
+    return run(Pass::Norm, segs, nseg, nullptr, 0, nullptr, seg_sumsq, partials, true, stream);
 }
 
 int adt_device_sm_count(int *sm_count) {

@@ -246,7 +246,7 @@ adt_unpack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) 
                 const uint32_t bytes = (ti.m * ti.r / 16) * 16;
                 if (bytes) {
                     mbar_expect_tx(&S.full[st], bytes);
-                    bulk_g2s(S.stage[st], T.packed_in + T.offset[ti.s] + ti.e0 * ti.r, bytes, &S.full[st]);
+                    bulk_g2s(S.stage[st], T.srcs[T.src_idx[ti.s]] + T.offset[ti.s] + ti.e0 * ti.r, bytes, &S.full[st]);
                 } else {
                     mbar_arrive(&S.full[st]);
                 }
@@ -265,7 +265,7 @@ adt_unpack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) 
         if (ti.m < kTile) {
             // ragged tail: the last (< 16) payload bytes come straight from global
             const uint32_t nbytes = ti.m * r, done = (nbytes / 16) * 16;
-            const uint8_t *src = T.packed_in + T.offset[ti.s] + ti.e0 * r;
+            const uint8_t *src = T.srcs[T.src_idx[ti.s]] + T.offset[ti.s] + ti.e0 * r;
             uint8_t *s1 = reinterpret_cast<uint8_t *>(stg);
             if (threadIdx.x < nbytes - done) s1[done + threadIdx.x] = src[done + threadIdx.x];
             consumer_sync(2);

@@ -50,14 +50,16 @@ class SegmentTable:
     long-lived callers (WeightSync, bench) build it once and reuse it.
     """
 
-    def __init__(self, weights: Sequence[torch.Tensor], layout: PackedLayout):
+    def __init__(self, weights: Sequence[torch.Tensor], layout: PackedLayout, sources: Sequence[int] | None = None):
+        """`sources[l]`: index of the buffer layer l's payload lives in (unpack_multi)."""
         if len(weights) != layout.num_layers:
             raise ValueError(f"{len(weights)} tensors for a {layout.num_layers}-layer layout")
         self.layout = layout
         self.tensors = list(weights)  # keep alive
+        src = list(sources) if sources is not None else [0] * layout.num_layers
         segs = []
         for i, (t, n, off, r) in enumerate(zip(weights, layout.counts, layout.offsets, layout.round_tos)):
-            segs.append((_check_weight(t, n, f"layer {i}"), n, off, r))
+            segs.append((_check_weight(t, n, f"layer {i}"), n, off, r, src[i]))
         self.nseg = len(segs)
         self.array = _lib.segment_array(segs)
         self.npartials = _lib.partials_count(self.array, self.nseg)
@@ -124,6 +126,43 @@ def unpack(table: SegmentTable, packed: torch.Tensor, stream: torch.cuda.Stream 
     if not packed.is_cuda and not packed.is_pinned():
         raise ValueError("packed must live on the device or in pinned (page-locked) host memory")
     _lib.check(_lib.load().adt_unpack(table.array, table.nseg, packed.data_ptr(), stream_handle(stream)))
+
+
+def unpack_multi(table: SegmentTable, sources: Sequence[int], stream: torch.cuda.Stream | None = None) -> None:
+    """adt_unpack_multi: layer l's payload read from sources[table source index]
+    (raw device addresses: local buffers or peer buffers mapped by ipc_open)."""
+    arr = _lib.pointer_array(sources)
+    _lib.check(_lib.load().adt_unpack_multi(table.array, table.nseg, arr, len(sources), stream_handle(stream)))
+
+
+def copy_multi(dst: torch.Tensor, sources: Sequence[int], offset: int, nbytes: int,
+               stream: torch.cuda.Stream | None = None) -> None:
+    """dst[q*nbytes:(q+1)*nbytes] = bytes [offset, offset+nbytes) of sources[q]."""
+    if dst.dtype != torch.uint8 or not dst.is_cuda or dst.numel() < nbytes * len(sources):
+        raise ValueError("dst must be a CUDA uint8 tensor of len(sources)*nbytes")
+    arr = _lib.pointer_array(sources)
+    _lib.check(_lib.load().adt_copy_multi(dst.data_ptr(), arr, len(sources), offset, nbytes, stream_handle(stream)))
+
+
+def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(CUDA IPC handle of the allocation holding `t`, t's byte offset inside it)."""
+    lib = _lib.load()
+    buf = ctypes.create_string_buffer(lib.adt_ipc_handle_bytes())
+    off = ctypes.c_uint64(0)
+    _lib.check(lib.adt_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation; returns its base device address here."""
+    lib = _lib.load()
+    out = ctypes.c_void_p(0)
+    _lib.check(lib.adt_ipc_open(ctypes.create_string_buffer(handle, len(handle)), ctypes.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.check(_lib.load().adt_ipc_close(ptr))
 
 
 def sumsq(table: SegmentTable, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:

@@ -105,17 +105,31 @@ class ShardPlan:
 
 
 class ShardedWeightSync:
-    """Per-step packed weight all-gather across the ranks of `group`.
+    """Per-step packed weight distribution across the ranks of `group`.
 
     `masters[l]` are this rank's FP32 master tensors (full layer shape; only
     this rank's shard ranges are read), `replicas[l]` receive every weight.
+
+    transport = "nccl": pack -> ncclAllGather(uint8) of the packed send
+        buffers -> unpack the gathered stream.
+    transport = "p2p": every rank's send buffer is mapped into every other
+        rank with CUDA IPC; after one stream-ordered barrier each rank unpacks
+        straight out of its peers' send buffers over NVLink
+        (adt_unpack_multi) — the gather and the unpack are one kernel, and the
+        gathered stream is never written to or re-read from HBM. Send buffers
+        alternate between two slots so one barrier per step covers both the
+        read-after-write and the write-after-read hazard.
     """
 
-    def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None):
+    def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None,
+                 transport: str = "nccl"):
         import torch.distributed as dist
         engine.require_cuda()
+        if transport not in ("nccl", "p2p"):
+            raise ValueError("transport must be 'nccl' or 'p2p'")
         self.dist = dist
         self.group = group
+        self.transport = transport
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.masters = [m.detach().reshape(-1) for m in masters]
@@ -127,58 +141,126 @@ class ShardedWeightSync:
             replicas = [torch.empty_like(m) for m in self.masters]
         self.replicas = [r.reshape(-1) for r in replicas]
         self.send = self.recv = None
+        self._slot = 0
+        self._peer = None      # p2p: per slot, every rank's send-buffer address in this process
+        self._opened = []
         self._plan(self.schedule.round_tos())
 
+    # ------------------------------------------------------------- planning
     def _plan(self, round_tos):
         from .layout import PackedLayout
         self.plan = ShardPlan.plan(self.counts, round_tos, self.world)
         S = self.plan.send_bytes
-        if self.send is None or self.send.numel() < S:
-            cap = ShardPlan.plan(self.counts, [4] * len(self.counts), self.world).send_bytes
-            self.send = torch.zeros(cap, dtype=torch.uint8, device=self.device)
-            # one rank: unpack straight from the send buffer (no gather, no copy)
-            self.recv = self.send if self.world == 1 else torch.zeros(cap * self.world, dtype=torch.uint8,
-                                                                       device=self.device)
+        if self.send is None or self.send[0].numel() < S:
+            cap = max(S, ShardPlan.plan(self.counts, [4] * len(self.counts), self.world).send_bytes)
+            self._alloc(cap)
+        if self.transport == "p2p":
+            need = self.world * 8 * self.plan.max_pieces
+            if getattr(self, "tails", None) is None or self.tails.numel() < need:
+                self.tails = torch.zeros(need, dtype=torch.uint8, device=self.device)
         mine = self.plan.pieces[self.rank]
-        # pack table over this rank's pieces (views into the masters)
         views = [self.masters[pc.layer][pc.lo:pc.hi] for pc in mine]
         lay = PackedLayout(tuple(pc.hi - pc.lo for pc in mine), tuple(self.plan.round_tos[pc.layer] for pc in mine),
                            tuple(pc.offset for pc in mine), self.plan.payload_cap)
         self.pack_table = engine.SegmentTable(views, lay)
-        # norm tail view inside the send buffer
-        self.tail = self.send[self.plan.payload_cap:self.plan.payload_cap + 8 * self.plan.max_pieces].view(torch.float64)
-        # unpack table over every rank's pieces in the gathered buffer
-        outs, cnt, rs, offs = [], [], [], []
+        outs, cnt, rs, offs, srcs = [], [], [], [], []
         for q in range(self.world):
             for pc in self.plan.pieces[q]:
                 outs.append(self.replicas[pc.layer][pc.lo:pc.hi])
                 cnt.append(pc.hi - pc.lo)
                 rs.append(self.plan.round_tos[pc.layer])
-                offs.append(q * S + pc.offset)
+                # nccl: offsets inside the gathered buffer; p2p: inside rank q's own send buffer
+                offs.append(pc.offset if self.transport == "p2p" else q * S + pc.offset)
+                srcs.append(q if self.transport == "p2p" else 0)
         self.unpack_layout = PackedLayout(tuple(cnt), tuple(rs), tuple(offs), S * self.world)
-        self.unpack_table = engine.SegmentTable(outs, self.unpack_layout)
+        self.unpack_table = engine.SegmentTable(outs, self.unpack_layout,
+                                                sources=srcs if self.transport == "p2p" else None)
+
+    def _alloc(self, cap: int) -> None:
+        nslots = 2 if self.transport == "p2p" else 1
+        self._close_peers()
+        self.send = [torch.zeros(cap, dtype=torch.uint8, device=self.device) for _ in range(nslots)]
+        if self.transport == "nccl":
+            # one rank: unpack straight from the send buffer (no gather, no copy)
+            self.recv = self.send[0] if self.world == 1 else torch.zeros(cap * self.world, dtype=torch.uint8,
+                                                                          device=self.device)
+            return
+        handles = [engine.ipc_handle(b) for b in self.send]
+        everyone = [None] * self.world
+        self.dist.all_gather_object(everyone, handles, group=self.group)
+        self._peer = []
+        for slot in range(nslots):
+            ptrs = []
+            for q in range(self.world):
+                if q == self.rank:
+                    ptrs.append(self.send[slot].data_ptr())
+                else:
+                    handle, offset = everyone[q][slot]
+                    base = engine.ipc_open(handle)
+                    self._opened.append(base)
+                    ptrs.append(base + offset)
+            self._peer.append(ptrs)
+
+    def _close_peers(self) -> None:
+        for p in self._opened:
+            engine.ipc_close(p)
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self._close_peers()
+        except Exception:
+            pass
 
     @property
     def round_tos(self) -> list[int]:
         return list(self.plan.round_tos)
 
+    # ------------------------------------------------------------- one step
+    def _barrier(self) -> None:
+        """Stream-ordered cross-rank barrier: every rank's pack is complete
+        (and its previous unpack, by stream order) before anyone reads."""
+        if self.dist.get_backend(self.group) == "nccl":
+            if not hasattr(self, "_flag"):
+                self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.dist.all_reduce(self._flag, group=self.group)
+        else:  # gloo (tests): host-side
+            torch.cuda.current_stream().synchronize()
+            self.dist.barrier(group=self.group)
+
     def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
-        """pack shard (norm finalized into the send tail) -> ncclAllGather -> unpack."""
+        """pack shard (norm finalized into the send tail) -> exchange -> unpack."""
         S = self.plan.send_bytes
-        send = self.send[:S]
-        recv = self.recv[:S * self.world]
-        engine.pack(self.pack_table, send, self.tail if fused_norm else None)
-        if self.world > 1:
-            self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        if self.transport == "nccl":
+            send, recv = self.send[0][:S], self.recv[:S * self.world]
+            engine.pack(self.pack_table, send, self._tail(send) if fused_norm else None)
+            if self.world > 1:
+                self.dist.all_gather_into_tensor(recv, send, group=self.group)
+            if mid_event is not None:
+                mid_event.record(torch.cuda.current_stream())
+            engine.unpack(self.unpack_table, recv)
+            return
+        slot = self._slot
+        self._slot ^= 1
+        send = self.send[slot]
+        engine.pack(self.pack_table, send, self._tail(send) if fused_norm else None)
+        self._barrier()
         if mid_event is not None:
             mid_event.record(torch.cuda.current_stream())
-        engine.unpack(self.unpack_table, recv)
+        if fused_norm:
+            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
+        engine.unpack_multi(self.unpack_table, self._peer[slot])
+
+    def _tail(self, send: torch.Tensor) -> torch.Tensor:
+        base = self.plan.payload_cap
+        return send[base:base + 8 * self.plan.max_pieces].view(torch.float64)
 
     def _norms(self) -> list[float]:
-        S = self.plan.send_bytes
-        base = self.plan.payload_cap
-        m = self.plan.max_pieces
-        g = self.recv[:S * self.world].view(self.world, S)[:, base:base + 8 * m].contiguous()
+        S, base, m = self.plan.send_bytes, self.plan.payload_cap, self.plan.max_pieces
+        if self.transport == "nccl":
+            g = self.recv[:S * self.world].view(self.world, S)[:, base:base + 8 * m].contiguous()
+        else:
+            g = self.tails[:self.world * 8 * m].view(self.world, 8 * m)
         tails = g.view(torch.float64).view(self.world, m).cpu().tolist()
         return [math.sqrt(v) for v in self.plan.combine_sumsq(tails)]
 

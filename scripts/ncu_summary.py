@@ -75,7 +75,8 @@ def traffic(rep, config):
     res = {}
     for r in rows:
         name = r[hdr.index("Kernel Name")]
-        short = "adt_unpack_kernel" if "unpack" in name else "adt_pack_kernel"
+        short = ("adt_unpack_kernel" if "unpack" in name else
+                 "adt_norm_finalize_kernel" if "finalize" in name else "adt_pack_kernel")
         rd = to_bytes(r[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_read.sum")])
         wr = to_bytes(r[hdr.index("dram__bytes_write.sum")], units[hdr.index("dram__bytes_write.sum")])
         res[short] = rd + wr

@@ -27,7 +27,8 @@ def lib():
 def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
         ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
-         "adt_sumsq", "adt_device_sm_count"])
+         "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
+         "adt_ipc_close", "adt_sumsq", "adt_device_sm_count"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -65,6 +66,12 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_unpack(bad_off, 1, 16, None) == lib.ADT_ERR_ALIGN
     assert h.adt_unpack(lib.segment_array([(16, 10, 0, 2)]), 1, 0, None) == lib.ADT_ERR_ARG
     assert h.adt_pack(None, -1, 0, None, None, None) == lib.ADT_ERR_ARG
+    # unpack_multi: source index out of range / too many sources
+    seg = lib.segment_array([(16, 10, 0, 2, 1)])
+    assert h.adt_unpack_multi(seg, 1, lib.pointer_array([16]), 1, None) == lib.ADT_ERR_ARG
+    assert h.adt_unpack_multi(seg, 1, lib.pointer_array([16] * 17), 17, None) == lib.ADT_ERR_ARG
+    assert h.adt_unpack_multi(seg, 1, lib.pointer_array([16, 8]), 2, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_ipc_handle_bytes() == 64
     # sums requested without partials scratch
     assert h.adt_pack(lib.segment_array([(16, 10, 0, 2)]), 1, 16, 16, None, None) == lib.ADT_ERR_ARG
     assert h.adt_norm_finalize(lib.segment_array([(16, 10, 0, 2)]), 1, None, 16, None) == lib.ADT_ERR_ARG

@@ -1,0 +1,129 @@
+"""GPU tests of the multi-rank path on ONE device (the boxes have one GPU).
+
+* virtual ranks in one process: every rank's packed send buffer is a local
+  allocation; adt_unpack_multi must reassemble the reference's bytes;
+* two processes sharing cuda:0 (gloo for the host-side exchange): the real
+  ShardedWeightSync(transport="p2p") path — CUDA IPC mapping of the peer's send
+  buffers, the peer-read norm tails and the fused gather-unpack — against the
+  oracle, including an AWP escalation that re-plans the shards.
+"""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import weightpack_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def adt():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2004_02297_b200 as adt
+    return adt
+
+
+def test_unpack_multi_virtual_ranks(adt):
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    from paper_2004_02297_b200.sharded import ShardPlan
+    rng = np.random.default_rng(4)
+    counts = [500, 25000, 3 * 4096 + 17, 5000, 9 * 4096]
+    rs = [1, 2, 3, 4, 2]
+    hosts = [rng.integers(0, 1 << 32, n, dtype=np.uint32).view(np.float32) for n in counts]
+    world = 3
+    plan = ShardPlan.plan(counts, rs, world)
+    bufs = []
+    for q in range(world):
+        b = np.zeros(plan.send_bytes, np.uint8)
+        for pc in plan.pieces[q]:
+            pay = np.frombuffer(O.pack_vectorized(hosts[pc.layer][pc.lo:pc.hi], rs[pc.layer]), np.uint8)
+            b[pc.offset:pc.offset + pay.size] = pay
+        bufs.append(torch.from_numpy(b).cuda())
+    outs = [torch.empty(n, dtype=torch.float32, device="cuda") for n in counts]
+    views, cnt, rr, offs, srcs = [], [], [], [], []
+    for q in range(world):
+        for pc in plan.pieces[q]:
+            views.append(outs[pc.layer][pc.lo:pc.hi])
+            cnt.append(pc.hi - pc.lo)
+            rr.append(rs[pc.layer])
+            offs.append(pc.offset)
+            srcs.append(q)
+    lay = PackedLayout(tuple(cnt), tuple(rr), tuple(offs), plan.send_bytes)
+    engine.unpack_multi(engine.SegmentTable(views, lay, sources=srcs), [b.data_ptr() for b in bufs])
+    torch.cuda.synchronize()
+    for h, r, o in zip(hosts, rs, outs):
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2004_02297_b200 as adt
+        from paper_2004_02297_b200.sharded import ShardedWeightSync
+        counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
+        rng = np.random.default_rng(11)
+        hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+        masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+        cfg = adt.PrecisionConfig(threshold=-1e-3, interval=1, step_bits=8, initial_bits=8)
+        sync = ShardedWeightSync(masters, adt.PrecisionController(len(counts), cfg), transport="p2p")
+        ok, notes, norms_seen = True, [], []
+        for step in range(4):
+            res = sync.step(batch=step)
+            torch.cuda.synchronize()
+            for i, (h, r) in enumerate(zip(hosts, res.round_tos)):
+                want = h.view(np.uint32) & np.uint32(O.keep_mask(r))
+                if not np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want):
+                    ok = False
+                    notes.append(f"step {step} layer {i} r={r} replica mismatch")
+            for row in res.trace:
+                ref = O.l2_norm(hosts[row[1]])
+                if abs(row[2] - ref) > 1e-12 * ref:
+                    ok = False
+                    notes.append(f"norm {row}")
+                norms_seen.append(row[2])
+            # shrink every layer by 1% -> delta < threshold -> escalation each step (re-plan)
+            for m, h in zip(masters, hosts):
+                h *= np.float32(0.99)
+                m.copy_(torch.from_numpy(h))
+        q.put((rank, ok, notes, norms_seen, sync.round_tos))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surface child failures to the parent
+        q.put((rank, False, [repr(e)], [], []))
+
+
+def test_p2p_sync_two_processes_one_gpu():
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, notes, _, _ in res:
+        assert ok, (rank, notes[:5])
+    assert res[0][3] == res[1][3] and len(res[0][3]) > 0   # identical norm bits on both ranks
+    assert res[0][4] == res[1][4] and max(res[0][4]) > 1    # both escalated identically
