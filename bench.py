@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-norm", action="store_true", help="A/B only: pack without the fused l2-norm")
     ap.add_argument("--eager", action="store_true", help="launch each step eagerly instead of from CUDA graphs")
     ap.add_argument("--no-h2d", action="store_true", help="skip the pinned host->device comparison")
+    ap.add_argument("--no-sgd", action="store_true", help="skip the fused SGD+pack comparison")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
                     help="N > 1: ncclAllGather of packed bytes, or fused peer-read gather-unpack (CUDA IPC)")
     return ap.parse_args()
@@ -311,6 +312,9 @@ def main_ours(args):
     h2d = None
     if not args.no_h2d and world == 1:
         h2d = run_h2d(sync)
+    sgd = None
+    if not args.no_sgd and world == 1:
+        sgd = run_sgd_compare(masters, rs, dev)
     fp32_gather = None
     if world > 1:
         fp32_gather = run_fp32_allgather(counts, world, dev)
@@ -332,6 +336,7 @@ def main_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
+            "fused_sgd_pack": sgd,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -396,6 +401,43 @@ def run_h2d(sync, reps=10):
     return {"raw_fp32_ms": t_raw, "adt_copy_unpack_ms": t_cu, "adt_zero_copy_unpack_ms": t_zc,
             "raw_fp32_GBps": raw_b / t_raw / 1e6, "packed_bytes": pk_b, "raw_bytes": raw_b,
             "payload_ratio": raw_b / pk_b, "speedup_vs_fp32": t_raw / min(t_cu, t_zc)}
+
+
+def run_sgd_compare(dev_masters, rs, dev, reps=20):
+    """momentum-SGD step fused with pack + norm (adt_sgd_pack,
+    one pass: read W, v, g; write W, v, packed) vs the unfused sequence
+    (the same update as four in-place torch kernels, then adt_pack with the
+    norm). Algorithmic bytes per weight: fused 20 + r; unfused 24 + r."""
+    import torch
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    lay = PackedLayout.plan([m.numel() for m in dev_masters], rs)
+    w = [m.clone() for m in dev_masters]
+    v = [torch.zeros_like(m) for m in dev_masters]
+    g = [torch.randn_like(m) * 0.01 for m in dev_masters]
+    packed = torch.empty(lay.nbytes, dtype=torch.uint8, device=dev)
+    ss = torch.empty(len(w), dtype=torch.float64, device=dev)
+    fused_t = engine.SgdTable(w, v, g, lay)
+    pack_t = engine.SegmentTable(w, lay)
+    lr, mu, wd = 1e-4, 0.9, 5e-4
+
+    def fused():
+        engine.sgd_pack(fused_t, lr, mu, wd, packed, ss)
+
+    def unfused():
+        for wi, vi, gi in zip(w, v, g):
+            gi2 = gi.add(wi, alpha=wd)   # g + wd*W (alpha-scaled add)
+            vi.mul_(mu).add_(gi2)
+            wi.sub_(vi, alpha=lr)
+        engine.pack(pack_t, packed, ss)
+
+    tf, tu = _time_ms(fused, reps), _time_ms(unfused, reps)
+    n = sum(lay.counts)
+    pb = lay.total_payload_bytes
+    return {"fused_ms": tf, "unfused_ms": tu, "speedup": tu / tf,
+            "fused_GBps": (20 * n + pb) / (tf * 1e-3) / 1e9,
+            "note": "fused: adt_sgd_pack (update + pack + norm, 20+r B/weight); unfused: torch in-place update "
+                    "kernels + adt_pack"}
 
 
 def run_fp32_allgather(counts, world, dev, reps=20):

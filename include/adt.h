@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 4
+#define ADT_ABI_VERSION 5
 
 /* status codes */
 #define ADT_OK 0
@@ -57,6 +57,17 @@ typedef struct adt_segment {
     int32_t round_to;   /* bytes kept per weight, 1..4 (codec.py:52-57; bits_to_round_to codec.py:60-67) */
     int32_t reserved;   /* 0; for adt_unpack_multi: index of the source buffer holding this payload */
 } adt_segment;
+
+/* One layer of the fused SGD step + pack (adt_sgd_pack). */
+typedef struct adt_sgd_segment {
+    void *weights;      /* FP32 master W, updated in place (16-B aligned) */
+    void *velocity;     /* FP32 momentum buffer v, updated in place */
+    const void *grad;   /* FP32 averaged gradient g */
+    uint64_t count;
+    uint64_t offset;    /* payload offset of the packed W' in the packed buffer (16-B aligned) */
+    int32_t round_to;
+    int32_t reserved;   /* must be 0 */
+} adt_sgd_segment;
 
 /* ABI version (ADT_ABI_VERSION). */
 int adt_abi_version(void);
@@ -132,6 +143,18 @@ int adt_ipc_close(void *dev_ptr);
  */
 int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq,
               double *partials, void *stream);
+
+/*
+ * Fused momentum-SGD step + pack + norm. Per weight, in
+ * float32 with the reference's rounding at every operation (net.py:236-246):
+ *   g' = g + weight_decay*W (only if weight_decay != 0); v = v*momentum + g';
+ *   W = W - lr*v
+ * then W's top round_to bytes go to the packed buffer and, with partials /
+ * seg_sumsq, W's float64 sums of squares are fused in (as adt_pack). One pass
+ * reads W, v, g (12 B/weight) and writes W, v, packed (8 + r B/weight).
+ */
+int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
+                 uint8_t *packed, double *seg_sumsq, double *partials, void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

@@ -213,3 +213,20 @@ def lenet_walk(steps=200, seed=7):
         f = (1.0 + rng.uniform(-0.015, 0.012, size=len(ws))).astype(np.float32)
         ws = [w * f[i] for i, w in enumerate(ws)]
         yield t, ws
+
+
+# ------------------------------------------------- SGD step
+def sgd_step(w, v, g, lr, momentum, weight_decay):
+    """net.py:236-246, weight half of gather_and_update for one averaged
+    gradient: float32 arrays, rounding after every operation.
+    Returns (new weights, new velocity)."""
+    f = np.float32
+    w = np.array(w, dtype=np.float32, copy=True)
+    v = np.array(v, dtype=np.float32, copy=True)
+    g = np.array(g, dtype=np.float32, copy=True)
+    if weight_decay:
+        g += f(weight_decay) * w
+    v *= f(momentum)
+    v += g
+    w -= f(lr) * v
+    return w, v

@@ -40,6 +40,6 @@ from .precision import (  # noqa: F401
     change_rate,
     l2_norm,
 )
-from .sync import SyncResult, WeightSync  # noqa: F401
+from .sync import NonFiniteParameters, SyncResult, WeightSync  # noqa: F401
 
 __version__ = "0.1.0"

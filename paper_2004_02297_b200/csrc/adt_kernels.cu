@@ -264,6 +264,54 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
     for (uint32_t i = n16 * 16 + lane; i < nbytes; i += 32) dst[i] = s1[i];
 }
 
+// Write a tile's packed bytes (the r top bytes of each of the thread's 16 words).
+// r = 1/2/4 full tiles: coalesced 32/64/128-bit stores straight from registers;
+// r = 3 and ragged tiles: the warp's span via its staging words, 16-B vectors.
+__device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec], uint32_t m, int r, int warp,
+                                             int lane, uint32_t g0, uint32_t *ws) {
+    if (m == kTile && r != 3) {
+        if (r == 1) {
+            uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); d[g0 + 32 * k] = o[0]; }
+        } else if (r == 2) {
+            uint2 *d = reinterpret_cast<uint2 *>(dst);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); d[g0 + 32 * k] = make_uint2(o[0], o[1]); }
+        } else {
+            uint4 *d = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) { uint32_t o[4]; pack_r4(v[k], o); d[g0 + 32 * k] = make_uint4(o[0], o[1], o[2], o[3]); }
+        }
+        return;
+    }
+    if (r == 3) {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            uint32_t o[3];
+            pack_r3(v[k], o);
+            uint32_t *p = ws + (lane + 32 * k) * 3;   // stride 3: conflict-free
+            p[0] = o[0]; p[1] = o[1]; p[2] = o[2];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            uint32_t o[4];
+            pack_any(r, v[k], o);
+            uint32_t *p = ws + (lane + 32 * k) * r;
+            p[0] = o[0];
+            if (r > 1) p[1] = o[1];
+            if (r > 2) p[2] = o[2];
+            if (r > 3) p[3] = o[3];
+        }
+    }
+    __syncwarp();
+    const uint32_t span = kWarpGroups * 4 * r;            // the warp's packed bytes
+    const uint32_t lo = warp * span, nbytes = m * r;
+    if (lo < nbytes) warp_store_bytes(ws, dst + lo, min(span, nbytes - lo), lane);
+    __syncwarp();
+}
+
 // WRITE=false is the norm-only pass (adt_sumsq).
 #ifndef ADT_PACK_MIN_BLOCKS
 #define ADT_PACK_MIN_BLOCKS 6   // resident CTAs/SM the register budget must allow (A/B: profiles/r01_ab_occupancy.md)
@@ -301,50 +349,7 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
         }
     }
 
-    if (WRITE) {
-        uint8_t *dst = T.packed_out + T.offset[s] + e0 * r;
-        if (m == kTile && r != 3) {
-            if (r == 1) {
-                uint32_t *d = reinterpret_cast<uint32_t *>(dst);
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); d[g0 + 32 * k] = o[0]; }
-            } else if (r == 2) {
-                uint2 *d = reinterpret_cast<uint2 *>(dst);
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); d[g0 + 32 * k] = make_uint2(o[0], o[1]); }
-            } else {
-                uint4 *d = reinterpret_cast<uint4 *>(dst);
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) { uint32_t o[4]; pack_r4(v[k], o); d[g0 + 32 * k] = make_uint4(o[0], o[1], o[2], o[3]); }
-            }
-        } else {
-            uint32_t *ws = stage[warp];
-            if (r == 3) {
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) {
-                    uint32_t o[3];
-                    pack_r3(v[k], o);
-                    uint32_t *p = ws + (lane + 32 * k) * 3;   // stride 3: conflict-free
-                    p[0] = o[0]; p[1] = o[1]; p[2] = o[2];
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) {
-                    uint32_t o[4];
-                    pack_any(r, v[k], o);
-                    uint32_t *p = ws + (lane + 32 * k) * r;
-                    p[0] = o[0];
-                    if (r > 1) p[1] = o[1];
-                    if (r > 2) p[2] = o[2];
-                    if (r > 3) p[3] = o[3];
-                }
-            }
-            __syncwarp();
-            const uint32_t span = kWarpGroups * 4 * r;            // the warp's packed bytes
-            const uint32_t lo = warp * span, nbytes = m * r;
-            if (lo < nbytes) warp_store_bytes(ws, dst + lo, min(span, nbytes - lo), lane);
-        }
-    }
+    if (WRITE) store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, stage[warp]);
 
     if (NORM) warp_partial(T.partials, tile, sumsq16(v));
 }
@@ -431,6 +436,91 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
             if (g * 4 + 2 < m) dst1[g * 4 + 2] = o.z;
         }
     }
+}
+
+
+// ------------------------------------------------- fused SGD update + pack
+// the momentum-SGD step right before the path
+// (net.py:236-246, weight half) fused with the pack and the norm: one pass
+// reads W, v, g and writes W', v' and W''s packed bytes + norm partials, so
+// the updated master is never re-read. Per weight, float32 with the
+// reference's rounding at every operation (no FMA contraction):
+//   g' = g + wd*W   (only when wd != 0)   v' = v*mu + g'   W' = W - lr*v'
+template <int MAXSEG>
+struct SgdTable : Table<MAXSEG> {
+    uintptr_t velocity[MAXSEG];
+    uintptr_t grad[MAXSEG];
+    float lr, momentum, weight_decay;
+};
+
+__device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb, float lr, float mu, float wd) {
+    const float w = __uint_as_float(wb);
+    float g = __uint_as_float(gb);
+    if (wd != 0.0f) g = __fadd_rn(g, __fmul_rn(wd, w));
+    const float v = __fadd_rn(__fmul_rn(__uint_as_float(vb), mu), g);
+    vb = __float_as_uint(v);
+    return __float_as_uint(__fsub_rn(w, __fmul_rn(lr, v)));
+}
+
+#ifndef ADT_SGD_MIN_BLOCKS
+#define ADT_SGD_MIN_BLOCKS 4
+#endif
+template <int MAXSEG, bool NORM>
+__global__ void __launch_bounds__(kThreads, ADT_SGD_MIN_BLOCKS)
+adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    const uint32_t tile = blockIdx.x;
+    const int s = find_segment(T, tile);
+    const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
+    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
+    const int r = T.round_to[s];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t g0 = warp * kWarpGroups + lane;
+    uint4 *wp = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
+    uint4 *vp = reinterpret_cast<uint4 *>(T.velocity[s]) + e0 / 4;
+    const uint4 *gp = reinterpret_cast<const uint4 *>(T.grad[s]) + e0 / 4;
+    const float lr = T.lr, mu = T.momentum, wd = T.weight_decay;
+
+    uint4 w[kVec], v[kVec], g[kVec];
+    if (m == kTile) {
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            w[k] = __ldcs(wp + g0 + 32 * k);
+            v[k] = __ldcs(vp + g0 + 32 * k);
+            g[k] = __ldcs(gp + g0 + 32 * k);
+        }
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            w[k].x = sgd1(w[k].x, v[k].x, g[k].x, lr, mu, wd);
+            w[k].y = sgd1(w[k].y, v[k].y, g[k].y, lr, mu, wd);
+            w[k].z = sgd1(w[k].z, v[k].z, g[k].z, lr, mu, wd);
+            w[k].w = sgd1(w[k].w, v[k].w, g[k].w, lr, mu, wd);
+            wp[g0 + 32 * k] = w[k];
+            vp[g0 + 32 * k] = v[k];
+        }
+    } else {
+        uint32_t *w1 = reinterpret_cast<uint32_t *>(wp), *v1 = reinterpret_cast<uint32_t *>(vp);
+        const uint32_t *g1 = reinterpret_cast<const uint32_t *>(gp);
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
+            const uint32_t i = (g0 + 32 * k) * 4;
+            uint32_t ww[4], vv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                ww[j] = 0u;
+                vv[j] = 0u;
+                if (i + j < m) {
+                    vv[j] = v1[i + j];
+                    ww[j] = sgd1(w1[i + j], vv[j], g1[i + j], lr, mu, wd);
+                    w1[i + j] = ww[j];
+                    v1[i + j] = vv[j];
+                }
+            }
+            w[k] = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+        }
+    }
+    store_packed(T.packed_out + T.offset[s] + e0 * r, w, m, r, warp, lane, g0, stage[warp]);
+    if (NORM) warp_partial(T.partials, tile, sumsq16(w));
 }
 
 }  // namespace
@@ -631,6 +721,68 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs
     return ADT_OK;
 }
 
+
+template <int MAXSEG>
+int launch_sgd_chunk(const adt_sgd_segment *segs, int nseg, uint8_t *pout, double *seg_sumsq, double *partials,
+                     uint32_t ntiles, float lr, float mu, float wd, cudaStream_t stream) {
+    SgdTable<MAXSEG> T;
+    for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = nullptr;
+    T.packed_out = pout;
+    T.seg_sumsq = seg_sumsq;
+    T.partials = partials;
+    T.nseg = nseg;
+    T.lr = lr;
+    T.momentum = mu;
+    T.weight_decay = wd;
+    uint32_t acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+        T.tile_begin[i] = acc;
+        acc += static_cast<uint32_t>((segs[i].count + kTile - 1) / kTile);
+        T.count[i] = segs[i].count;
+        T.offset[i] = segs[i].offset;
+        T.weights[i] = reinterpret_cast<uintptr_t>(segs[i].weights);
+        T.velocity[i] = reinterpret_cast<uintptr_t>(segs[i].velocity);
+        T.grad[i] = reinterpret_cast<uintptr_t>(segs[i].grad);
+        T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
+        T.src_idx[i] = 0;
+    }
+    T.tile_begin[nseg] = acc;
+    cudaError_t e = cudaSuccess;
+    if (ntiles > 0) {
+        if (partials) adt_sgd_pack_kernel<MAXSEG, true><<<ntiles, kThreads, 0, stream>>>(T);
+        else adt_sgd_pack_kernel<MAXSEG, false><<<ntiles, kThreads, 0, stream>>>(T);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && seg_sumsq != nullptr && nseg > 0)
+        e = launch_finalize<MAXSEG>(static_cast<const Table<MAXSEG> &>(T), true, stream);
+    return cuda_status(e);
+}
+
+int run_sgd(const adt_sgd_segment *segs, int nseg, uint8_t *pout, double *seg_sumsq, double *partials, float lr,
+            float mu, float wd, cudaStream_t stream) {
+    uint64_t partial_base = 0;
+    int base = 0;
+    while (base < nseg) {
+        int cnt = 0;
+        uint64_t tiles = 0;
+        while (base + cnt < nseg && cnt < kLargeSeg) {
+            const uint64_t t = (segs[base + cnt].count + kTile - 1) / kTile;
+            if (cnt > 0 && tiles + t > static_cast<uint64_t>(INT_MAX)) break;
+            tiles += t;
+            ++cnt;
+        }
+        double *ss = seg_sumsq ? seg_sumsq + base : nullptr;
+        double *pp = partials ? partials + partial_base : nullptr;
+        const int st = cnt <= kSmallSeg
+            ? launch_sgd_chunk<kSmallSeg>(segs + base, cnt, pout, ss, pp, static_cast<uint32_t>(tiles), lr, mu, wd, stream)
+            : launch_sgd_chunk<kLargeSeg>(segs + base, cnt, pout, ss, pp, static_cast<uint32_t>(tiles), lr, mu, wd, stream);
+        if (st != ADT_OK) return st;
+        partial_base += tiles * kWarpsPerTile;
+        base += cnt;
+    }
+    return ADT_OK;
+}
+
 }  // namespace
 
 // -------------------------------------------------------------------- C ABI
@@ -747,6 +899,30 @@ int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *part
     if (v != ADT_OK) return v;
     if (nseg > 0 && (seg_sumsq == nullptr || partials == nullptr)) return ADT_ERR_ARG;
     return run(Pass::Norm, segs, nseg, nullptr, 0, nullptr, seg_sumsq, partials, true, stream);
+}
+
+int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
+                 uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+    if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
+    if (nseg > 0 && seg_sumsq != nullptr && partials == nullptr) return ADT_ERR_ARG;
+    bool any = false;
+    for (int i = 0; i < nseg; ++i) {
+        const adt_sgd_segment &g = segs[i];
+        if (g.round_to < 1 || g.round_to > 4) return ADT_ERR_ROUND_TO;
+        if (g.reserved != 0) return ADT_ERR_ARG;
+        if (g.count == 0) continue;
+        any = true;
+        if (!g.weights || !g.velocity || !g.grad) return ADT_ERR_ARG;
+        if (reinterpret_cast<uintptr_t>(g.weights) % 16 || reinterpret_cast<uintptr_t>(g.velocity) % 16 ||
+            reinterpret_cast<uintptr_t>(g.grad) % 16 || g.offset % 16)
+            return ADT_ERR_ALIGN;
+        if (g.count > (UINT64_MAX - g.offset) / 4) return ADT_ERR_ARG;
+        if ((g.count + kTile - 1) / kTile > static_cast<uint64_t>(INT_MAX)) return ADT_ERR_ARG;
+    }
+    if (any && (packed == nullptr)) return ADT_ERR_ARG;
+    if (any && reinterpret_cast<uintptr_t>(packed) % 16) return ADT_ERR_ALIGN;
+    return run_sgd(segs, nseg, packed, seg_sumsq, partials, lr, momentum, weight_decay,
+                   static_cast<cudaStream_t>(stream));
 }
 
 int adt_device_sm_count(int *sm_count) {

@@ -65,6 +65,43 @@ class SegmentTable:
         self.npartials = _lib.partials_count(self.array, self.nseg)
 
 
+class SgdTable:
+    """A prepared adt_sgd_segment[] (masters, velocities, gradients, layout)."""
+
+    def __init__(self, masters, velocities, grads, layout: PackedLayout):
+        n = layout.num_layers
+        if not (len(masters) == len(velocities) == len(grads) == n):
+            raise ValueError("masters, velocities, grads and layout disagree on the layer count")
+        self.layout = layout
+        self.tensors = (list(masters), list(velocities), list(grads))
+        self.nseg = n
+        self.array = (_lib.SgdSegment * max(1, n))()
+        for i, (w, v, g, cnt, off, r) in enumerate(zip(masters, velocities, grads, layout.counts,
+                                                     layout.offsets, layout.round_tos)):
+            a = self.array[i]
+            a.weights = _check_weight(w, cnt, f"master {i}")
+            a.velocity = _check_weight(v, cnt, f"velocity {i}")
+            a.grad = _check_weight(g, cnt, f"grad {i}")
+            a.count, a.offset, a.round_to, a.reserved = cnt, off, r, 0
+        self.npartials = sum((c + _lib.TILE_WEIGHTS - 1) // _lib.TILE_WEIGHTS for c in layout.counts) \
+            * _lib.PARTIALS_PER_TILE
+
+
+def sgd_pack(table: SgdTable, lr: float, momentum: float, weight_decay: float, packed: torch.Tensor,
+             sumsq: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
+             partials: torch.Tensor | None = None) -> None:
+    """adt_sgd_pack: W, v updated in place (reference rounding), W' packed,
+    W' norm partials / per-layer sums fused in (see pack())."""
+    if packed.dtype != torch.uint8 or not packed.is_cuda or packed.numel() < table.layout.payload_end:
+        raise ValueError("packed must be a CUDA uint8 tensor covering every layer's payload")
+    sh = stream_handle(stream)
+    if partials is None and sumsq is not None:
+        partials = _Scratch.get(packed.device, sh, table.npartials)
+    _lib.check(_lib.load().adt_sgd_pack(table.array, table.nseg, float(lr), float(momentum), float(weight_decay),
+                                        packed.data_ptr(), sumsq.data_ptr() if sumsq is not None else None,
+                                        partials.data_ptr() if partials is not None else None, sh))
+
+
 class _Scratch:
     """Per (device, stream) norm scratch: the float64 partials of one pass."""
 

@@ -31,6 +31,10 @@ from .layout import PackedLayout
 from .precision import FixedPrecision, PrecisionController
 
 
+class NonFiniteParameters(FloatingPointError):
+    """net.py:20 — an update left a layer's weights outside the finite range."""
+
+
 @dataclass
 class SyncResult:
     round_tos: list[int]             # widths the replicas were produced with this step
@@ -66,6 +70,7 @@ class WeightSync:
         self._fin_pending = False
         self._partials = None
         self._graphs = None      # (key, pack graph, finalize+unpack graph)
+        self.velocities = None   # momentum buffers, created by the first update()
         self.device = dev
         self.layout = None
         self.packed = None
@@ -154,6 +159,50 @@ class WeightSync:
         if not observe:
             return res
         res.trace = self.schedule.observe_all(self._read_norms(), batch=batch - 1)
+        new = self.schedule.round_tos()
+        if new != used:
+            self._plan(new)
+            self.launch(fused_norm=False)
+            res.round_tos = new
+            res.repacked = True
+        return res
+
+    def update(self, grads: Sequence[torch.Tensor], lr: float, momentum: float = 0.9,
+               weight_decay: float = 5e-4, batch: int = 0) -> SyncResult:
+        """Fused optimizer step + distribution of the updated weights.
+
+        Reference order (training.py:240-254, then the next batch's :209-225):
+        update W_b -> W_{b+1} (net.py:236-246) -> l2-norms of W_{b+1} ->
+        observe (trace rows labelled `batch`) -> pack W_{b+1} at the new
+        widths -> unpack. Here one kernel does the update, packs W_{b+1} at
+        the widths in force and fuses its norms; the norms are observed and,
+        if a width escalated, W_{b+1} is re-packed (without updating again).
+        The replicas then hold batch b+1's weights.
+        """
+        if len(grads) != len(self.masters):
+            raise ValueError("one gradient tensor per layer")
+        if self.velocities is None:
+            self.velocities = [torch.zeros_like(m) for m in self.masters]
+        g = [t.detach().reshape(-1) for t in grads]
+        table = engine.SgdTable(self.masters, self.velocities, g, self.layout)
+        main = torch.cuda.current_stream()
+        if self._fin_pending:
+            main.wait_event(self._fin_done)
+        engine.sgd_pack(table, lr, momentum, weight_decay, self.packed, None, main, partials=self._partials)
+        self._side.wait_stream(main)
+        engine.finalize(self.pack_table, self._partials, self.sumsq, self._side)
+        self._fin_done.record(self._side)
+        self._fin_pending = True
+        engine.unpack(self.unpack_table, self.packed, main)
+        used = self.round_tos
+        res = SyncResult(round_tos=used)
+        norms = self._read_norms()
+        bad = [i for i, n in enumerate(norms) if not math.isfinite(n)]
+        if bad:
+            raise NonFiniteParameters(f"layer {bad[0]} parameters left the finite range")
+        if not self.adaptive:
+            return res
+        res.trace = self.schedule.observe_all(norms, batch=batch)
         new = self.schedule.round_tos()
         if new != used:
             self._plan(new)

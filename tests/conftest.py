@@ -54,3 +54,10 @@ def golden_awp():
 @pytest.fixture(scope="session")
 def golden_lenet():
     return dict(_load("golden_lenet.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_sgd():
+    g = _load("golden_sgd.npz")
+    return [dict(w=g[f"s{i}_w"], v=g[f"s{i}_v"], g=g[f"s{i}_g"], hp=tuple(float(x) for x in g[f"s{i}_hp"]),
+                 w1=g[f"s{i}_w1"], v1=g[f"s{i}_v1"]) for i in range(int(g["ncases"]))]

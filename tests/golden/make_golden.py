@@ -15,6 +15,8 @@ writes, next to this script:
 * golden_awp.npz    — controller traces (delta, counter, bits) for the
   reference tests' seeded norm walks (test_precision.py:175-202,
   test_acceptance.py:126-155) plus consecutive-mode and grouped variants.
+* golden_sgd.npz    — net.gather_and_update's weight/velocity step (net.py:236-246)
+  for the fused SGD + pack kernel.
 * golden_lenet.npz  — SURVEY.md §8d config 1: the LeNet weight set under a
   seeded multiplicative walk, 200 batches, driven in the reference's own
   order (training.py:209-254): pack every layer at the controller's widths
@@ -197,7 +199,31 @@ def lenet_case():
     }
 
 
+def sgd_cases():
+    """net.gather_and_update (net.py:203-257) on a one-layer network with one
+    gradient contribution: the weight/velocity update the fused kernel restates."""
+    from weightpack import net
+    out = {}
+    rng = np.random.default_rng(5)
+    cases = [((37, 41), 0.05, 0.9, 5e-4), ((128, 300), 1e-3, 0.9, 0.0), ((64, 65), 0.1, 0.0, 5e-4),
+             ((10, 4099), 0.02, 0.5, 1e-2)]
+    for i, (shape, lr, mom, wd) in enumerate(cases):
+        w = (rng.standard_normal(shape) * 0.1).astype(np.float32)
+        v = (rng.standard_normal(shape) * 0.01).astype(np.float32)
+        g = (rng.standard_normal(shape) * 0.05).astype(np.float32)
+        network = net.Network([net.Layer(w.copy(), np.zeros(shape[1], np.float32))])
+        state = net.SgdState(vel_weights=[v.copy()], vel_biases=[np.zeros(shape[1], np.float32)])
+        grads = net.GradientSet(weight_grads=[g.copy()], bias_grads=[np.zeros(shape[1], np.float32)], sample_count=1)
+        cfg = net.SgdConfig(learning_rate=lr, momentum=mom, weight_decay=wd)
+        net.gather_and_update(network, [grads], cfg, state, lr)
+        out.update({f"s{i}_w": w, f"s{i}_v": v, f"s{i}_g": g, f"s{i}_hp": np.array([lr, mom, wd]),
+                    f"s{i}_w1": network.layers[0].weights, f"s{i}_v1": state.vel_weights[0]})
+    out["ncases"] = np.array(len(cases))
+    return out
+
+
 def main():
+    np.savez_compressed(os.path.join(HERE, "golden_sgd.npz"), **sgd_cases())
     np.savez_compressed(os.path.join(HERE, "golden_codec.npz"), **codec_cases())
     np.savez_compressed(os.path.join(HERE, "golden_awp.npz"), **awp_cases())
     np.savez_compressed(os.path.join(HERE, "golden_lenet.npz"), **lenet_case())

@@ -28,7 +28,7 @@ def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
         ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
          "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
-         "adt_ipc_close", "adt_sumsq", "adt_device_sm_count"])
+         "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_device_sm_count"])
 
 
 def test_library_exports_every_declared_symbol(lib):

@@ -266,3 +266,60 @@ def test_graphed_step_matches_eager(adt):
         assert torch.equal(b.packed[lo:hi], eager[0][lo:hi])
     assert all(torch.equal(x, y) for x, y in zip(b.replicas, eager[1]))
     assert b._read_norms() == eager[2]
+
+
+# ------------------------------------------- fused SGD + pack
+def test_sgd_pack_matches_reference_update(adt, golden_sgd):
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    for i, c in enumerate(golden_sgd):
+        r = (i % 4) + 1
+        w = torch.from_numpy(c["w"].reshape(-1).copy()).cuda()
+        v = torch.from_numpy(c["v"].reshape(-1).copy()).cuda()
+        g = torch.from_numpy(c["g"].reshape(-1).copy()).cuda()
+        lay = PackedLayout.plan([w.numel()], [r])
+        packed = torch.zeros(lay.nbytes, dtype=torch.uint8, device="cuda")
+        ss = torch.empty(1, dtype=torch.float64, device="cuda")
+        engine.sgd_pack(engine.SgdTable([w], [v], [g], lay), *c["hp"], packed, ss)
+        torch.cuda.synchronize()
+        w1 = c["w1"].reshape(-1)
+        assert np.array_equal(w.cpu().numpy().view(np.uint32), w1.view(np.uint32)), i
+        assert np.array_equal(v.cpu().numpy().view(np.uint32), c["v1"].reshape(-1).view(np.uint32)), i
+        lo, hi = lay.span(0)
+        assert packed[lo:hi].cpu().numpy().tobytes() == O.pack_vectorized(w1, r), i
+        assert math.sqrt(float(ss.item())) == pytest.approx(O.l2_norm(w1), rel=1e-12)
+
+
+def test_weightsync_update_walk_matches_reference_order(adt):
+    """30 batches of momentum SGD with AWP through WeightSync.update (fused
+    update + pack + norm, repack on escalation) vs the oracle in the
+    reference's order: update -> norm -> observe -> pack at the new widths."""
+    rng = np.random.default_rng(21)
+    counts = [500, 25000, 4096 * 3 + 7, 5000]
+    L = len(counts)
+    hp = (0.05, 0.9, 5e-4)
+    w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+    v_ref = [np.zeros(n, np.float32) for n in counts]
+    grads = [[rng.standard_normal(n, dtype=np.float32) * np.float32(0.02) + np.float32(0.004)
+              for n in counts] for _ in range(30)]
+    kw = dict(threshold=-2e-3, interval=3, step_bits=8, initial_bits=8)
+    octl = O.OracleController(L, **kw)
+    masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
+    sync = adt.WeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)))
+    sync.step(batch=0)
+    for b in range(30):
+        res = sync.update([torch.from_numpy(x).cuda() for x in grads[b]], *hp, batch=b)
+        for i in range(L):
+            w_ref[i], v_ref[i] = O.sgd_step(w_ref[i], v_ref[i], grads[b][i], *hp)
+        for i in range(L):
+            octl.observe_layer(i, O.l2_norm(w_ref[i]))
+        rs = [octl.round_to(i) for i in range(L)]
+        assert res.round_tos == rs, b
+        for i in range(L):
+            assert np.array_equal(masters[i].cpu().numpy().view(np.uint32), w_ref[i].view(np.uint32)), (b, i)
+            lo, hi = sync.layout.span(i)
+            assert sync.packed[lo:hi].cpu().numpy().tobytes() == O.pack_vectorized(w_ref[i], rs[i]), (b, i)
+            want = w_ref[i].view(np.uint32) & np.uint32(O.keep_mask(rs[i]))
+            assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), (b, i)
+        assert [row[5] for row in res.trace] == [octl.bits[i] for i in range(L)]
+    assert max(sync.round_tos) > 1  # the walk exercised escalation

@@ -100,3 +100,10 @@ def test_c_oracle_matches_golden(golden_codec, golden_norms):
     for x, want in golden_norms:
         got = math.sqrt(C.sumsq(x))
         assert got == pytest.approx(want, rel=1e-12) or got == want == 0.0
+
+
+def test_sgd_step_matches_reference_update(golden_sgd):
+    for c in golden_sgd:
+        w1, v1 = O.sgd_step(c["w"], c["v"], c["g"], *c["hp"])
+        assert np.array_equal(w1.view(np.uint32), c["w1"].view(np.uint32))
+        assert np.array_equal(v1.view(np.uint32), c["v1"].view(np.uint32))
