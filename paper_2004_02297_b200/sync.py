@@ -111,28 +111,31 @@ class WeightSync:
         engine.unpack(self.unpack_table, self.packed, main)
 
     def launch_graphed(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
-        """launch() replayed from two CUDA graphs captured once per layout:
-        [pack (+partials)] then [fork: finalize on the side branch | unpack; join].
-        Removes the per-step host launch cost (ctypes + stream bookkeeping),
-        which matters for small sets (ResNet-50: 161 layers, ~40 us of HBM work)."""
-        key = (fused_norm, self.layout)
+        """launch() replayed from CUDA graphs captured once per layout: one
+        graph [pack -> fork(finalize on the side branch) | unpack -> join], or,
+        when the caller wants the pack/unpack split (`mid_event`), two graphs
+        with the event recorded between them. Removes the per-step host launch
+        cost (ctypes + stream bookkeeping): LeNet 39.6 -> 18.7 us per step."""
+        split = mid_event is not None
+        key = (fused_norm, split, self.layout)
         if self._graphs is None or self._graphs[0] != key:
-            self._graphs = (key,) + self._capture(fused_norm)
-        _, g_pack, g_rest = self._graphs
-        g_pack.replay()
-        if mid_event is not None:
+            self._graphs = (key, self._capture(fused_norm, split))
+        graphs = self._graphs[1]
+        graphs[0].replay()
+        if split:
             mid_event.record(torch.cuda.current_stream())
-        g_rest.replay()
+            graphs[1].replay()
 
-    def _capture(self, fused_norm: bool):
+    def _capture(self, fused_norm: bool, split: bool):
         self.launch(fused_norm)              # eager warm-up (lazy CUDA init, scratch)
         torch.cuda.synchronize()
         self._fin_pending = False
-        g_pack, g_rest = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_pack):
+
+        def pack():
             engine.pack(self.pack_table, self.packed, None, torch.cuda.current_stream(),
                         partials=self._partials if fused_norm else None)
-        with torch.cuda.graph(g_rest):
+
+        def rest():
             cap = torch.cuda.current_stream()
             if fused_norm:
                 self._side.wait_stream(cap)
@@ -140,6 +143,18 @@ class WeightSync:
             engine.unpack(self.unpack_table, self.packed, cap)
             if fused_norm:
                 cap.wait_stream(self._side)
+
+        if not split:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                pack()
+                rest()
+            return (g,)
+        g_pack, g_rest = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_pack):
+            pack()
+        with torch.cuda.graph(g_rest):
+            rest()
         return g_pack, g_rest
 
     def _read_norms(self) -> list[float]:

@@ -300,17 +300,18 @@ def test_weightsync_update_walk_matches_reference_order(adt):
     hp = (0.05, 0.9, 5e-4)
     w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
     v_ref = [np.zeros(n, np.float32) for n in counts]
-    grads = [[rng.standard_normal(n, dtype=np.float32) * np.float32(0.02) + np.float32(0.004)
-              for n in counts] for _ in range(30)]
+    noise = [[rng.standard_normal(n, dtype=np.float32) * np.float32(0.002) for n in counts] for _ in range(30)]
     kw = dict(threshold=-2e-3, interval=3, step_bits=8, initial_bits=8)
     octl = O.OracleController(L, **kw)
     masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
     sync = adt.WeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)))
     sync.step(batch=0)
     for b in range(30):
-        res = sync.update([torch.from_numpy(x).cuda() for x in grads[b]], *hp, batch=b)
+        # gradients pulling the weights toward zero (weight-decay-like): the norms shrink -> AWP escalates
+        grads = [np.float32(0.4) * w + noise[b][i] for i, w in enumerate(w_ref)]
+        res = sync.update([torch.from_numpy(x).cuda() for x in grads], *hp, batch=b)
         for i in range(L):
-            w_ref[i], v_ref[i] = O.sgd_step(w_ref[i], v_ref[i], grads[b][i], *hp)
+            w_ref[i], v_ref[i] = O.sgd_step(w_ref[i], v_ref[i], grads[i], *hp)
         for i in range(L):
             octl.observe_layer(i, O.l2_norm(w_ref[i]))
         rs = [octl.round_to(i) for i in range(L)]
