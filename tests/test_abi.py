@@ -72,6 +72,15 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_unpack_multi(seg, 1, lib.pointer_array([16] * 17), 17, None) == lib.ADT_ERR_ARG
     assert h.adt_unpack_multi(seg, 1, lib.pointer_array([16, 8]), 2, None) == lib.ADT_ERR_ALIGN
     assert h.adt_ipc_handle_bytes() == 64
+    # fused SGD + pack: bad width / misaligned velocity / sums without partials
+    def sgd(ptrs, r, off=0):
+        arr = (lib.SgdSegment * 1)()
+        arr[0].weights, arr[0].velocity, arr[0].grad = ptrs
+        arr[0].count, arr[0].offset, arr[0].round_to, arr[0].reserved = 10, off, r, 0
+        return arr
+    assert h.adt_sgd_pack(sgd((16, 32, 48), 5), 1, 0.1, 0.9, 0.0, 16, None, None, None) == lib.ADT_ERR_ROUND_TO
+    assert h.adt_sgd_pack(sgd((16, 40, 48), 2), 1, 0.1, 0.9, 0.0, 16, None, None, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_sgd_pack(sgd((16, 32, 48), 2), 1, 0.1, 0.9, 0.0, 16, 16, None, None) == lib.ADT_ERR_ARG
     # sums requested without partials scratch
     assert h.adt_pack(lib.segment_array([(16, 10, 0, 2)]), 1, 16, 16, None, None) == lib.ADT_ERR_ARG
     assert h.adt_norm_finalize(lib.segment_array([(16, 10, 0, 2)]), 1, None, 16, None) == lib.ADT_ERR_ARG

@@ -324,3 +324,30 @@ def test_weightsync_update_walk_matches_reference_order(adt):
             assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), (b, i)
         assert [row[5] for row in res.trace] == [octl.bits[i] for i in range(L)]
     assert max(sync.round_tos) > 1  # the walk exercised escalation
+
+
+def test_single_layer_beyond_4gb_packed_offsets(adt):
+    """A 1.5e9-weight layer at r = 3: payload offsets pass 4 GiB (64-bit tile
+    addressing). Spot windows against the oracle; the mask law over all of it."""
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    n, r = 1_500_000_003, 3
+    free, _ = torch.cuda.mem_get_info()
+    if free < 24 * (1 << 30):
+        pytest.skip("needs ~18 GB of free HBM")
+    g = torch.Generator(device="cuda").manual_seed(9)
+    bits = torch.randint(-(1 << 31), 1 << 31, (n,), dtype=torch.int32, device="cuda", generator=g)
+    w = bits.view(torch.float32)
+    lay = PackedLayout.plan([n], [r])
+    packed = torch.empty(lay.nbytes, dtype=torch.uint8, device="cuda")
+    engine.pack(engine.SegmentTable([w], lay), packed)
+    out = torch.empty_like(w)
+    engine.unpack(engine.SegmentTable([out], lay), packed)
+    torch.cuda.synchronize()
+    mask = torch.tensor(O.keep_mask(r) - (1 << 32), dtype=torch.int32, device="cuda")
+    assert torch.equal(out.view(torch.int32), bits & mask)
+    for start in (0, 4095, 1_431_655_760, n - 4100):   # 3*start crosses 2^32 at the third window
+        hw = w[start:start + 4100].cpu().numpy()
+        assert packed[3 * start:3 * (start + 4100)].cpu().numpy().tobytes() == O.pack_vectorized(hw, r)
+    del bits, w, out, packed
+    torch.cuda.empty_cache()
