@@ -211,10 +211,17 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ADT_BENCH_BACKEND=gloo (test hook): ranks may share one GPU; only the
+    # p2p transport runs there (NCCL refuses two ranks on one device).
+    backend = os.environ.get("ADT_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2004_02297_b200 as adt
     from paper_2004_02297_b200 import engine
@@ -282,7 +289,7 @@ def main_ours(args):
         dist.barrier()
     ms = e_start.elapsed_time(e_end) / K
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     total_bytes = (sum((4 + r) * n for n, r in zip(counts, rs))            # pack: every weight once (sharded)
@@ -320,7 +327,7 @@ def main_ours(args):
         sgd = run_sgd_compare(masters, rs, dev)
     fp32_gather = None
     if world > 1:
-        fp32_gather = run_fp32_allgather(counts, world, dev)
+        fp32_gather = run_fp32_allgather(counts, world, dev) if backend == "nccl" else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
