@@ -264,6 +264,9 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
     for (uint32_t i = n16 * 16 + lane; i < nbytes; i += 32) dst[i] = s1[i];
 }
 
+#ifndef ADT_PACK_BULK_STORE
+#define ADT_PACK_BULK_STORE 0
+#endif
 // Write a tile's packed bytes (the r top bytes of each of the thread's 16 words).
 // r = 1/2/4 full tiles: coalesced 32/64/128-bit stores straight from registers;
 // r = 3 and ragged tiles: the warp's span via its staging words, 16-B vectors.
@@ -305,10 +308,29 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
             if (r > 3) p[3] = o[3];
         }
     }
-    __syncwarp();
     const uint32_t span = kWarpGroups * 4 * r;            // the warp's packed bytes
     const uint32_t lo = warp * span, nbytes = m * r;
+#if ADT_PACK_BULK_STORE
+    // The warp's 16-B-multiple part leaves shared memory as ONE bulk async copy
+    // (cp.async.bulk shared->global, SASS UBLKCP) issued by lane 0; the ragged
+    // (< 16 B) tail of a layer goes out with plain stores.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // STS -> async proxy
+    __syncwarp();
+    if (lo < nbytes) {
+        const uint32_t mine = min(span, nbytes - lo), n16 = mine & ~15u;
+        if (lane == 0 && n16) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                         "cp.async.bulk.commit_group;\n\t"
+                         "cp.async.bulk.wait_group.read 0;" ::"l"(dst + lo),
+                         "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ws))), "r"(n16) : "memory");
+        }
+        const uint8_t *s1 = reinterpret_cast<const uint8_t *>(ws);
+        for (uint32_t i = n16 + lane; i < mine; i += 32) dst[lo + i] = s1[i];
+    }
+#else
+    __syncwarp();
     if (lo < nbytes) warp_store_bytes(ws, dst + lo, min(span, nbytes - lo), lane);
+#endif
     __syncwarp();
 }
 
