@@ -265,7 +265,7 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
 }
 
 #ifndef ADT_PACK_BULK_STORE
-#define ADT_PACK_BULK_STORE 0
+#define ADT_PACK_BULK_STORE 1   // A/B (profiles/r01_ab_bulk_store.md): 1B r=3 step 2308 -> 2183 us
 #endif
 // Write a tile's packed bytes (the r top bytes of each of the thread's 16 words).
 // r = 1/2/4 full tiles: coalesced 32/64/128-bit stores straight from registers;
