@@ -264,6 +264,9 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
     for (uint32_t i = n16 * 16 + lane; i < nbytes; i += 32) dst[i] = s1[i];
 }
 
+#ifndef ADT_PACK_STAGE_ALL
+#define ADT_PACK_STAGE_ALL 0    // A/B: route r = 1/2/4 full tiles through the staged (bulk-store) path too
+#endif
 #ifndef ADT_PACK_BULK_STORE
 #define ADT_PACK_BULK_STORE 1   // A/B (profiles/r01_ab_bulk_store.md): 1B r=3 step 2308 -> 2183 us
 #endif
@@ -272,7 +275,7 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
 // r = 3 and ragged tiles: the warp's span via its staging words, 16-B vectors.
 __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec], uint32_t m, int r, int warp,
                                              int lane, uint32_t g0, uint32_t *ws) {
-    if (m == kTile && r != 3) {
+    if (!ADT_PACK_STAGE_ALL && m == kTile && r != 3) {
         if (r == 1) {
             uint32_t *d = reinterpret_cast<uint32_t *>(dst);
 #pragma unroll
