@@ -276,15 +276,26 @@ def main_ours(args):
             run_step(fused)
         e_end.record(stream)
         torch.cuda.synchronize()
-    # pass 2 (per-kernel split for the roofline): K steps with an event between
-    # the pack and the unpack (two graphs per step), timed the same way
-    mids = [] if args.quiet_extra else [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-                                          torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    for k in range(len(mids)):
-        mids[k][0].record(stream)
-        run_step(fused, mid_event=mids[k][1])
-        mids[k][2].record(stream)
-    torch.cuda.synchronize()
+    # pass 2 (per-kernel split for the roofline). N = 1: the same one-graph
+    # step with timing events captured inside it (no host launch latency in the
+    # numbers), one replay at a time. N > 1 (eager): an event between the pack
+    # (+ gather) and the unpack of each step.
+    pk_list, up_list = [], []
+    if not args.quiet_extra:
+        if world == 1 and not args.eager:
+            for _ in range(min(K, 200)):
+                a_ms, b_ms = sync.timed_replay(fused)
+                pk_list.append(a_ms)
+                up_list.append(b_ms)
+        else:
+            for _ in range(K):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream)
+                run_step(fused, mid_event=e1)
+                e2.record(stream)
+                torch.cuda.synchronize()
+                pk_list.append(e0.elapsed_time(e1))
+                up_list.append(e1.elapsed_time(e2))
     if world > 1:
         dist.barrier()
     ms = e_start.elapsed_time(e_end) / K
@@ -297,9 +308,9 @@ def main_ours(args):
     value = total_bytes / (ms * 1e-3) / 1e9
 
     pk = up = None
-    if mids:
-        pk = sum(a.elapsed_time(b) for a, b, _ in mids) / K
-        up = sum(b.elapsed_time(c) for _, b, c in mids) / K
+    if pk_list:
+        pk = sum(pk_list) / len(pk_list)
+        up = sum(up_list) / len(up_list)
     hbm, peak_kind = peaks()
     roofline = None
     if pk is not None:
