@@ -127,36 +127,39 @@ class WeightSync:
             mid_event.record(torch.cuda.current_stream())
             graphs[1].replay()
 
-    def timed_replay(self, fused_norm: bool) -> tuple[float, float]:
-        """Replay the one-graph step with three external timing events captured
-        INSIDE it (before pack, between pack and unpack, after the join) and
-        return (pack ms, finalize||unpack ms) for that replay: per-kernel times
-        without any host launch latency in them. Synchronizes."""
-        key = ("timed", fused_norm, self.layout)
+    def timed_replay(self, fused_norm: bool, steps: int = 20) -> tuple[list[float], list[float]]:
+        """Replay `steps` back-to-back steps from ONE graph with external timing
+        events captured inside it around every pack and every finalize||unpack;
+        returns the per-step (pack ms, finalize||unpack ms). The steps run as in
+        the timed loop (no host gaps, no launch latency inside the numbers).
+        Synchronizes."""
+        key = ("timed", fused_norm, steps, self.layout)
         if getattr(self, "_timed", None) is None or self._timed[0] != key:
             self.launch(fused_norm)
             torch.cuda.synchronize()
             self._fin_pending = False
-            ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
+            ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * steps + 1)]
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 cap = torch.cuda.current_stream()
                 ev[0].record(cap)
-                engine.pack(self.pack_table, self.packed, None, cap,
-                            partials=self._partials if fused_norm else None)
-                ev[1].record(cap)
-                if fused_norm:
-                    self._side.wait_stream(cap)
-                    engine.finalize(self.pack_table, self._partials, self.sumsq, self._side)
-                engine.unpack(self.unpack_table, self.packed, cap)
-                if fused_norm:
-                    cap.wait_stream(self._side)
-                ev[2].record(cap)
+                for k in range(steps):
+                    engine.pack(self.pack_table, self.packed, None, cap,
+                                partials=self._partials if fused_norm else None)
+                    ev[2 * k + 1].record(cap)
+                    if fused_norm:
+                        self._side.wait_stream(cap)
+                        engine.finalize(self.pack_table, self._partials, self.sumsq, self._side)
+                    engine.unpack(self.unpack_table, self.packed, cap)
+                    if fused_norm:
+                        cap.wait_stream(self._side)
+                    ev[2 * k + 2].record(cap)
             self._timed = (key, g, ev)
         _, g, ev = self._timed
         g.replay()
-        ev[2].synchronize()
-        return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        ev[-1].synchronize()
+        return ([ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(steps)],
+                [ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(steps)])
 
     def _capture(self, fused_norm: bool, split: bool):
         self.launch(fused_norm)              # eager warm-up (lazy CUDA init, scratch)
