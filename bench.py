@@ -276,17 +276,16 @@ def main_ours(args):
             run_step(fused)
         e_end.record(stream)
         torch.cuda.synchronize()
-    # pass 2 (per-kernel split for the roofline). N = 1: the same one-graph
-    # step with timing events captured inside it (no host launch latency in the
-    # numbers), one replay at a time. N > 1 (eager): an event between the pack
-    # (+ gather) and the unpack of each step.
+    # pass 2 (per-kernel split for the roofline). N = 1: each phase of the step
+    # (pack | finalize||unpack) replayed back to back from a graph of 20 copies,
+    # two events around each replay batch (no launch latency, no event nodes
+    # between kernels). N > 1 (eager): an event between the pack (+ gather) and
+    # the unpack of each step.
     pk_list, up_list = [], []
     if not args.quiet_extra:
         if world == 1 and not args.eager:
-            for _ in range(max(1, min(K, 200) // 20)):
-                a_ms, b_ms = sync.timed_replay(fused, steps=20)
-                pk_list += a_ms[1:]          # the first step of each replay starts from idle
-                up_list += b_ms[1:]
+            a_ms, b_ms = sync.phase_ms(fused, reps=20, rounds=max(1, min(K, 200) // 20))
+            pk_list, up_list = [a_ms], [b_ms]
         else:
             for _ in range(K):
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))

@@ -127,39 +127,43 @@ class WeightSync:
             mid_event.record(torch.cuda.current_stream())
             graphs[1].replay()
 
-    def timed_replay(self, fused_norm: bool, steps: int = 20) -> tuple[list[float], list[float]]:
-        """Replay `steps` back-to-back steps from ONE graph with external timing
-        events captured inside it around every pack and every finalize||unpack;
-        returns the per-step (pack ms, finalize||unpack ms). The steps run as in
-        the timed loop (no host gaps, no launch latency inside the numbers).
-        Synchronizes."""
-        key = ("timed", fused_norm, steps, self.layout)
+    def phase_ms(self, fused_norm: bool, reps: int = 20, rounds: int = 5) -> tuple[float, float]:
+        """Average device time of each phase of the step, measured as `reps`
+        back-to-back copies of that phase in one CUDA graph timed by two events
+        outside it (event nodes inside a graph cost several us each, which would
+        distort short kernels): (pack ms, finalize||unpack ms). Synchronizes."""
+        key = ("phase", fused_norm, reps, self.layout)
         if getattr(self, "_timed", None) is None or self._timed[0] != key:
             self.launch(fused_norm)
             torch.cuda.synchronize()
             self._fin_pending = False
-            ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * steps + 1)]
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                cap = torch.cuda.current_stream()
-                ev[0].record(cap)
-                for k in range(steps):
-                    engine.pack(self.pack_table, self.packed, None, cap,
+            g_pack, g_rest = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_pack):
+                for _ in range(reps):
+                    engine.pack(self.pack_table, self.packed, None, torch.cuda.current_stream(),
                                 partials=self._partials if fused_norm else None)
-                    ev[2 * k + 1].record(cap)
+            with torch.cuda.graph(g_rest):
+                cap = torch.cuda.current_stream()
+                for _ in range(reps):
                     if fused_norm:
                         self._side.wait_stream(cap)
                         engine.finalize(self.pack_table, self._partials, self.sumsq, self._side)
                     engine.unpack(self.unpack_table, self.packed, cap)
                     if fused_norm:
                         cap.wait_stream(self._side)
-                    ev[2 * k + 2].record(cap)
-            self._timed = (key, g, ev)
-        _, g, ev = self._timed
-        g.replay()
-        ev[-1].synchronize()
-        return ([ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(steps)],
-                [ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(steps)])
+            self._timed = (key, g_pack, g_rest)
+        _, g_pack, g_rest = self._timed
+        out = []
+        for g in (g_pack, g_rest):
+            g.replay()                                   # warm
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(rounds):
+                g.replay()
+            b.record()
+            b.synchronize()
+            out.append(a.elapsed_time(b) / (rounds * reps))
+        return out[0], out[1]
 
     def _capture(self, fused_norm: bool, split: bool):
         self.launch(fused_norm)              # eager warm-up (lazy CUDA init, scratch)
