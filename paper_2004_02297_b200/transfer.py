@@ -52,3 +52,72 @@ def weight_stream_ratio(records) -> float:
     if wire == 0:
         raise ValueError("no to-worker weight transfers recorded")
     return raw / wire
+
+
+def _loop_ms(fn, reps: int = 20, rounds: int = 5) -> float:
+    """Device ms per call of `fn` (stream work only), from one CUDA graph of
+    `reps` back-to-back calls replayed `rounds` times between two events."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(rounds):
+        g.replay()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / (reps * rounds)
+
+
+def measured_profile(sync, bias_bytes=None) -> dict:
+    """The reference's per-phase profile (transfer.py:254-286, `profile_report`)
+    with MEASURED B200 device times in place of its LinkModel / CodecCostModel,
+    for one WeightSync step — the rows of the paper's Table 2:
+    pack (with and without the fused l2-norm), unpack, standalone l2-norm, and the
+    CPU->GPU weight transfer from pinned host memory, FP32 vs ADT-packed
+    (memcpy + unpack, and the zero-copy unpack)."""
+    import torch
+    from . import engine
+    lay = sync.layout
+    pack_norm, fin_unpack = sync.phase_ms(True)
+    pack_only, unpack_only = sync.phase_ms(False)
+    sums = torch.empty(len(sync.masters), dtype=torch.float64, device=sync.device)
+    norm_only = _loop_ms(lambda: engine.sumsq(sync.pack_table, sums))
+    host_packed = torch.empty(lay.nbytes, dtype=torch.uint8, pin_memory=True)
+    host_packed.copy_(sync.packed[:lay.nbytes])
+    dev_packed = torch.empty(lay.nbytes, dtype=torch.uint8, device=sync.device)
+    host_fp32 = [m.cpu().pin_memory() for m in sync.masters]
+    dev_fp32 = [torch.empty_like(m) for m in sync.masters]
+
+    def raw_h2d():
+        for d, h in zip(dev_fp32, host_fp32):
+            d.copy_(h, non_blocking=True)
+
+    def packed_h2d():
+        dev_packed.copy_(host_packed, non_blocking=True)
+
+    t_raw = _loop_ms(raw_h2d, reps=4, rounds=3)
+    t_pk = _loop_ms(packed_h2d, reps=4, rounds=3)
+    t_zc = _loop_ms(lambda: engine.unpack(sync.unpack_table, host_packed), reps=4, rounds=3)
+    recs = layout_records(lay, bias_bytes)
+    ms = 1e-3
+    return {
+        "phases": {
+            "pack": {"device_s": pack_only * ms, "with_fused_l2_norm_s": pack_norm * ms},
+            "unpack": {"device_s": unpack_only * ms, "with_concurrent_finalize_s": fin_unpack * ms},
+            "l2_norm": {"fused_extra_s": max(0.0, pack_norm - pack_only) * ms, "standalone_s": norm_only * ms},
+            "to_worker": {"raw_fp32_h2d_s": t_raw * ms, "packed_h2d_s": t_pk * ms,
+                          "packed_h2d_plus_unpack_s": (t_pk + unpack_only) * ms,
+                          "zero_copy_unpack_s": t_zc * ms},
+        },
+        "wire_bytes": {"to_worker": sum(r.wire_bytes for r in recs)},
+        "raw_bytes": {"to_worker": sum(r.raw_bytes for r in recs)},
+        "weight_stream": {"raw_bytes": sum(r.weight_raw_bytes for r in recs),
+                          "wire_bytes": sum(r.weight_wire_bytes for r in recs),
+                          "ratio": weight_stream_ratio(recs)},
+    }
