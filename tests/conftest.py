@@ -14,6 +14,10 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    # a fresh checkout has no libadt.so: build it (nvcc cross-compiles sm_100a without a GPU)
+    from paper_2004_02297_b200 import _build
+    if _build.needs_build():
+        _build.build()
 
 
 def _load(name):
