@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 5
+#define ADT_ABI_VERSION 6
 
 /* status codes */
 #define ADT_OK 0
@@ -68,6 +68,20 @@ typedef struct adt_sgd_segment {
     int32_t round_to;
     int32_t reserved;   /* must be 0 */
 } adt_sgd_segment;
+
+/* One layer piece of the fused gradient-reduce + SGD step + pack
+ * (adt_reduce_sgd_pack). Its gradient contributions live at the SAME byte
+ * offset `grad_offset` inside every contribution's gradient buffer (a flat
+ * per-worker gradient bucket, or a rank's received shard). */
+typedef struct adt_grad_segment {
+    void *weights;         /* FP32 master W (this rank's shard piece), updated in place, 16-B aligned */
+    void *velocity;        /* FP32 momentum buffer v, updated in place */
+    uint64_t count;
+    uint64_t offset;       /* payload offset of the packed W' in the packed buffer (16-B aligned) */
+    uint64_t grad_offset;  /* byte offset of this piece's gradients in every grads[c] (16-B aligned) */
+    int32_t round_to;
+    int32_t reserved;      /* must be 0 */
+} adt_grad_segment;
 
 /* ABI version (ADT_ABI_VERSION). */
 int adt_abi_version(void);
@@ -155,6 +169,25 @@ int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq,
  */
 int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
                  uint8_t *packed, double *seg_sumsq, double *partials, void *stream);
+
+/*
+ * Gradient return path fused with the update and the pack (SURVEY.md §8f
+ * item 4). Replaces net.gather_and_update's weight half (net.py:203-246) fed
+ * by transfer.TransferBoundary.return_gradients (transfer.py:247-251):
+ *   g  = pairwise_sum_c( g_c * f32(sample_counts[c]) ) / f32(sum of sample_counts)
+ *        (pairwise_sum's association tree, net.py:186-200; float32, rounded
+ *        after every operation)
+ * then the momentum step of adt_sgd_pack, the pack of W' and (optionally) its
+ * fused norm.  grads[c] (c < ncontrib <= ADT_MAX_SOURCES) are the workers'
+ * gradient buffers: local device memory, or the peer ranks' gradient buckets
+ * mapped with adt_ipc_open — then the reduce-scatter onto this rank's master
+ * shard IS this kernel's load stage (the gradients cross NVLink once, are
+ * combined in registers, and never land in HBM as a reduced copy).
+ */
+int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *const *grads,
+                        const int64_t *sample_counts, int ncontrib, float lr, float momentum,
+                        float weight_decay, uint8_t *packed, double *seg_sumsq, double *partials,
+                        void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

@@ -230,3 +230,35 @@ def sgd_step(w, v, g, lr, momentum, weight_decay):
     v += g
     w -= f(lr) * v
     return w, v
+
+
+# ------------------------------------ gradient return
+def pairwise_sum(arrays):
+    """net.py:186-200: adjacent pairing, level by level (the association tree
+    depends only on the list length); an odd leftover is carried up as is."""
+    if not arrays:
+        raise ValueError("pairwise_sum of no arrays")
+    level = list(arrays)
+    while len(level) > 1:
+        nxt = [level[i] + level[i + 1] for i in range(0, len(level) - 1, 2)]
+        if len(level) % 2:
+            nxt.append(level[-1])
+        level = nxt
+    return level[0]
+
+
+def combine_gradients(grads, sample_counts):
+    """net.py:229-231: sum_c f32(count_c) * g_c over the pairwise tree, then
+    / f32(total) — float32 with rounding after every operation."""
+    f = np.float32
+    total = sum(int(c) for c in sample_counts)
+    g = pairwise_sum([np.asarray(x, dtype=np.float32) * f(c) for x, c in zip(grads, sample_counts)])
+    g = np.array(g, dtype=np.float32, copy=True)
+    g /= f(total)
+    return g
+
+
+def gather_and_update_weights(w, v, grads, sample_counts, lr, momentum, weight_decay):
+    """net.py:203-246, weight half of gather_and_update with several worker
+    contributions. Returns (new weights, new velocity)."""
+    return sgd_step(w, v, combine_gradients(grads, sample_counts), lr, momentum, weight_decay)

@@ -23,13 +23,13 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 5
+ABI_VERSION = 6
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
            "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
-           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_device_sm_count")
+           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_device_sm_count")
 
 
 class Segment(ctypes.Structure):
@@ -53,6 +53,20 @@ class SgdSegment(ctypes.Structure):
         ("grad", ctypes.c_void_p),
         ("count", ctypes.c_uint64),
         ("offset", ctypes.c_uint64),
+        ("round_to", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class GradSegment(ctypes.Structure):
+    """adt_grad_segment (include/adt.h)."""
+
+    _fields_ = [
+        ("weights", ctypes.c_void_p),
+        ("velocity", ctypes.c_void_p),
+        ("count", ctypes.c_uint64),
+        ("offset", ctypes.c_uint64),
+        ("grad_offset", ctypes.c_uint64),
         ("round_to", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
     ]
@@ -114,6 +128,10 @@ def load() -> ctypes.CDLL:
         lib.adt_sgd_pack.restype = ctypes.c_int
         lib.adt_sgd_pack.argtypes = [P(SgdSegment), ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                      vp, vp, vp, vp]
+        lib.adt_reduce_sgd_pack.restype = ctypes.c_int
+        lib.adt_reduce_sgd_pack.argtypes = [P(GradSegment), ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int64),
+                                            ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                            vp, vp, vp, vp]
         lib.adt_sumsq.restype = ctypes.c_int
         lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_device_sm_count.restype = ctypes.c_int

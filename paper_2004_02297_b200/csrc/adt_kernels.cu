@@ -465,18 +465,54 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 
 
 // ------------------------------------------------- fused SGD update + pack
-// SURVEY.md §8f item 1: the momentum-SGD step right before the path
-// (net.py:236-246, weight half) fused with the pack and the norm: one pass
-// reads W, v, g and writes W', v' and W''s packed bytes + norm partials, so
-// the updated master is never re-read. Per weight, float32 with the
-// reference's rounding at every operation (no FMA contraction):
+// SURVEY.md §8f items 1 and 4: the momentum-SGD step right before the path
+// (net.py:203-246, weight half of gather_and_update) fused with the pack and
+// the norm: one pass reads W, v and the gradient(s) and writes W', v' and W''s
+// packed bytes + norm partials, so the updated master is never re-read.
+//
+// NC = 0 (adt_sgd_pack): one pre-averaged gradient g.
+// NC >= 1 (adt_reduce_sgd_pack, the gradient return path): NC worker
+//   contributions g_c, read from NC source buffers (local, or peer ranks'
+//   gradient buckets mapped over NVLink — the reduce-scatter is this kernel's
+//   load stage), combined exactly as net.py:229-231:
+//     g = pairwise_sum(g_c * f32(count_c)) / f32(total)
+//   with pairwise_sum's association tree (net.py:186-200).
+// Then per weight, float32 with the reference's rounding at every operation
+// (no FMA contraction):
 //   g' = g + wd*W   (only when wd != 0)   v' = v*mu + g'   W' = W - lr*v'
 template <int MAXSEG>
 struct SgdTable : Table<MAXSEG> {
     uintptr_t velocity[MAXSEG];
-    uintptr_t grad[MAXSEG];
+    uintptr_t grad[MAXSEG];        // NC = 0: gradient address; NC >= 1: byte offset inside every srcs[c]
+    float scale[ADT_MAX_SOURCES];  // f32(sample_count_c)
+    float total;                   // f32(sum of sample counts)
     float lr, momentum, weight_decay;
 };
+
+// net.py:186-200 on registers: adjacent pairs, level by level, an odd
+// leftover carried up unchanged. x[] is fully unrolled (constant indices).
+template <int LEN>
+struct Pairwise {
+    static __device__ __forceinline__ float run(float *x) {
+#pragma unroll
+        for (int i = 0; i < LEN / 2; ++i) x[i] = __fadd_rn(x[2 * i], x[2 * i + 1]);
+        if (LEN % 2) x[LEN / 2] = x[LEN - 1];
+        return Pairwise<(LEN + 1) / 2>::run(x);
+    }
+};
+template <>
+struct Pairwise<1> {
+    static __device__ __forceinline__ float run(float *x) { return x[0]; }
+};
+
+template <int NC, int MAXSEG>
+__device__ __forceinline__ uint32_t combine(const uint32_t *g, const SgdTable<MAXSEG> &T) {
+    if (NC == 0) return g[0];
+    float x[NC > 0 ? NC : 1];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) x[c] = __fmul_rn(__uint_as_float(g[c]), T.scale[c]);
+    return __float_as_uint(__fdiv_rn(Pairwise<NC>::run(x), T.total));
+}
 
 __device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb, float lr, float mu, float wd) {
     const float w = __uint_as_float(wb);
@@ -490,9 +526,12 @@ __device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb,
 #ifndef ADT_SGD_MIN_BLOCKS
 #define ADT_SGD_MIN_BLOCKS 4
 #endif
-template <int MAXSEG, bool NORM>
-__global__ void __launch_bounds__(kThreads, ADT_SGD_MIN_BLOCKS)
+constexpr int sgd_min_blocks(int nc) { return nc == 0 ? ADT_SGD_MIN_BLOCKS : (nc <= 2 ? 3 : 2); }
+
+template <int MAXSEG, int NC>
+__global__ void __launch_bounds__(kThreads, sgd_min_blocks(NC))
 adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
+    constexpr int NG = NC > 0 ? NC : 1;
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     const uint32_t tile = blockIdx.x;
     const int s = find_segment(T, tile);
@@ -503,29 +542,41 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
     const uint32_t g0 = warp * kWarpGroups + lane;
     uint4 *wp = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
     uint4 *vp = reinterpret_cast<uint4 *>(T.velocity[s]) + e0 / 4;
-    const uint4 *gp = reinterpret_cast<const uint4 *>(T.grad[s]) + e0 / 4;
+    const uint4 *gp[NG];
+#pragma unroll
+    for (int c = 0; c < NG; ++c)
+        gp[c] = reinterpret_cast<const uint4 *>((NC == 0 ? static_cast<uintptr_t>(0)
+                                                         : reinterpret_cast<uintptr_t>(T.srcs[c])) + T.grad[s]) + e0 / 4;
     const float lr = T.lr, mu = T.momentum, wd = T.weight_decay;
 
-    uint4 w[kVec], v[kVec], g[kVec];
+    uint4 w[kVec], v[kVec];
     if (m == kTile) {
 #pragma unroll
         for (int k = 0; k < kVec; ++k) {
             w[k] = __ldcs(wp + g0 + 32 * k);
             v[k] = __ldcs(vp + g0 + 32 * k);
-            g[k] = __ldcs(gp + g0 + 32 * k);
         }
 #pragma unroll
         for (int k = 0; k < kVec; ++k) {
-            w[k].x = sgd1(w[k].x, v[k].x, g[k].x, lr, mu, wd);
-            w[k].y = sgd1(w[k].y, v[k].y, g[k].y, lr, mu, wd);
-            w[k].z = sgd1(w[k].z, v[k].z, g[k].z, lr, mu, wd);
-            w[k].w = sgd1(w[k].w, v[k].w, g[k].w, lr, mu, wd);
+            uint4 g[NG];
+#pragma unroll
+            for (int c = 0; c < NG; ++c) g[c] = __ldcs(gp[c] + g0 + 32 * k);
+            uint32_t gx[NG], gy[NG], gz[NG], gw[NG];
+#pragma unroll
+            for (int c = 0; c < NG; ++c) { gx[c] = g[c].x; gy[c] = g[c].y; gz[c] = g[c].z; gw[c] = g[c].w; }
+            w[k].x = sgd1(w[k].x, v[k].x, combine<NC>(gx, T), lr, mu, wd);
+            w[k].y = sgd1(w[k].y, v[k].y, combine<NC>(gy, T), lr, mu, wd);
+            w[k].z = sgd1(w[k].z, v[k].z, combine<NC>(gz, T), lr, mu, wd);
+            w[k].w = sgd1(w[k].w, v[k].w, combine<NC>(gw, T), lr, mu, wd);
+        }
+        // stores after every load: no load is ordered behind a possibly-aliasing store
+#pragma unroll
+        for (int k = 0; k < kVec; ++k) {
             wp[g0 + 32 * k] = w[k];
             vp[g0 + 32 * k] = v[k];
         }
     } else {
         uint32_t *w1 = reinterpret_cast<uint32_t *>(wp), *v1 = reinterpret_cast<uint32_t *>(vp);
-        const uint32_t *g1 = reinterpret_cast<const uint32_t *>(gp);
 #pragma unroll
         for (int k = 0; k < kVec; ++k) {
             const uint32_t i = (g0 + 32 * k) * 4;
@@ -535,8 +586,11 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
                 ww[j] = 0u;
                 vv[j] = 0u;
                 if (i + j < m) {
+                    uint32_t gg[NG];
+#pragma unroll
+                    for (int c = 0; c < NG; ++c) gg[c] = reinterpret_cast<const uint32_t *>(gp[c])[i + j];
                     vv[j] = v1[i + j];
-                    ww[j] = sgd1(w1[i + j], vv[j], g1[i + j], lr, mu, wd);
+                    ww[j] = sgd1(w1[i + j], vv[j], combine<NC>(gg, T), lr, mu, wd);
                     w1[i + j] = ww[j];
                     v1[i + j] = vv[j];
                 }
@@ -545,7 +599,7 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
         }
     }
     store_packed(T.packed_out + T.offset[s] + e0 * r, w, m, r, warp, lane, g0, stage[warp]);
-    if (NORM) warp_partial(T.partials, tile, sumsq16(w));
+    if (T.partials != nullptr) warp_partial(T.partials, tile, sumsq16(w));
 }
 
 }  // namespace
@@ -747,60 +801,113 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs
 }
 
 
+// Per-call SGD parameters shared by every chunk.
+struct SgdArgs {
+    const uint8_t *srcs[ADT_MAX_SOURCES];  // gradient buffers (NC >= 1)
+    float scale[ADT_MAX_SOURCES];
+    float total, lr, mu, wd;
+    int nc;                                 // 0 = one pre-averaged gradient per segment
+};
+
+template <int MAXSEG, int NC>
+cudaError_t launch_sgd_kernel(const SgdTable<MAXSEG> &T, uint32_t ntiles, cudaStream_t stream) {
+    adt_sgd_pack_kernel<MAXSEG, NC><<<ntiles, kThreads, 0, stream>>>(T);
+    return cudaGetLastError();
+}
+
 template <int MAXSEG>
-int launch_sgd_chunk(const adt_sgd_segment *segs, int nseg, uint8_t *pout, double *seg_sumsq, double *partials,
-                     uint32_t ntiles, float lr, float mu, float wd, cudaStream_t stream) {
+cudaError_t launch_sgd_nc(const SgdTable<MAXSEG> &T, int nc, uint32_t ntiles, cudaStream_t stream) {
+    switch (nc) {
+        case 0: return launch_sgd_kernel<MAXSEG, 0>(T, ntiles, stream);
+        case 1: return launch_sgd_kernel<MAXSEG, 1>(T, ntiles, stream);
+        case 2: return launch_sgd_kernel<MAXSEG, 2>(T, ntiles, stream);
+        case 3: return launch_sgd_kernel<MAXSEG, 3>(T, ntiles, stream);
+        case 4: return launch_sgd_kernel<MAXSEG, 4>(T, ntiles, stream);
+        case 5: return launch_sgd_kernel<MAXSEG, 5>(T, ntiles, stream);
+        case 6: return launch_sgd_kernel<MAXSEG, 6>(T, ntiles, stream);
+        case 7: return launch_sgd_kernel<MAXSEG, 7>(T, ntiles, stream);
+        case 8: return launch_sgd_kernel<MAXSEG, 8>(T, ntiles, stream);
+        case 9: return launch_sgd_kernel<MAXSEG, 9>(T, ntiles, stream);
+        case 10: return launch_sgd_kernel<MAXSEG, 10>(T, ntiles, stream);
+        case 11: return launch_sgd_kernel<MAXSEG, 11>(T, ntiles, stream);
+        case 12: return launch_sgd_kernel<MAXSEG, 12>(T, ntiles, stream);
+        case 13: return launch_sgd_kernel<MAXSEG, 13>(T, ntiles, stream);
+        case 14: return launch_sgd_kernel<MAXSEG, 14>(T, ntiles, stream);
+        case 15: return launch_sgd_kernel<MAXSEG, 15>(T, ntiles, stream);
+        case 16: return launch_sgd_kernel<MAXSEG, 16>(T, ntiles, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// One chunk of <= MAXSEG segments. Segment i: weights/velocity/count/offset/
+// round_to from the caller's arrays; gradient = grad[i] (an address for nc = 0,
+// a byte offset into every gradient buffer otherwise).
+template <int MAXSEG>
+int launch_sgd_chunk(const adt_sgd_segment *segs, const adt_grad_segment *gsegs, int nseg, const SgdArgs &A,
+                     uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, cudaStream_t stream) {
     SgdTable<MAXSEG> T;
-    for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = nullptr;
+    for (int i = 0; i < ADT_MAX_SOURCES; ++i) {
+        T.srcs[i] = A.srcs[i];
+        T.scale[i] = A.scale[i];
+    }
     T.packed_out = pout;
     T.seg_sumsq = seg_sumsq;
     T.partials = partials;
     T.nseg = nseg;
-    T.lr = lr;
-    T.momentum = mu;
-    T.weight_decay = wd;
+    T.total = A.total;
+    T.lr = A.lr;
+    T.momentum = A.mu;
+    T.weight_decay = A.wd;
     uint32_t acc = 0;
     for (int i = 0; i < nseg; ++i) {
+        const uint64_t count = segs ? segs[i].count : gsegs[i].count;
         T.tile_begin[i] = acc;
-        acc += static_cast<uint32_t>((segs[i].count + kTile - 1) / kTile);
-        T.count[i] = segs[i].count;
-        T.offset[i] = segs[i].offset;
-        T.weights[i] = reinterpret_cast<uintptr_t>(segs[i].weights);
-        T.velocity[i] = reinterpret_cast<uintptr_t>(segs[i].velocity);
-        T.grad[i] = reinterpret_cast<uintptr_t>(segs[i].grad);
-        T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
+        acc += static_cast<uint32_t>((count + kTile - 1) / kTile);
+        T.count[i] = count;
+        if (segs) {
+            T.offset[i] = segs[i].offset;
+            T.weights[i] = reinterpret_cast<uintptr_t>(segs[i].weights);
+            T.velocity[i] = reinterpret_cast<uintptr_t>(segs[i].velocity);
+            T.grad[i] = reinterpret_cast<uintptr_t>(segs[i].grad);
+            T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
+        } else {
+            T.offset[i] = gsegs[i].offset;
+            T.weights[i] = reinterpret_cast<uintptr_t>(gsegs[i].weights);
+            T.velocity[i] = reinterpret_cast<uintptr_t>(gsegs[i].velocity);
+            T.grad[i] = static_cast<uintptr_t>(gsegs[i].grad_offset);
+            T.round_to[i] = static_cast<uint8_t>(gsegs[i].round_to);
+        }
         T.src_idx[i] = 0;
     }
     T.tile_begin[nseg] = acc;
     cudaError_t e = cudaSuccess;
-    if (ntiles > 0) {
-        if (partials) adt_sgd_pack_kernel<MAXSEG, true><<<ntiles, kThreads, 0, stream>>>(T);
-        else adt_sgd_pack_kernel<MAXSEG, false><<<ntiles, kThreads, 0, stream>>>(T);
-        e = cudaGetLastError();
-    }
+    if (ntiles > 0) e = launch_sgd_nc<MAXSEG>(T, A.nc, ntiles, stream);
     if (e == cudaSuccess && seg_sumsq != nullptr && nseg > 0)
         e = launch_finalize<MAXSEG>(static_cast<const Table<MAXSEG> &>(T), true, stream);
     return cuda_status(e);
 }
 
-int run_sgd(const adt_sgd_segment *segs, int nseg, uint8_t *pout, double *seg_sumsq, double *partials, float lr,
-            float mu, float wd, cudaStream_t stream) {
+int run_sgd(const adt_sgd_segment *segs, const adt_grad_segment *gsegs, int nseg, const SgdArgs &A, uint8_t *pout,
+            double *seg_sumsq, double *partials, cudaStream_t stream) {
     uint64_t partial_base = 0;
     int base = 0;
+    auto count_of = [&](int i) { return segs ? segs[i].count : gsegs[i].count; };
     while (base < nseg) {
         int cnt = 0;
         uint64_t tiles = 0;
         while (base + cnt < nseg && cnt < kLargeSeg) {
-            const uint64_t t = (segs[base + cnt].count + kTile - 1) / kTile;
+            const uint64_t t = (count_of(base + cnt) + kTile - 1) / kTile;
             if (cnt > 0 && tiles + t > static_cast<uint64_t>(INT_MAX)) break;
             tiles += t;
             ++cnt;
         }
         double *ss = seg_sumsq ? seg_sumsq + base : nullptr;
         double *pp = partials ? partials + partial_base : nullptr;
+        const adt_sgd_segment *sb = segs ? segs + base : nullptr;
+        const adt_grad_segment *gb = gsegs ? gsegs + base : nullptr;
         const int st = cnt <= kSmallSeg
-            ? launch_sgd_chunk<kSmallSeg>(segs + base, cnt, pout, ss, pp, static_cast<uint32_t>(tiles), lr, mu, wd, stream)
-            : launch_sgd_chunk<kLargeSeg>(segs + base, cnt, pout, ss, pp, static_cast<uint32_t>(tiles), lr, mu, wd, stream);
+            ? launch_sgd_chunk<kSmallSeg>(sb, gb, cnt, A, pout, ss, pp, static_cast<uint32_t>(tiles), stream)
+            : launch_sgd_chunk<kLargeSeg>(sb, gb, cnt, A, pout, ss, pp, static_cast<uint32_t>(tiles), stream);
         if (st != ADT_OK) return st;
         partial_base += tiles * kWarpsPerTile;
         base += cnt;
@@ -946,8 +1053,52 @@ int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum
     }
     if (any && (packed == nullptr)) return ADT_ERR_ARG;
     if (any && reinterpret_cast<uintptr_t>(packed) % 16) return ADT_ERR_ALIGN;
-    return run_sgd(segs, nseg, packed, seg_sumsq, partials, lr, momentum, weight_decay,
-                   static_cast<cudaStream_t>(stream));
+    SgdArgs A = {};
+    A.lr = lr;
+    A.mu = momentum;
+    A.wd = weight_decay;
+    A.nc = 0;
+    return run_sgd(segs, nullptr, nseg, A, packed, seg_sumsq, partials, static_cast<cudaStream_t>(stream));
+}
+
+int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *const *grads,
+                        const int64_t *sample_counts, int ncontrib, float lr, float momentum, float weight_decay,
+                        uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+    if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
+    if (ncontrib < 1 || ncontrib > ADT_MAX_SOURCES || grads == nullptr || sample_counts == nullptr)
+        return ADT_ERR_ARG;
+    if (nseg > 0 && seg_sumsq != nullptr && partials == nullptr) return ADT_ERR_ARG;
+    SgdArgs A = {};
+    int64_t total = 0;
+    for (int c = 0; c < ncontrib; ++c) {
+        if (grads[c] == nullptr) return ADT_ERR_ARG;
+        if (reinterpret_cast<uintptr_t>(grads[c]) % 16) return ADT_ERR_ALIGN;
+        A.srcs[c] = reinterpret_cast<const uint8_t *>(grads[c]);
+        A.scale[c] = static_cast<float>(sample_counts[c]);   // dtype.type(c.sample_count), net.py:230
+        total += sample_counts[c];
+    }
+    A.total = static_cast<float>(total);                      // dtype.type(total), net.py:231
+    A.lr = lr;
+    A.mu = momentum;
+    A.wd = weight_decay;
+    A.nc = ncontrib;
+    bool any = false;
+    for (int i = 0; i < nseg; ++i) {
+        const adt_grad_segment &g = segs[i];
+        if (g.round_to < 1 || g.round_to > 4) return ADT_ERR_ROUND_TO;
+        if (g.reserved != 0) return ADT_ERR_ARG;
+        if (g.count == 0) continue;
+        any = true;
+        if (!g.weights || !g.velocity) return ADT_ERR_ARG;
+        if (reinterpret_cast<uintptr_t>(g.weights) % 16 || reinterpret_cast<uintptr_t>(g.velocity) % 16 ||
+            g.grad_offset % 16 || g.offset % 16)
+            return ADT_ERR_ALIGN;
+        if (g.count > (UINT64_MAX - g.offset) / 4 || g.count > (UINT64_MAX - g.grad_offset) / 4) return ADT_ERR_ARG;
+        if ((g.count + kTile - 1) / kTile > static_cast<uint64_t>(INT_MAX)) return ADT_ERR_ARG;
+    }
+    if (any && (packed == nullptr)) return ADT_ERR_ARG;
+    if (any && reinterpret_cast<uintptr_t>(packed) % 16) return ADT_ERR_ALIGN;
+    return run_sgd(nullptr, segs, nseg, A, packed, seg_sumsq, partials, static_cast<cudaStream_t>(stream));
 }
 
 int adt_device_sm_count(int *sm_count) {

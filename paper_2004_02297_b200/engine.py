@@ -102,6 +102,53 @@ def sgd_pack(table: SgdTable, lr: float, momentum: float, weight_decay: float, p
                                         partials.data_ptr() if partials is not None else None, sh))
 
 
+class ReduceSgdTable:
+    """A prepared adt_grad_segment[] for adt_reduce_sgd_pack: per layer piece,
+    the master and velocity views, the packed layout, and the byte offset of
+    the piece's gradients inside every contribution buffer."""
+
+    def __init__(self, masters, velocities, grad_offsets: Sequence[int], layout: PackedLayout):
+        n = layout.num_layers
+        if not (len(masters) == len(velocities) == len(grad_offsets) == n):
+            raise ValueError("masters, velocities, grad offsets and layout disagree on the layer count")
+        self.layout = layout
+        self.tensors = (list(masters), list(velocities))
+        self.nseg = n
+        self.array = (_lib.GradSegment * max(1, n))()
+        for i, (w, v, go, cnt, off, r) in enumerate(zip(masters, velocities, grad_offsets, layout.counts,
+                                                        layout.offsets, layout.round_tos)):
+            a = self.array[i]
+            a.weights = _check_weight(w, cnt, f"master {i}")
+            a.velocity = _check_weight(v, cnt, f"velocity {i}")
+            if go % 16:
+                raise ValueError(f"piece {i}: gradient offset {go} not 16-byte aligned")
+            a.count, a.offset, a.grad_offset, a.round_to, a.reserved = cnt, off, int(go), r, 0
+        self.npartials = sum((c + _lib.TILE_WEIGHTS - 1) // _lib.TILE_WEIGHTS for c in layout.counts) \
+            * _lib.PARTIALS_PER_TILE
+
+
+def reduce_sgd_pack(table: ReduceSgdTable, grads: Sequence[int], sample_counts: Sequence[int], lr: float,
+                    momentum: float, weight_decay: float, packed: torch.Tensor,
+                    sumsq: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
+                    partials: torch.Tensor | None = None) -> None:
+    """adt_reduce_sgd_pack: the contributions at device addresses `grads`
+    (local buffers or peer buckets mapped by ipc_open) are combined as
+    net.gather_and_update does, the masters/velocities stepped in place, the
+    new masters packed (+ norm partials / per-layer sums, see pack())."""
+    if len(grads) != len(sample_counts) or not 1 <= len(grads) <= _lib.MAX_SOURCES:
+        raise ValueError(f"need 1..{_lib.MAX_SOURCES} contributions with one sample count each")
+    if packed.dtype != torch.uint8 or not packed.is_cuda or packed.numel() < table.layout.payload_end:
+        raise ValueError("packed must be a CUDA uint8 tensor covering every layer's payload")
+    sh = stream_handle(stream)
+    if partials is None and sumsq is not None:
+        partials = _Scratch.get(packed.device, sh, table.npartials)
+    counts = (ctypes.c_int64 * len(sample_counts))(*[int(c) for c in sample_counts])
+    _lib.check(_lib.load().adt_reduce_sgd_pack(
+        table.array, table.nseg, _lib.pointer_array(grads), counts, len(grads), float(lr), float(momentum),
+        float(weight_decay), packed.data_ptr(), sumsq.data_ptr() if sumsq is not None else None,
+        partials.data_ptr() if partials is not None else None, sh))
+
+
 class _Scratch:
     """Per (device, stream) norm scratch: the float64 partials of one pass."""
 
@@ -190,16 +237,39 @@ def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
     return buf.raw, int(off.value)
 
 
+_ipc_lock = threading.Lock()
+_ipc_maps: dict = {}     # handle bytes -> [base address, refcount]
+_ipc_bases: dict = {}    # base address -> handle bytes
+
+
 def ipc_open(handle: bytes) -> int:
-    """Map another process's allocation; returns its base device address here."""
-    lib = _lib.load()
-    out = ctypes.c_void_p(0)
-    _lib.check(lib.adt_ipc_open(ctypes.create_string_buffer(handle, len(handle)), ctypes.byref(out)))
-    return int(out.value)
+    """Map another process's allocation; returns its base device address here.
+    One mapping per allocation per process (a caching allocator may carve
+    several exported buffers out of one allocation): reference counted."""
+    with _ipc_lock:
+        ent = _ipc_maps.get(handle)
+        if ent is not None:
+            ent[1] += 1
+            return ent[0]
+        lib = _lib.load()
+        out = ctypes.c_void_p(0)
+        _lib.check(lib.adt_ipc_open(ctypes.create_string_buffer(handle, len(handle)), ctypes.byref(out)))
+        _ipc_maps[handle] = [int(out.value), 1]
+        _ipc_bases[int(out.value)] = handle
+        return int(out.value)
 
 
 def ipc_close(ptr: int) -> None:
-    _lib.check(_lib.load().adt_ipc_close(ptr))
+    with _ipc_lock:
+        handle = _ipc_bases.get(ptr)
+        if handle is not None:
+            ent = _ipc_maps[handle]
+            ent[1] -= 1
+            if ent[1] > 0:
+                return
+            del _ipc_maps[handle]
+            del _ipc_bases[ptr]
+        _lib.check(_lib.load().adt_ipc_close(ptr))
 
 
 def sumsq(table: SegmentTable, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:

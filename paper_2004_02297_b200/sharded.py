@@ -31,7 +31,8 @@ from . import engine
 from ._lib import TILE_WEIGHTS
 from .layout import align_up
 from .precision import FixedPrecision, PrecisionController
-from .sync import SyncResult
+from .grads import GradBucket, bucket_offsets, shard_ranges
+from .sync import NonFiniteParameters, SyncResult
 
 
 @dataclass(frozen=True)
@@ -91,6 +92,24 @@ class ShardPlan:
         return ShardPlan(counts, round_tos, world, tuple(pieces), cap, max_pieces,
                          align_up(cap + 8 * max_pieces))
 
+    def with_widths(self, round_tos: Sequence[int]) -> "ShardPlan":
+        """The same ownership (every rank keeps its (layer, lo, hi) pieces) at
+        new widths: only the packed offsets and buffer sizes change. Used once
+        masters are sharded (update()), where moving ownership would move
+        master/velocity state between ranks."""
+        round_tos = tuple(int(r) for r in round_tos)
+        pieces, cap = [], 0
+        for lst0 in self.pieces:
+            off, lst = 0, []
+            for pc in lst0:
+                lst.append(Piece(pc.layer, pc.lo, pc.hi, off))
+                off = align_up(off + (pc.hi - pc.lo) * round_tos[pc.layer])
+            cap = max(cap, off)
+            pieces.append(tuple(lst))
+        cap = align_up(max(cap, 16))
+        return ShardPlan(self.counts, round_tos, self.world, tuple(pieces), cap, self.max_pieces,
+                         align_up(cap + 8 * self.max_pieces))
+
     def rank_payload_bytes(self, rank: int) -> int:
         return sum((pc.hi - pc.lo) * self.round_tos[pc.layer] for pc in self.pieces[rank])
 
@@ -144,15 +163,24 @@ class ShardedWeightSync:
         self._slot = 0
         self._peer = None      # p2p: per slot, every rank's send-buffer address in this process
         self._opened = []
+        self.velocities = None     # momentum buffers (only this rank's shard ranges are stepped)
+        self._gpeer = None         # p2p: (bucket data_ptr, every rank's bucket address here)
+        self._gopened = []
+        self._grecv = None         # nccl: all-to-all'd gradient slices of this rank's shard
         self._plan(self.schedule.round_tos())
 
     # ------------------------------------------------------------- planning
     def _plan(self, round_tos):
         from .layout import PackedLayout
-        self.plan = ShardPlan.plan(self.counts, round_tos, self.world)
+        if getattr(self, "_owners_fixed", False):
+            self.plan = self.plan.with_widths(round_tos)
+        else:
+            self.plan = ShardPlan.plan(self.counts, round_tos, self.world)
         S = self.plan.send_bytes
         if self.send is None or self.send[0].numel() < S:
-            cap = max(S, ShardPlan.plan(self.counts, [4] * len(self.counts), self.world).send_bytes)
+            widest = [4] * len(self.counts)
+            cap = max(S, (self.plan.with_widths(widest) if getattr(self, "_owners_fixed", False)
+                          else ShardPlan.plan(self.counts, widest, self.world)).send_bytes)
             self._alloc(cap)
         if self.transport == "p2p":
             need = self.world * 8 * self.plan.max_pieces
@@ -173,6 +201,8 @@ class ShardedWeightSync:
                 offs.append(pc.offset if self.transport == "p2p" else q * S + pc.offset)
                 srcs.append(q if self.transport == "p2p" else 0)
         self.unpack_layout = PackedLayout(tuple(cnt), tuple(rs), tuple(offs), S * self.world)
+        self.grad_ranges = shard_ranges(self.plan, self.counts)
+        self._reduce_table = None
         self.unpack_table = engine.SegmentTable(outs, self.unpack_layout,
                                                 sources=srcs if self.transport == "p2p" else None)
 
@@ -209,6 +239,8 @@ class ShardedWeightSync:
     def __del__(self):
         try:
             self._close_peers()
+            for p in self._gopened:
+                engine.ipc_close(p)
         except Exception:
             pass
 
@@ -275,6 +307,108 @@ class ShardedWeightSync:
         res.trace = self.schedule.observe_all(self._norms(), batch=batch - 1)
         new = self.schedule.round_tos()
         if new != used:
+            self._plan(new)
+            self.launch(fused_norm=False)
+            res.round_tos = new
+            res.repacked = True
+        return res
+
+    # ------------------------------------------- gradient return (§8f #4)
+    def _grad_sources(self, bucket: GradBucket) -> tuple[list[int], int]:
+        """Device addresses of every rank's gradients for this rank's shard,
+        in rank order, and the byte base the piece offsets are relative to."""
+        b0, b1 = self.grad_ranges[self.rank]
+        if self.transport == "p2p":
+            if self._gpeer is None or self._gpeer[0] != bucket.flat.data_ptr():
+                for p in self._gopened:
+                    engine.ipc_close(p)
+                self._gopened = []
+                handle = engine.ipc_handle(bucket.flat)
+                everyone = [None] * self.world
+                self.dist.all_gather_object(everyone, handle, group=self.group)
+                ptrs = []
+                for q in range(self.world):
+                    if q == self.rank:
+                        ptrs.append(bucket.flat.data_ptr())
+                    else:
+                        base = engine.ipc_open(everyone[q][0])
+                        self._gopened.append(base)
+                        ptrs.append(base + everyone[q][1])
+                self._gpeer = (bucket.flat.data_ptr(), ptrs)
+            return self._gpeer[1], 0
+        mine = b1 - b0
+        if self._grecv is None or self._grecv.numel() < max(4, mine * self.world):
+            self._grecv = torch.empty(max(4, mine * self.world), dtype=torch.float32, device=self.device)
+        if self.world > 1:
+            splits = [e - b for b, e in self.grad_ranges]
+            self.dist.all_to_all_single(self._grecv[:mine * self.world], bucket.flat[:sum(splits)],
+                                        output_split_sizes=[mine] * self.world, input_split_sizes=splits,
+                                        group=self.group)
+            base = self._grecv.data_ptr()
+            return [base + 4 * mine * q for q in range(self.world)], 4 * b0
+        return [bucket.flat.data_ptr()], 0
+
+    def update(self, bucket: GradBucket, sample_counts, lr: float, momentum: float = 0.9,
+               weight_decay: float = 5e-4, batch: int = 0) -> SyncResult:
+        """One data-parallel step (net.gather_and_update, net.py:203-257, over
+        the ranks' gradient buckets, then the weight distribution):
+
+        every rank's bucket -> [fused: gather this rank's shard of all ranks'
+        gradients (p2p: peer loads over NVLink; nccl: all_to_all), combine
+        them with the reference's weighting and pairwise tree, momentum-step
+        the master shard, pack it at the AWP widths, fuse its norm]
+        -> exchange packed bytes -> unpack every replica -> AWP observe.
+
+        `sample_counts[q]` = rank q's GradientSet.sample_count. Only this
+        rank's shard of `masters` / `velocities` is stepped (the masters are
+        sharded, as in the paper's single master copy); the replicas hold
+        every updated weight, truncated to the widths in force."""
+        if len(sample_counts) != self.world:
+            raise ValueError("one sample count per rank")
+        if list(bucket.counts) != list(self.counts):
+            raise ValueError("gradient bucket layer sizes differ from the masters")
+        if self.velocities is None:
+            self.velocities = [torch.zeros_like(m) for m in self.masters]
+        self._owners_fixed = True
+        grads, rel = self._grad_sources(bucket)
+        if self._reduce_table is None:
+            offs, _ = bucket_offsets(self.counts)
+            mine = self.plan.pieces[self.rank]
+            self._reduce_table = engine.ReduceSgdTable(
+                [self.masters[pc.layer][pc.lo:pc.hi] for pc in mine],
+                [self.velocities[pc.layer][pc.lo:pc.hi] for pc in mine],
+                [4 * (offs[pc.layer] + pc.lo) - rel for pc in mine], self.pack_table.layout)
+        S = self.plan.send_bytes
+        if self.transport == "nccl":
+            send, recv = self.send[0][:S], self.recv[:S * self.world]
+        else:
+            slot = self._slot
+            self._slot ^= 1
+            send = self.send[slot]
+            self._barrier()                      # every rank's gradients are written
+        engine.reduce_sgd_pack(self._reduce_table, grads, sample_counts, lr, momentum, weight_decay, send,
+                               self._tail(send))
+        if self.transport == "nccl":
+            if self.world > 1:
+                self.dist.all_gather_into_tensor(recv, send, group=self.group)
+            engine.unpack(self.unpack_table, recv)
+        else:
+            self._barrier()                      # every shard is stepped and packed
+            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
+            engine.unpack_multi(self.unpack_table, self._peer[slot])
+        used = self.round_tos
+        res = SyncResult(round_tos=used)
+        norms = self._norms()
+        bad = [i for i, n in enumerate(norms) if not math.isfinite(n)]
+        if bad:
+            raise NonFiniteParameters(f"layer {bad[0]} parameters left the finite range")
+        if not self.adaptive:
+            return res
+        res.trace = self.schedule.observe_all(norms, batch=batch)
+        new = self.schedule.round_tos()
+        if new != used:
+            # re-pack the owners' (already stepped) master shards at the new
+            # widths; ownership is fixed, so no master state moves
             self._plan(new)
             self.launch(fused_norm=False)
             res.round_tos = new

@@ -71,6 +71,8 @@ class WeightSync:
         self._partials = None
         self._graphs = None      # (key, pack graph, finalize+unpack graph)
         self.velocities = None   # momentum buffers, created by the first update()
+        self._grad_stage = {}    # gather_and_update: staging buckets for per-layer gradient lists
+        self._reduce_table = None
         self.device = dev
         self.layout = None
         self.packed = None
@@ -235,14 +237,65 @@ class WeightSync:
         """
         if len(grads) != len(self.masters):
             raise ValueError("one gradient tensor per layer")
-        if self.velocities is None:
-            self.velocities = [torch.zeros_like(m) for m in self.masters]
+        self._ensure_velocities()
         g = [t.detach().reshape(-1) for t in grads]
         table = engine.SgdTable(self.masters, self.velocities, g, self.layout)
+
+        def launch(main):
+            engine.sgd_pack(table, lr, momentum, weight_decay, self.packed, None, main, partials=self._partials)
+        return self._update_step(launch, batch)
+
+    def gather_and_update(self, contributions, lr: float, momentum: float = 0.9, weight_decay: float = 5e-4,
+                          batch: int = 0) -> SyncResult:
+        """net.gather_and_update (net.py:203-257) + distribution, fused.
+
+        `contributions`: 1..16 worker gradient sets — `grads.GradBucket`s (used
+        in place) or objects with `weight_grads` / `sample_count` (a
+        `grads.GradientSet`, staged into a bucket). One kernel combines them
+        with the reference's sample-count weighting and pairwise_sum tree,
+        steps W and v, packs W' and fuses its norm; then the replicas are
+        unpacked and AWP observes, exactly as update()."""
+        from .grads import GradBucket
+        if not 1 <= len(contributions) <= 16:
+            raise ValueError("gather_and_update takes 1..16 gradient contributions")
+        buckets = []
+        for i, c in enumerate(contributions):
+            if isinstance(c, GradBucket):
+                b = c
+            else:
+                if len(c.weight_grads) != len(self.masters):
+                    raise ValueError(f"contribution has {len(c.weight_grads)} layers, network has {len(self.masters)}")
+                stage = self._grad_stage.get(i)
+                if stage is None:
+                    stage = self._grad_stage[i] = GradBucket(self.counts, self.device)
+                b = stage.load(c.weight_grads)
+                b.sample_count = int(c.sample_count)
+            if list(b.counts) != list(self.counts):
+                raise ValueError("gradient bucket layer sizes differ from the masters")
+            buckets.append(b)
+        self._ensure_velocities()
+        key = self.layout
+        if self._reduce_table is None or self._reduce_table[0] != key:
+            offs = [buckets[0].byte_offset(l) for l in range(len(self.masters))]
+            self._reduce_table = (key, engine.ReduceSgdTable(self.masters, self.velocities, offs, self.layout))
+        table = self._reduce_table[1]
+        ptrs = [b.flat.data_ptr() for b in buckets]
+        counts = [b.sample_count for b in buckets]
+
+        def launch(main):
+            engine.reduce_sgd_pack(table, ptrs, counts, lr, momentum, weight_decay, self.packed, None, main,
+                                   partials=self._partials)
+        return self._update_step(launch, batch)
+
+    def _ensure_velocities(self) -> None:
+        if self.velocities is None:
+            self.velocities = [torch.zeros_like(m) for m in self.masters]
+
+    def _update_step(self, launch, batch: int) -> SyncResult:
         main = torch.cuda.current_stream()
         if self._fin_pending:
             main.wait_event(self._fin_done)
-        engine.sgd_pack(table, lr, momentum, weight_decay, self.packed, None, main, partials=self._partials)
+        launch(main)
         self._side.wait_stream(main)
         engine.finalize(self.pack_table, self._partials, self.sumsq, self._side)
         self._fin_done.record(self._side)

@@ -65,3 +65,11 @@ def golden_sgd():
     g = _load("golden_sgd.npz")
     return [dict(w=g[f"s{i}_w"], v=g[f"s{i}_v"], g=g[f"s{i}_g"], hp=tuple(float(x) for x in g[f"s{i}_hp"]),
                  w1=g[f"s{i}_w1"], v1=g[f"s{i}_v1"]) for i in range(int(g["ncases"]))]
+
+
+@pytest.fixture(scope="session")
+def golden_reduce_sgd():
+    g = _load("golden_reduce_sgd.npz")
+    return [dict(w=g[f"r{i}_w"], v=g[f"r{i}_v"], g=g[f"r{i}_g"], counts=[int(x) for x in g[f"r{i}_counts"]],
+                 hp=tuple(float(x) for x in g[f"r{i}_hp"]), w1=g[f"r{i}_w1"], v1=g[f"r{i}_v1"])
+            for i in range(int(g["ncases"]))]

@@ -17,6 +17,9 @@ writes, next to this script:
   test_acceptance.py:126-155) plus consecutive-mode and grouped variants.
 * golden_sgd.npz    — net.gather_and_update's weight/velocity step (net.py:236-246)
   for the fused SGD + pack kernel.
+* golden_reduce_sgd.npz — net.gather_and_update with 1..16 weighted gradient
+  contributions (pairwise_sum tree, net.py:186-257) for the fused
+  gradient-reduce + SGD + pack kernel.
 * golden_lenet.npz  — SURVEY.md §8d config 1: the LeNet weight set under a
   seeded multiplicative walk, 200 batches, driven in the reference's own
   order (training.py:209-254): pack every layer at the controller's widths
@@ -222,7 +225,47 @@ def sgd_cases():
     return out
 
 
+REDUCE_CASES = [
+    # (shape, sample counts per contribution, lr, momentum, weight_decay)
+    ((37, 41), [64], 0.05, 0.9, 5e-4),
+    ((64, 130), [32, 32], 0.02, 0.9, 5e-4),
+    ((33, 257), [17, 33, 50], 0.1, 0.9, 0.0),
+    ((50, 100), [1, 2, 3, 4, 5], 0.01, 0.5, 1e-3),
+    ((8, 4099), [64] * 8, 0.05, 0.9, 5e-4),
+    ((12, 345), [3, 64, 7, 1, 100, 9, 12, 5, 64, 2, 31, 8, 4, 64, 1, 77], 0.03, 0.9, 5e-4),
+    ((5, 9), [7, 7, 7, 7, 7, 7, 7], 0.2, 0.0, 0.0),
+]
+
+
+def reduce_sgd_cases():
+    """net.gather_and_update (net.py:203-257) with several gradient
+    contributions: sample-count weighting, the pairwise_sum association tree
+    (net.py:186-200), the division by the total count, then the momentum step
+    — what the fused reduce + SGD + pack kernel (gradient return path,
+    SURVEY.md §8f item 4) restates."""
+    from weightpack import net
+    out = {}
+    rng = np.random.default_rng(9)
+    for i, (shape, counts, lr, mom, wd) in enumerate(REDUCE_CASES):
+        w = (rng.standard_normal(shape) * 0.1).astype(np.float32)
+        v = (rng.standard_normal(shape) * 0.01).astype(np.float32)
+        gs = [(rng.standard_normal(shape) * 0.05).astype(np.float32) for _ in counts]
+        zb = np.zeros(shape[1], np.float32)
+        network = net.Network([net.Layer(w.copy(), zb.copy())])
+        state = net.SgdState(vel_weights=[v.copy()], vel_biases=[zb.copy()])
+        contribs = [net.GradientSet(weight_grads=[g.copy()], bias_grads=[zb.copy()], sample_count=c)
+                    for g, c in zip(gs, counts)]
+        cfg = net.SgdConfig(learning_rate=lr, momentum=mom, weight_decay=wd)
+        net.gather_and_update(network, contribs, cfg, state, lr)
+        out.update({f"r{i}_w": w, f"r{i}_v": v, f"r{i}_g": np.stack(gs), f"r{i}_counts": np.array(counts, np.int64),
+                    f"r{i}_hp": np.array([lr, mom, wd]),
+                    f"r{i}_w1": network.layers[0].weights, f"r{i}_v1": state.vel_weights[0]})
+    out["ncases"] = np.array(len(REDUCE_CASES))
+    return out
+
+
 def main():
+    np.savez_compressed(os.path.join(HERE, "golden_reduce_sgd.npz"), **reduce_sgd_cases())
     np.savez_compressed(os.path.join(HERE, "golden_sgd.npz"), **sgd_cases())
     np.savez_compressed(os.path.join(HERE, "golden_codec.npz"), **codec_cases())
     np.savez_compressed(os.path.join(HERE, "golden_awp.npz"), **awp_cases())

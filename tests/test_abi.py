@@ -28,7 +28,7 @@ def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
         ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
          "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
-         "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_device_sm_count"])
+         "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_device_sm_count"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -86,3 +86,25 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_norm_finalize(lib.segment_array([(16, 10, 0, 2)]), 1, None, 16, None) == lib.ADT_ERR_ARG
     # norm pass without scratch
     assert h.adt_sumsq(lib.segment_array([(16, 10, 0, 2)]), 1, None, None, None) == lib.ADT_ERR_ARG
+    # fused gradient reduce + SGD + pack: contribution count, alignment, width
+    def red(r, goff=0, wptr=16):
+        arr = (lib.GradSegment * 1)()
+        arr[0].weights, arr[0].velocity = wptr, 32
+        arr[0].count, arr[0].offset, arr[0].grad_offset, arr[0].round_to, arr[0].reserved = 10, 0, goff, r, 0
+        return arr
+    C = ctypes.c_int64
+    cnt = (C * 17)(*([1] * 17))
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 0, 0.1, 0.9, 0.0, 16, None, None, None) \
+        == lib.ADT_ERR_ARG
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48] * 17), cnt, 17, 0.1, 0.9, 0.0, 16, None, None,
+                                 None) == lib.ADT_ERR_ARG
+    assert h.adt_reduce_sgd_pack(red(5), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None) \
+        == lib.ADT_ERR_ROUND_TO
+    assert h.adt_reduce_sgd_pack(red(2, goff=8), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None,
+                                 None) == lib.ADT_ERR_ALIGN
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([40]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None) \
+        == lib.ADT_ERR_ALIGN
+    assert h.adt_reduce_sgd_pack(red(2, wptr=8), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None,
+                                 None) == lib.ADT_ERR_ALIGN
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, 16, None, None) \
+        == lib.ADT_ERR_ARG

@@ -1,0 +1,236 @@
+"""GPU parity of the gradient return path.
+
+adt_reduce_sgd_pack combines 1..16 worker gradient contributions exactly as
+the reference's net.gather_and_update (net.py:203-257: sample-count weights,
+pairwise_sum tree, division by the total, momentum step) and packs the new
+master in the same pass. Bar: W', v' and packed bytes bit-exact with the
+reference (golden_reduce_sgd.npz, produced by the reference itself); AWP
+decisions identical; norms within 1e-6 relative.
+
+The multi-rank form (ShardedWeightSync.update, p2p transport: the peers'
+gradient buckets read over CUDA IPC inside the kernel) runs as two processes
+sharing cuda:0 — the boxes have one GPU.
+"""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import weightpack_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def adt():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2004_02297_b200 as adt
+    return adt
+
+
+def test_reduce_sgd_pack_matches_reference(adt, golden_reduce_sgd):
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.grads import GradBucket
+    from paper_2004_02297_b200.layout import PackedLayout
+    for i, c in enumerate(golden_reduce_sgd):
+        r = (i % 4) + 1
+        n = c["w"].size
+        w = torch.from_numpy(c["w"].reshape(-1).copy()).cuda()
+        v = torch.from_numpy(c["v"].reshape(-1).copy()).cuda()
+        buckets = [GradBucket([n]).load([torch.from_numpy(g.reshape(-1).copy()).cuda()]) for g in c["g"]]
+        lay = PackedLayout.plan([n], [r])
+        packed = torch.zeros(lay.nbytes, dtype=torch.uint8, device="cuda")
+        ss = torch.empty(1, dtype=torch.float64, device="cuda")
+        table = engine.ReduceSgdTable([w], [v], [0], lay)
+        engine.reduce_sgd_pack(table, [b.flat.data_ptr() for b in buckets], c["counts"], *c["hp"], packed, ss)
+        torch.cuda.synchronize()
+        w1 = c["w1"].reshape(-1)
+        assert np.array_equal(w.cpu().numpy().view(np.uint32), w1.view(np.uint32)), (i, len(c["counts"]))
+        assert np.array_equal(v.cpu().numpy().view(np.uint32), c["v1"].reshape(-1).view(np.uint32)), i
+        lo, hi = lay.span(0)
+        assert packed[lo:hi].cpu().numpy().tobytes() == O.pack_vectorized(w1, r), i
+        assert math.sqrt(float(ss.item())) == pytest.approx(O.l2_norm(w1), rel=1e-12)
+
+
+def test_reduce_sgd_pack_every_contribution_count(adt):
+    """NC = 1..16 over a multi-layer ragged set (several tiles per layer,
+    ragged tails, r = 1..4) against the oracle's combine + step."""
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.grads import GradBucket
+    from paper_2004_02297_b200.layout import PackedLayout
+    rng = np.random.default_rng(3)
+    counts = [4096 * 2 + 5, 300, 4096 * 3, 77]
+    rs = [1, 2, 3, 4]
+    hp = (0.03, 0.9, 5e-4)
+    lay = PackedLayout.plan(counts, rs)
+    for nc in range(1, 17):
+        w0 = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+        v0 = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.01) for n in counts]
+        gs = [[rng.standard_normal(n, dtype=np.float32) * np.float32(0.05) for n in counts] for _ in range(nc)]
+        sc = [int(x) for x in rng.integers(1, 100, nc)]
+        buckets = [GradBucket(counts).load([torch.from_numpy(x).cuda() for x in g]) for g in gs]
+        w = [torch.from_numpy(x.copy()).cuda() for x in w0]
+        v = [torch.from_numpy(x.copy()).cuda() for x in v0]
+        packed = torch.zeros(lay.nbytes, dtype=torch.uint8, device="cuda")
+        ss = torch.empty(len(counts), dtype=torch.float64, device="cuda")
+        table = engine.ReduceSgdTable(w, v, [buckets[0].byte_offset(l) for l in range(len(counts))], lay)
+        engine.reduce_sgd_pack(table, [b.flat.data_ptr() for b in buckets], sc, *hp, packed, ss)
+        torch.cuda.synchronize()
+        for l in range(len(counts)):
+            w1, v1 = O.gather_and_update_weights(w0[l], v0[l], [g[l] for g in gs], sc, *hp)
+            assert np.array_equal(w[l].cpu().numpy().view(np.uint32), w1.view(np.uint32)), (nc, l)
+            assert np.array_equal(v[l].cpu().numpy().view(np.uint32), v1.view(np.uint32)), (nc, l)
+            lo, hi = lay.span(l)
+            assert packed[lo:hi].cpu().numpy().tobytes() == O.pack_vectorized(w1, rs[l]), (nc, l)
+            assert math.sqrt(float(ss[l].item())) == pytest.approx(O.l2_norm(w1), rel=1e-12)
+
+
+def test_reduce_sgd_pack_argument_errors(adt):
+    from paper_2004_02297_b200 import _lib, engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    w = torch.zeros(64, device="cuda")
+    v = torch.zeros(64, device="cuda")
+    g = torch.zeros(64, device="cuda")
+    lay = PackedLayout.plan([64], [2])
+    packed = torch.zeros(lay.nbytes, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        engine.ReduceSgdTable([w], [v], [4], lay)            # misaligned gradient offset
+    table = engine.ReduceSgdTable([w], [v], [0], lay)
+    with pytest.raises(ValueError):
+        engine.reduce_sgd_pack(table, [g.data_ptr()] * 17, [1] * 17, 0.1, 0.9, 0.0, packed)
+    with pytest.raises(_lib.AdtError):
+        engine.reduce_sgd_pack(table, [g.data_ptr() + 4], [1], 0.1, 0.9, 0.0, packed)   # misaligned buffer
+
+
+def test_weightsync_gather_and_update_walk(adt):
+    """20 batches of WeightSync.gather_and_update with 3 weighted worker
+    contributions (GradientSet lists and GradBuckets) and AWP, vs the oracle
+    in the reference's order: combine + update -> norm -> observe -> pack at
+    the new widths -> unpack."""
+    from paper_2004_02297_b200.grads import GradBucket, GradientSet
+    rng = np.random.default_rng(22)
+    counts = [500, 25000, 4096 * 3 + 7, 5000]
+    L = len(counts)
+    hp = (0.05, 0.9, 5e-4)
+    sc = [64, 17, 40]
+    w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+    v_ref = [np.zeros(n, np.float32) for n in counts]
+    kw = dict(threshold=-2e-3, interval=3, step_bits=8, initial_bits=8)
+    octl = O.OracleController(L, **kw)
+    masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
+    sync = adt.WeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)))
+    sync.step(batch=0)
+    bucket = GradBucket(counts, sample_count=sc[2])
+    for b in range(20):
+        grads = [[np.float32(0.4 + 0.1 * k) * w + rng.standard_normal(w.size, dtype=np.float32) * np.float32(0.002)
+                  for w in w_ref] for k in range(3)]
+        contribs = [GradientSet([torch.from_numpy(x).cuda() for x in grads[k]], [], sc[k]) for k in range(2)]
+        contribs.append(bucket.load([torch.from_numpy(x).cuda() for x in grads[2]]))
+        res = sync.gather_and_update(contribs, *hp, batch=b)
+        for i in range(L):
+            w_ref[i], v_ref[i] = O.gather_and_update_weights(w_ref[i], v_ref[i], [g[i] for g in grads], sc, *hp)
+            octl.observe_layer(i, O.l2_norm(w_ref[i]))
+        rs = [octl.round_to(i) for i in range(L)]
+        assert res.round_tos == rs, b
+        for i in range(L):
+            assert np.array_equal(masters[i].cpu().numpy().view(np.uint32), w_ref[i].view(np.uint32)), (b, i)
+            want = w_ref[i].view(np.uint32) & np.uint32(O.keep_mask(rs[i]))
+            assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), (b, i)
+        assert [row[5] for row in res.trace] == [octl.bits[i] for i in range(L)]
+    assert max(sync.round_tos) > 1
+
+
+def test_gather_and_update_nonfinite_raises(adt):
+    from paper_2004_02297_b200.grads import GradientSet
+    m = [torch.ones(100, device="cuda")]
+    sync = adt.WeightSync(m)
+    g = torch.full((100,), 3.0e38, device="cuda")
+    with pytest.raises(adt.NonFiniteParameters):
+        sync.gather_and_update([GradientSet([g], [], 64), GradientSet([g], [], 64)], lr=1.0)
+
+
+# ------------------------------------------------ two ranks sharing cuda:0
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2004_02297_b200 as adt
+        from paper_2004_02297_b200.grads import GradBucket
+        from paper_2004_02297_b200.sharded import ShardedWeightSync
+        counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
+        L = len(counts)
+        hp = (0.05, 0.9, 5e-4)
+        sc = [48, 80]
+        rng = np.random.default_rng(11)          # same stream on both ranks
+        w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+        v_ref = [np.zeros(n, np.float32) for n in counts]
+        masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
+        kw = dict(threshold=-2e-3, interval=2, step_bits=8, initial_bits=8)
+        octl = O.OracleController(L, **kw)
+        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport="p2p")
+        bucket = GradBucket(counts)
+        ok, notes, seen = True, [], []
+        for b in range(8):
+            grads = [[np.float32(0.5 + 0.2 * k) * w + rng.standard_normal(w.size, dtype=np.float32)
+                      * np.float32(0.002) for w in w_ref] for k in range(world)]
+            bucket.load([torch.from_numpy(x).cuda() for x in grads[rank]])
+            res = sync.update(bucket, sc, *hp, batch=b)
+            torch.cuda.synchronize()
+            for i in range(L):
+                w_ref[i], v_ref[i] = O.gather_and_update_weights(w_ref[i], v_ref[i], [g[i] for g in grads], sc, *hp)
+                octl.observe_layer(i, O.l2_norm(w_ref[i]))
+            rs = [octl.round_to(i) for i in range(L)]
+            if res.round_tos != rs:
+                ok = False
+                notes.append(f"batch {b}: widths {res.round_tos} != {rs}")
+            for i in range(L):
+                want = w_ref[i].view(np.uint32) & np.uint32(O.keep_mask(rs[i]))
+                if not np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want):
+                    ok = False
+                    notes.append(f"batch {b} layer {i} replica mismatch")
+            for row in res.trace:
+                ref = O.l2_norm(w_ref[row[1]])
+                if abs(row[2] - ref) > 1e-6 * ref:
+                    ok = False
+                    notes.append(f"norm {row} vs {ref}")
+                seen.append(row[2])
+        q.put((rank, ok, notes, seen, sync.round_tos))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surface child failures to the parent
+        import traceback
+        q.put((rank, False, [traceback.format_exc()], [], []))
+
+
+def test_sharded_update_p2p_two_processes_one_gpu():
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, notes, _, _ in res:
+        assert ok, (rank, notes[:5])
+    assert res[0][3] == res[1][3] and len(res[0][3]) > 0
+    assert res[0][4] == res[1][4] and max(res[0][4]) > 1

@@ -107,3 +107,17 @@ def test_sgd_step_matches_reference_update(golden_sgd):
         w1, v1 = O.sgd_step(c["w"], c["v"], c["g"], *c["hp"])
         assert np.array_equal(w1.view(np.uint32), c["w1"].view(np.uint32))
         assert np.array_equal(v1.view(np.uint32), c["v1"].view(np.uint32))
+
+
+def test_gather_and_update_matches_reference(golden_reduce_sgd):
+    for c in golden_reduce_sgd:
+        w1, v1 = O.gather_and_update_weights(c["w"], c["v"], list(c["g"]), c["counts"], *c["hp"])
+        assert np.array_equal(w1.view(np.uint32), c["w1"].view(np.uint32))
+        assert np.array_equal(v1.view(np.uint32), c["v1"].view(np.uint32))
+
+
+def test_pairwise_tree_shape():
+    # the association tree of net.py:186-200 for 5 leaves: ((a+b)+(c+d))+e
+    leaves = [np.float32(x) for x in (1e8, 1.0, -1e8, 1.0, 3.0)]
+    want = ((leaves[0] + leaves[1]) + (leaves[2] + leaves[3])) + leaves[4]
+    assert O.pairwise_sum(leaves) == want

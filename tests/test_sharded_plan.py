@@ -117,3 +117,81 @@ def test_gloo_world2_packed_allgather_reassembles_reference_payloads():
     assert all(ok for _, ok, _ in res)
     # identical norm bits on both ranks -> identical AWP decisions
     assert res[0][2] == res[1][2]
+
+
+# ------------------------------------------- gradient return (§8f #4) host logic
+@pytest.mark.parametrize("name", ["lenet", "alexnet", "resnet50"])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_grad_shard_ranges_tile_the_bucket(name, world):
+    from paper_2004_02297_b200.grads import bucket_offsets, shard_ranges
+    counts = workloads.counts_of(name)
+    rs = [(i % 4) + 1 for i in range(len(counts))]
+    plan = ShardPlan.plan(counts, rs, world)
+    offs, total = bucket_offsets(counts)
+    assert all(o % 4 == 0 for o in offs) and total % 4 == 0
+    ranges = shard_ranges(plan, counts)
+    assert ranges[0][0] == 0 and ranges[-1][1] == total
+    for (b0, e0), (b1, _) in zip(ranges, ranges[1:]):
+        assert e0 == b1 and b0 <= e0
+    for q, (b, e) in enumerate(ranges):
+        assert b % 4 == 0
+        for pc in plan.pieces[q]:
+            lo = offs[pc.layer] + pc.lo
+            assert b <= lo and lo + (pc.hi - pc.lo) <= e
+    # fixed ownership at new widths keeps every piece, moves only packed offsets
+    wide = plan.with_widths([4] * len(counts))
+    check_plan(wide, counts, [4] * len(counts))
+    assert [[(p.layer, p.lo, p.hi) for p in x] for x in wide.pieces] == \
+        [[(p.layer, p.lo, p.hi) for p in x] for x in plan.pieces]
+
+
+def _a2a_worker(rank, world, port, counts, rs, q):
+    """The NCCL transport's gradient exchange on CPU (gloo all_to_all_single):
+    each rank must receive every rank's gradients for exactly its own pieces,
+    and combining them (oracle) must equal the reference's combine of the
+    full layers restricted to those pieces."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import weightpack_oracle as O
+    from paper_2004_02297_b200.grads import bucket_offsets, shard_ranges
+    plan = ShardPlan.plan(counts, rs, world)
+    offs, total = bucket_offsets(counts)
+    rng = np.random.default_rng(5)
+    grads = [[rng.standard_normal(n, dtype=np.float32) for n in counts] for _ in range(world)]
+    sc = [3, 64, 17][:world]
+    flat = np.zeros(total, np.float32)
+    for layer, g in enumerate(grads[rank]):
+        flat[offs[layer]:offs[layer] + g.size] = g
+    ranges = shard_ranges(plan, counts)
+    b0, b1 = ranges[rank]
+    mine = b1 - b0
+    recv = torch.zeros(mine * world)
+    dist.all_to_all_single(recv, torch.from_numpy(flat), output_split_sizes=[mine] * world,
+                           input_split_sizes=[e - b for b, e in ranges])
+    recv = recv.numpy()
+    ok = True
+    for pc in plan.pieces[rank]:
+        rel = offs[pc.layer] + pc.lo - b0
+        n = pc.hi - pc.lo
+        contrib = [recv[c * mine + rel:c * mine + rel + n] for c in range(world)]
+        got = O.combine_gradients(contrib, sc)
+        want = O.combine_gradients([g[pc.layer] for g in grads], sc)[pc.lo:pc.hi]
+        ok &= np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_alltoall_gradient_shards_match_reference_combine(world):
+    counts = [20 * 25, 50 * 20 * 25, 3 * TILE + 17, 10 * 500, 9 * TILE]
+    rs = [1, 2, 3, 4, 2]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, counts, rs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res)
