@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--eager", action="store_true", help="launch each step eagerly instead of from CUDA graphs")
     ap.add_argument("--no-h2d", action="store_true", help="skip the pinned host->device comparison")
     ap.add_argument("--no-sgd", action="store_true", help="skip the fused SGD+pack comparison")
+    ap.add_argument("--no-reduce", action="store_true",
+                    help="skip the fused gradient-reduce + SGD + pack comparison (gradient return path)")
+    ap.add_argument("--reduce-contribs", type=int, default=8, help="worker contributions for that comparison")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
                     help="N > 1: ncclAllGather of packed bytes, or fused peer-read gather-unpack (CUDA IPC)")
     return ap.parse_args()
@@ -335,6 +338,9 @@ def main_ours(args):
     sgd = None
     if not args.no_sgd and world == 1:
         sgd = run_sgd_compare(masters, rs, dev)
+    red = None
+    if not args.no_reduce and world == 1:
+        red = run_reduce_compare(masters, rs, dev, args.reduce_contribs)
     fp32_gather = None
     if world > 1:
         fp32_gather = run_fp32_allgather(counts, world, dev) if backend == "nccl" else None
@@ -356,7 +362,7 @@ def main_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
-            "fused_sgd_pack": sgd,
+            "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -458,6 +464,65 @@ def run_sgd_compare(dev_masters, rs, dev, reps=20):
             "fused_GBps": (20 * n + pb) / (tf * 1e-3) / 1e9,
             "note": "fused: adt_sgd_pack (update + pack + norm, 20+r B/weight); unfused: torch in-place update "
                     "kernels + adt_pack"}
+
+
+def run_reduce_compare(dev_masters, rs, dev, nc=8, reps=10):
+    """SURVEY §8f #4, gradient return path: `nc` worker gradient buckets are
+    combined as net.gather_and_update does (sample-count weights, pairwise
+    tree, / total), the momentum step applied, the new masters packed + normed
+    — one adt_reduce_sgd_pack pass (reads (4·nc + 8)·n, writes (8 + r)·n) — vs
+    the unfused sequence: torch weighted pairwise sum + divide, the update as
+    in-place torch kernels, then adt_pack with the norm. On one GPU the
+    buckets are local; at N > 1 the same kernel reads peers' buckets over
+    NVLink (ShardedWeightSync.update, transport p2p)."""
+    import torch
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.grads import GradBucket
+    from paper_2004_02297_b200.layout import PackedLayout
+    counts = [m.numel() for m in dev_masters]
+    lay = PackedLayout.plan(counts, rs)
+    w = [m.clone() for m in dev_masters]
+    v = [torch.zeros_like(m) for m in dev_masters]
+    buckets = []
+    for c in range(nc):
+        b = GradBucket(counts, dev, sample_count=32 + c)
+        b.flat.normal_(0.0, 0.01)
+        buckets.append(b)
+    packed = torch.empty(lay.nbytes, dtype=torch.uint8, device=dev)
+    ss = torch.empty(len(w), dtype=torch.float64, device=dev)
+    table = engine.ReduceSgdTable(w, v, [buckets[0].byte_offset(l) for l in range(len(w))], lay)
+    pack_t = engine.SegmentTable(w, lay)
+    ptrs = [b.flat.data_ptr() for b in buckets]
+    sc = [b.sample_count for b in buckets]
+    lr, mu, wd = 1e-4, 0.9, 5e-4
+    total = float(sum(sc))
+
+    def fused():
+        engine.reduce_sgd_pack(table, ptrs, sc, lr, mu, wd, packed, ss)
+
+    def unfused():
+        level = [b.flat * float(b.sample_count) for b in buckets]
+        while len(level) > 1:
+            nxt = [level[i] + level[i + 1] for i in range(0, len(level) - 1, 2)]
+            if len(level) % 2:
+                nxt.append(level[-1])
+            level = nxt
+        g = level[0].div_(total)
+        for l, (wi, vi) in enumerate(zip(w, v)):
+            gi = g[buckets[0].offsets[l]:buckets[0].offsets[l] + counts[l]]
+            gi.add_(wi, alpha=wd)
+            vi.mul_(mu).add_(gi)
+            wi.sub_(vi, alpha=lr)
+        engine.pack(pack_t, packed, ss)
+
+    tf, tu = _time_ms(fused, reps), _time_ms(unfused, reps)
+    n = sum(counts)
+    pb = lay.total_payload_bytes
+    alg = (4 * nc + 16) * n + pb
+    return {"contributions": nc, "fused_ms": tf, "unfused_ms": tu, "speedup": tu / tf,
+            "fused_GBps": alg / (tf * 1e-3) / 1e9, "algorithmic_bytes": alg,
+            "note": "fused: adt_reduce_sgd_pack ((4*nc+16)*n + sum(n*r) B); unfused: torch weighted pairwise "
+                    "sum + div + in-place update kernels + adt_pack"}
 
 
 def run_fp32_allgather(counts, world, dev, reps=20):
