@@ -48,6 +48,15 @@ def main():
     # zero-copy from pinned host
     engine.unpack(engine.SegmentTable(outs, lay), packed.cpu().pin_memory())
     torch.cuda.synchronize()
+    # fused gradient reduce + SGD + pack (gradient return path), 1, 3 and 8 contributions
+    from paper_2004_02297_b200.grads import GradBucket
+    for nc in (1, 3, 8):
+        buckets = [GradBucket(counts, sample_count=c + 1).load([torch.randn_like(d) for d in devs])
+                   for c in range(nc)]
+        table = engine.ReduceSgdTable(devs, v, [buckets[0].byte_offset(l) for l in range(len(counts))], lay)
+        engine.reduce_sgd_pack(table, [b.flat.data_ptr() for b in buckets], [b.sample_count for b in buckets],
+                               0.01, 0.9, 5e-4, packed, norms)
+    torch.cuda.synchronize()
     print("sanitize smoke ok")
 
 
