@@ -341,12 +341,17 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
 #ifndef ADT_PACK_MIN_BLOCKS
 #define ADT_PACK_MIN_BLOCKS 6   // resident CTAs/SM the register budget must allow (A/B: profiles/r01_ab_occupancy.md)
 #endif
+// ADT_PERSISTENT = 1: grid = resident CTAs, each CTA walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ... and tracks its layer incrementally, instead of
+// one CTA per tile with a per-warp binary search over the layer table (the
+// search was ~25 % of the pack's and ~50 % of the unpack's instructions on
+// ResNet-50's 161 layers, profiles/r01d). Results do not depend on it.
+#ifndef ADT_PERSISTENT
+#define ADT_PERSISTENT 0
+#endif
+
 template <int MAXSEG, bool NORM, bool WRITE>
-__global__ void __launch_bounds__(kThreads, ADT_PACK_MIN_BLOCKS)
-adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
-    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
-    const uint32_t tile = blockIdx.x;
-    const int s = find_segment(T, tile);
+__device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
     const int r = T.round_to[s];
@@ -374,9 +379,26 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
         }
     }
 
-    if (WRITE) store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, stage[warp]);
+    if (WRITE) store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
 
     if (NORM) warp_partial(T.partials, tile, sumsq16(v));
+}
+
+template <int MAXSEG, bool NORM, bool WRITE>
+__global__ void __launch_bounds__(kThreads, ADT_PACK_MIN_BLOCKS)
+adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    uint32_t *ws = stage[threadIdx.x >> 5];
+    if (!ADT_PERSISTENT) {
+        const uint32_t tile = blockIdx.x;
+        pack_tile<MAXSEG, NORM, WRITE>(T, tile, find_segment(T, tile), ws);
+        return;
+    }
+    int s = find_segment(T, blockIdx.x);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        while (T.tile_begin[s + 1] <= tile) ++s;                   // tile_begin[nseg] = ntiles stops it
+        pack_tile<MAXSEG, NORM, WRITE>(T, tile, s, ws);
+    }
 }
 
 // -------------------------------------------------------------- unpack pass
@@ -387,18 +409,7 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T) {
 #define ADT_UNPACK_REVERSE 1   // A/B: AlexNet step 132.7 -> 127.2 us (profiles/r01_ab_unpack_order.md)
 #endif
 template <int MAXSEG>
-__global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
-adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
-    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
-#if ADT_UNPACK_REVERSE
-    // Newest-first: CTAs are dispatched roughly in blockIdx order, so walking
-    // the tiles backwards reads the payload the pack pass wrote last — the
-    // part still resident in the 126 MB L2 — before it is evicted.
-    const uint32_t tile = gridDim.x - 1 - blockIdx.x;
-#else
-    const uint32_t tile = blockIdx.x;
-#endif
-    const int s = find_segment(T, tile);
+__device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
     const int r = T.round_to[s];
@@ -437,7 +448,6 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
     }
 
     // staged per warp: r = 3 tiles and every layer's ragged last tile
-    uint32_t *ws = stage[warp];
     const uint32_t span = kWarpGroups * 4 * r, lo = warp * span, nbytes = m * r;
     if (lo >= nbytes) return;
     const uint32_t mine = min(span, nbytes - lo), n16 = mine / 16;
@@ -459,6 +469,37 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T) {
             if (g * 4 + 0 < m) dst1[g * 4 + 0] = o.x;
             if (g * 4 + 1 < m) dst1[g * 4 + 1] = o.y;
             if (g * 4 + 2 < m) dst1[g * 4 + 2] = o.z;
+        }
+    }
+    __syncwarp();   // the staging words are reused by this warp's next tile (persistent walk)
+}
+
+template <int MAXSEG>
+__global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
+adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    uint32_t *ws = stage[threadIdx.x >> 5];
+    // Newest-first (ADT_UNPACK_REVERSE): CTAs are dispatched roughly in
+    // blockIdx order, so walking the tiles backwards reads the payload the
+    // pack pass wrote last — the part still resident in the 126 MB L2 —
+    // before it is evicted.
+    if (!ADT_PERSISTENT) {
+        const uint32_t tile = ADT_UNPACK_REVERSE ? ntiles - 1 - blockIdx.x : blockIdx.x;
+        unpack_tile<MAXSEG>(T, tile, find_segment(T, tile), ws);
+        return;
+    }
+    if (ADT_UNPACK_REVERSE) {
+        int s = find_segment(T, ntiles - 1 - blockIdx.x);
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const uint32_t tile = ntiles - 1 - t;
+            while (T.tile_begin[s] > tile) --s;
+            unpack_tile<MAXSEG>(T, tile, s, ws);
+        }
+    } else {
+        int s = find_segment(T, blockIdx.x);
+        for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            while (T.tile_begin[s + 1] <= tile) ++s;
+            unpack_tile<MAXSEG>(T, tile, s, ws);
         }
     }
 }
@@ -751,12 +792,20 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *co
         if (use_tma_kernels()) {
             e = launch_tma<MAXSEG>(pass, T, ntiles, stream);
         } else {
-            const dim3 grid(ntiles), block(kThreads);
+            const dim3 block(kThreads);
+            uint32_t g = ntiles;
+            if (ADT_PERSISTENT) {
+                int sms = 0;
+                if (sm_count_cached(&sms) != ADT_OK) return ADT_ERR_NO_DEVICE;
+                const int per_sm = pass == Pass::Unpack ? ADT_UNPACK_MIN_BLOCKS : ADT_PACK_MIN_BLOCKS;
+                g = min(ntiles, static_cast<uint32_t>(sms * per_sm));
+            }
+            const dim3 grid(g);
             switch (pass) {
-                case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T); break;
-                case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T); break;
-                case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T); break;
-                case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T); break;
+                case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T, ntiles); break;
+                case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T, ntiles); break;
+                case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T, ntiles); break;
+                case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T, ntiles); break;
                 case Pass::Finalize: break;
             }
             e = cudaGetLastError();
