@@ -49,7 +49,14 @@ struct Table {
     uintptr_t weights[MAXSEG];
     uint8_t round_to[MAXSEG];
     uint8_t src_idx[MAXSEG];    // which srcs[] a layer's payload is read from (adt_unpack_multi)
+    // Coarse tile -> layer map: seg_hint[k] = the layer holding tile k << hint_shift
+    // (<= kHints buckets). A CTA starts its layer search there and steps forward
+    // over the few layer boundaries inside its bucket, instead of a per-warp
+    // binary search over the whole table (~70 warp instructions for 161 layers).
+    uint32_t hint_shift;
+    uint8_t seg_hint[1024];
 };
+constexpr int kHints = 1024;
 
 // ----------------------------------------------------------- byte compaction
 // Word w of the layer is little-endian in memory (byte 3 = MSB). The payload
@@ -111,13 +118,27 @@ __device__ __forceinline__ uint4 unpack_words(int r, const uint32_t *w) {
 // ------------------------------------------------------------------ helpers
 template <int MAXSEG>
 __device__ __forceinline__ int find_segment(const Table<MAXSEG> &T, uint32_t tile) {
-    // last s with tile_begin[s] <= tile (zero-tile layers are never selected)
-    int lo = 0, hi = T.nseg - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (T.tile_begin[mid] <= tile) lo = mid; else hi = mid - 1;
+    // last s with tile_begin[s] <= tile (zero-tile layers are never selected;
+    // tile_begin[nseg] = the tile count stops the walk)
+    int s = T.seg_hint[tile >> T.hint_shift];
+    while (T.tile_begin[s + 1] <= tile) ++s;
+    return s;
+}
+
+// Host: fill hint_shift / seg_hint for a table whose tile_begin[0..nseg] is set.
+template <typename Tab>
+void fill_hints(Tab &T, int nseg, uint32_t ntiles) {
+    uint32_t shift = 0;
+    while ((static_cast<uint64_t>(ntiles) >> shift) >= static_cast<uint64_t>(kHints)) ++shift;
+    T.hint_shift = shift;
+    int seg = 0;
+    const uint32_t nb = ntiles == 0 ? 0 : ((ntiles - 1) >> shift) + 1;
+    for (uint32_t k = 0; k < static_cast<uint32_t>(kHints); ++k) {
+        const uint32_t tile = k < nb ? (k << shift) : 0;
+        if (k < nb)
+            while (seg + 1 < nseg && T.tile_begin[seg + 1] <= tile) ++seg;
+        T.seg_hint[k] = static_cast<uint8_t>(k < nb ? seg : 0);
     }
-    return lo;
 }
 
 // float32 -> float64 widening on the integer pipe. cvt.f64.f32 (F2F) issues on
@@ -135,20 +156,6 @@ __device__ __forceinline__ double widen(uint32_t w) {
 __device__ __forceinline__ double sq_acc(double acc, uint32_t w) {
     const double d = widen(w);  // exact
     return fma(d, d, acc);      // exact square, rounded add
-}
-
-// Fixed-order CTA reduction; result valid in thread 0.
-__device__ __forceinline__ double block_sum(double v, double *red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-    }
-    return s;
 }
 
 // Norm partials: ONE float64 per warp per tile (kWarpsPerTile per tile), a
@@ -334,6 +341,7 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
     __syncwarp();
     if (lo < nbytes) warp_store_bytes(ws, dst + lo, min(span, nbytes - lo), lane);
 #endif
+    (void)warp_store_bytes;
     __syncwarp();
 }
 
@@ -548,11 +556,14 @@ struct Pairwise<1> {
 
 template <int NC, int MAXSEG>
 __device__ __forceinline__ uint32_t combine(const uint32_t *g, const SgdTable<MAXSEG> &T) {
-    if (NC == 0) return g[0];
-    float x[NC > 0 ? NC : 1];
+    if constexpr (NC == 0) {
+        return g[0];
+    } else {
+        float x[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) x[c] = __fmul_rn(__uint_as_float(g[c]), T.scale[c]);
-    return __float_as_uint(__fdiv_rn(Pairwise<NC>::run(x), T.total));
+        for (int c = 0; c < NC; ++c) x[c] = __fmul_rn(__uint_as_float(g[c]), T.scale[c]);
+        return __float_as_uint(__fdiv_rn(Pairwise<NC>::run(x), T.total));
+    }
 }
 
 __device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb, float lr, float mu, float wd) {
@@ -787,6 +798,7 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *co
         T.src_idx[i] = static_cast<uint8_t>(pass == Pass::Unpack ? segs[i].reserved : 0);
     }
     T.tile_begin[nseg] = acc;
+    fill_hints(T, nseg, acc);
     cudaError_t e = cudaSuccess;
     if (ntiles > 0 && pass != Pass::Finalize) {
         if (use_tma_kernels()) {
@@ -929,6 +941,7 @@ int launch_sgd_chunk(const adt_sgd_segment *segs, const adt_grad_segment *gsegs,
         T.src_idx[i] = 0;
     }
     T.tile_begin[nseg] = acc;
+    fill_hints(T, nseg, acc);
     cudaError_t e = cudaSuccess;
     if (ntiles > 0) e = launch_sgd_nc<MAXSEG>(T, A.nc, ntiles, stream);
     if (e == cudaSuccess && seg_sumsq != nullptr && nseg > 0)
