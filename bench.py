@@ -378,6 +378,9 @@ def main_ours(args):
     fp32_gather = None
     if world > 1:
         fp32_gather = run_fp32_allgather(counts, world, dev) if backend == "nccl" else None
+    dp = None
+    if world > 1 and not args.no_reduce:
+        dp = run_dp_update(sync, counts, world, dev, backend)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -398,7 +401,7 @@ def main_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
-            "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red,
+            "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red, "dp_update": dp,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -559,6 +562,50 @@ def run_reduce_compare(dev_masters, rs, dev, nc=8, reps=10):
             "fused_GBps": alg / (tf * 1e-3) / 1e9, "algorithmic_bytes": alg,
             "note": "fused: adt_reduce_sgd_pack ((4*nc+16)*n + sum(n*r) B); unfused: torch weighted pairwise "
                     "sum + div + in-place update kernels + adt_pack"}
+
+
+def run_dp_update(sync, counts, world, dev, backend, reps=10):
+    """N > 1, the whole data-parallel step through ShardedWeightSync.update:
+    every rank's FP32 gradient bucket -> fused [gather this rank's shard of
+    all buckets (p2p: peer loads over NVLink; nccl: all_to_all) + weighted
+    pairwise combine + momentum step + pack + norm] -> packed all-gather ->
+    unpack -> AWP observe (one 8·L-byte norm read per step). Baseline: the
+    uncompressed DDP step — all_reduce of the FP32 bucket, the momentum update
+    of the full masters as torch kernels (every rank), no weight exchange.
+    Device ms per step, max over ranks (nccl only: gloo timings are not
+    meaningful)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2004_02297_b200.grads import GradBucket
+    bucket = GradBucket(counts, dev)
+    bucket.flat.normal_(0.0, 0.01)
+    sc = [64] * world
+    lr, mu, wd = 1e-5, 0.9, 5e-4
+
+    def ours():
+        sync.update(bucket, sc, lr, mu, wd)
+
+    w = [torch.zeros(n, device=dev) for n in counts]
+    v = [torch.zeros(n, device=dev) for n in counts]
+
+    def ddp():
+        dist.all_reduce(bucket.flat)
+        for l, (wi, vi) in enumerate(zip(w, v)):
+            g = bucket.views[l].reshape(-1).div(float(sum(sc)))
+            g.add_(wi, alpha=wd)
+            vi.mul_(mu).add_(g)
+            wi.sub_(vi, alpha=lr)
+
+    t_ours = _time_ms(ours, reps)
+    t_ddp = _time_ms(ddp, reps) if backend == "nccl" else None
+    if backend != "nccl":
+        return {"ms": None, "note": "gloo test hook: exercised, not timed"}
+    t = torch.tensor([t_ours, t_ddp], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    a, b = (float(x) for x in t.tolist())
+    return {"ms": a, "fp32_ddp_ms": b, "speedup": b / a, "transport": sync.transport,
+            "note": "ShardedWeightSync.update (fused reduce+SGD+pack, packed gather, unpack, AWP observe) vs "
+                    "FP32 all_reduce + torch momentum step; device ms per step, max over ranks"}
 
 
 def run_fp32_allgather(counts, world, dev, reps=20):

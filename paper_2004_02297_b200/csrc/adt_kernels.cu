@@ -176,7 +176,10 @@ __device__ __forceinline__ void warp_partial(double *partials, uint32_t tile, do
 // t+2048, ... (coalesced; 8 loads in flight), then a fixed shuffle/CTA tree.
 // (A contiguous-run-per-thread version was uncoalesced: 28 us for AlexNet.)
 // The order depends only on the layer's partial count: bit-identical results.
-constexpr int kFinThreads = 1024;
+#ifndef ADT_FIN_THREADS
+#define ADT_FIN_THREADS 1024
+#endif
+constexpr int kFinThreads = ADT_FIN_THREADS;
 template <int MAXSEG>
 __global__ void __launch_bounds__(kFinThreads)
 adt_norm_finalize_kernel(const __grid_constant__ Table<MAXSEG> T) {
