@@ -105,6 +105,17 @@ def launches(path):
     print("| kernel | launches | mean | total share |\n|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda kv: -sum(kv[1])):
         print(f"| `{k}` | {len(v)} | {sum(v) / len(v):.2f} {rows[hdr_i + 1][ui]} | {sum(v) / all_t:.1%} |")
+    # the ADT step alone (the process also launches setup kernels: input
+    # generation, the L2-flush read): each adt_ kernel's share of the step
+    adt = {k: v for k, v in tot.items() if "adt_" in k}
+    step = sum(sum(v) / len(v) for v in adt.values())
+    if adt:
+        print("\nShare of one step (mean launch time of each adt_ kernel / their sum; ncu serialises launches, "
+              "so the side-stream finalize is counted as if it ran alone):\n")
+        print("| kernel | mean | share of step |\n|---|---|---|")
+        for k, v in sorted(adt.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
+            m = sum(v) / len(v)
+            print(f"| `{k}` | {m:.2f} {rows[hdr_i + 1][ui]} | {m / step:.1%} |")
 
 
 if __name__ == "__main__":
