@@ -46,8 +46,12 @@ class WeightSync:
     """Masters (CUDA float32 tensors, one per layer) -> packed bytes -> replicas."""
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None,
-                 replicas: Sequence[torch.Tensor] | None = None):
+                 replicas: Sequence[torch.Tensor] | None = None, graphed: bool = True):
+        """graphed: step() replays its kernels from a CUDA graph captured once
+        per packed layout (one graph launch instead of three ctypes launches
+        and the stream bookkeeping per step)."""
         engine.require_cuda()
+        self.graphed = graphed
         self.masters = [m.detach().reshape(-1) for m in masters]
         for i, m in enumerate(self.masters):
             if not m.is_cuda or m.dtype != torch.float32 or not m.is_contiguous():
@@ -210,7 +214,10 @@ class WeightSync:
         if observe is None:
             observe = self.adaptive and batch > 0
         used = self.round_tos
-        self.launch(fused_norm=observe)
+        if self.graphed:
+            self.launch_graphed(fused_norm=observe)
+        else:
+            self.launch(fused_norm=observe)
         res = SyncResult(round_tos=used)
         if not observe:
             return res
