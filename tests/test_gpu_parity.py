@@ -351,3 +351,50 @@ def test_single_layer_beyond_4gb_packed_offsets(adt):
         assert packed[3 * start:3 * (start + 4100)].cpu().numpy().tobytes() == O.pack_vectorized(hw, r)
     del bits, w, out, packed
     torch.cuda.empty_cache()
+
+
+def test_concurrent_host_threads_on_separate_streams(adt):
+    """include/adt.h: callable from several host threads on different streams
+    (no hidden mutable state; per-stream norm scratch)."""
+    import threading
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    rng = np.random.default_rng(31)
+    jobs = []
+    for t in range(4):
+        counts = [int(x) for x in rng.integers(1, 20000, 6)]
+        rs = [int(x) for x in rng.integers(1, 5, 6)]
+        hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+        jobs.append((counts, rs, hosts))
+    results, errors = [None] * len(jobs), []
+
+    def work(i):
+        try:
+            counts, rs, hosts = jobs[i]
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                devs = [torch.from_numpy(h).cuda(non_blocking=False) for h in hosts]
+                lay = PackedLayout.plan(counts, rs)
+                packed = torch.empty(lay.nbytes, dtype=torch.uint8, device="cuda")
+                ss = torch.empty(len(counts), dtype=torch.float64, device="cuda")
+                outs = [torch.empty_like(d) for d in devs]
+                for _ in range(20):
+                    engine.pack(engine.SegmentTable(devs, lay), packed, ss, s)
+                    engine.unpack(engine.SegmentTable(outs, lay), packed, s)
+                s.synchronize()
+                results[i] = (packed.cpu().numpy(), [o.cpu().numpy() for o in outs], ss.cpu().numpy(), lay)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for (counts, rs, hosts), (packed, outs, ss, lay) in zip(jobs, results):
+        for l, (h, r) in enumerate(zip(hosts, rs)):
+            lo, hi = lay.span(l)
+            assert packed[lo:hi].tobytes() == O.pack_vectorized(h, r)
+            assert np.array_equal(outs[l].view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+            assert math.sqrt(ss[l]) == pytest.approx(O.l2_norm(h), rel=NORM_RTOL)
