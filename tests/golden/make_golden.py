@@ -264,7 +264,33 @@ def reduce_sgd_cases():
     return out
 
 
+def format_cases():
+    """Text formats next to the path, rendered by the reference itself: the
+    bench-codec table and CSV (bench.py:89-104) and the AWP trace CSV
+    (training.py:304-321) for fixed rows (None deltas, inf, nan, -0.0)."""
+    import io
+    import json
+    from weightpack import bench, training
+    rows = [("scalar", 1000, 1, 1, 0.0123456789, 1.23e9), ("vectorized", 1048576, 2, 1, 0.25, 16777216.0),
+            ("parallel", 1000000, 3, 8, 1.5e-05, 2.6666e11), ("unpack", 7, 4, 1, 3.3e-6, 9.1e9),
+            ("scalar", 2097152, 1, 1, 0.1, 8.0e7), ("vectorized", 2097152, 1, 1, 0.2, 4.0e7)]
+    csv_io = io.StringIO()
+    bench.write_bench_csv(csv_io, rows)
+    trace = [(0, 0, 1.2345678901234567, None, 0, 8), (1, 0, 1.2, -0.02799999999999997, 1, 8),
+             (1, 1, 0.0, float("inf"), 0, 16), (2, 1, float("nan"), float("nan"), 0, 16), (3, 2, -0.0, 0.0, 2, 32)]
+    tr_io = io.StringIO()
+    training.write_trace_csv(tr_io, trace)
+    return {"bench_rows": rows, "bench_table": bench.render_bench_table(rows), "bench_csv": csv_io.getvalue(),
+            "bench_warnings": bench.slow_vector_warnings(rows),
+            "trace_rows": [[None if (isinstance(v, float) and v != v) else v for v in r] for r in trace],
+            "trace_nan_cells": [[isinstance(v, float) and v != v for v in r] for r in trace],
+            "trace_csv": tr_io.getvalue()}
+
+
 def main():
+    import json
+    with open(os.path.join(HERE, "golden_formats.json"), "w") as f:
+        json.dump(format_cases(), f, indent=1, allow_nan=True)
     np.savez_compressed(os.path.join(HERE, "golden_reduce_sgd.npz"), **reduce_sgd_cases())
     np.savez_compressed(os.path.join(HERE, "golden_sgd.npz"), **sgd_cases())
     np.savez_compressed(os.path.join(HERE, "golden_codec.npz"), **codec_cases())

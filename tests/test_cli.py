@@ -56,3 +56,15 @@ def test_pack_unpack_roundtrip_matches_oracle_container(tmp_path, capsys):
                           "--round-to", "3", "--output", str(tmp_path / "m.adt")], cwd=ROOT,
                          capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
+
+
+@pytest.mark.gpu
+def test_bench_codec_runs_with_precheck(tmp_path, capsys):
+    out = tmp_path / "b.csv"
+    assert cli.main(["bench-codec", "--sizes", "1000,5000", "--round-tos", "1,3", "--workers", "1,2",
+                     "--repeats", "2", "--check-size", "20000", "--csv", str(out)]) == 0
+    text = capsys.readouterr().out
+    assert "precheck passed" in text and "device_unpack" in text
+    lines = out.read_text().splitlines()
+    assert lines[0] == "path,size,round_to,workers,seconds,bytes_per_s"
+    assert len(lines) == 1 + 2 * 2 * (2 + 2 + 1 + 2)   # sizes x r x (scalar, vectorized, 2 parallel, unpack, 2 device)
