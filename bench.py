@@ -61,8 +61,9 @@ def parse():
     ap.add_argument("--reduce-contribs", type=int, default=8, help="worker contributions for that comparison")
     ap.add_argument("--l2", choices=["auto", "flush", "none"], default="auto",
                     help="flush L2 before every timed step (auto: when the FP32 masters are < 1.5x L2)")
-    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
-                    help="N > 1: ncclAllGather of packed bytes, or fused peer-read gather-unpack (CUDA IPC)")
+    ap.add_argument("--transport", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="N > 1: fused peer-read gather-unpack over CUDA IPC (p2p; auto picks it when every "
+                         "rank's GPU is a peer), or ncclAllGather of the packed bytes (nccl)")
     return ap.parse_args()
 
 
@@ -397,7 +398,8 @@ def main_ours(args):
                        "l2": (f"flushed before every timed step (read of a {2 * l2 >> 20} MB buffer outside the "
                               "events; each step timed by its own events)") if flush else
                              "FP32 masters > 1.5x L2 (working set master + packed + replica several x L2); no flush",
-                       "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single"},
+                       "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single",
+                       "transport": getattr(sync, "transport", "local")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,

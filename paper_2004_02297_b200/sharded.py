@@ -123,12 +123,36 @@ class ShardPlan:
         return out
 
 
+def peer_transport(dist, group=None) -> str:
+    """"p2p" when every rank's GPU can map every other rank's memory (NVLink /
+    NVSwitch peers on one node: the fused peer-read kernels apply), else
+    "nccl". Collective: every rank must call it; all get the same answer."""
+    dev = torch.cuda.current_device()
+    info = (socket_host(), dev)
+    everyone = [None] * dist.get_world_size(group)
+    dist.all_gather_object(everyone, info, group=group)
+    if len({h for h, _ in everyone}) != 1:
+        ok = False                                  # several hosts: no CUDA IPC
+    else:
+        ok = all(d == dev or torch.cuda.can_device_access_peer(dev, d) for _, d in everyone)
+    votes = [None] * len(everyone)
+    dist.all_gather_object(votes, ok, group=group)
+    return "p2p" if all(votes) else "nccl"
+
+
+def socket_host() -> str:
+    import socket
+    return socket.gethostname()
+
+
 class ShardedWeightSync:
     """Per-step packed weight distribution across the ranks of `group`.
 
     `masters[l]` are this rank's FP32 master tensors (full layer shape; only
     this rank's shard ranges are read), `replicas[l]` receive every weight.
 
+    transport = "auto": "p2p" when all ranks' GPUs are peers on one node,
+        else "nccl" (peer_transport).
     transport = "nccl": pack -> ncclAllGather(uint8) of the packed send
         buffers -> unpack the gathered stream.
     transport = "p2p": every rank's send buffer is mapped into every other
@@ -144,13 +168,13 @@ class ShardedWeightSync:
                  transport: str = "nccl"):
         import torch.distributed as dist
         engine.require_cuda()
-        if transport not in ("nccl", "p2p"):
-            raise ValueError("transport must be 'nccl' or 'p2p'")
+        if transport not in ("nccl", "p2p", "auto"):
+            raise ValueError("transport must be 'nccl', 'p2p' or 'auto'")
         self.dist = dist
         self.group = group
-        self.transport = transport
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.transport = peer_transport(dist, group) if transport == "auto" else transport
         self.masters = [m.detach().reshape(-1) for m in masters]
         self.counts = [m.numel() for m in self.masters]
         self.schedule = schedule if schedule is not None else FixedPrecision(len(self.masters), 32)
