@@ -233,6 +233,10 @@ class ShardedWeightSync:
     def _alloc(self, cap: int) -> None:
         nslots = 2 if self.transport == "p2p" else 1
         self._close_peers()
+        # p2p: a peer may still be reading our previous send buffers until it
+        # reaches the handle exchange below (it syncs on its own unpack first),
+        # so they stay referenced (not recycled by the caching allocator) until then.
+        retired = self.send
         self.send = [torch.zeros(cap, dtype=torch.uint8, device=self.device) for _ in range(nslots)]
         if self.transport == "nccl":
             # one rank: unpack straight from the send buffer (no gather, no copy)
@@ -254,6 +258,7 @@ class ShardedWeightSync:
                     self._opened.append(base)
                     ptrs.append(base + offset)
             self._peer.append(ptrs)
+        del retired
 
     def _close_peers(self) -> None:
         for p in self._opened:
