@@ -333,6 +333,7 @@ def main_ours(args):
                 pk_list.append(e0.elapsed_time(e1))
                 up_list.append(e1.elapsed_time(e2))
     if world > 1:
+        sync.check_barrier()
         dist.barrier()
     ms = sum(step_ms) / K if flush else e_start.elapsed_time(e_end) / K
     if world > 1:

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 6
+#define ADT_ABI_VERSION 7
 
 /* status codes */
 #define ADT_OK 0
@@ -140,6 +140,20 @@ int adt_unpack_multi(const adt_segment *segs, int nseg, const uint8_t *const *so
  * (small peer reads, e.g. every rank's norm tail). */
 int adt_copy_multi(uint8_t *dst, const uint8_t *const *sources, int nsrc, uint64_t offset, uint64_t bytes,
                    void *stream);
+
+/*
+ * Stream-ordered barrier over peer memory (replaces the NCCL all-reduce of a
+ * flag the p2p transport would otherwise use between "my pack is written" and
+ * "peers read it"; the reference's in-process workers need none,
+ * training.py:214-225). flags[q] = rank q's array of nranks uint32 epochs,
+ * mapped into this process (adt_ipc_open) — flags[rank] is local; all start
+ * at 0. state = 2 local uint32: [0] this rank's epoch counter (start 0),
+ * [1] 0, or the epoch whose wait timed out after max_polls polls (the kernel
+ * then returns instead of hanging; callers check it on their next sync).
+ * Every rank must issue the same sequence of barriers. Graph-capturable.
+ */
+int adt_peer_barrier(uint32_t *const *flags, int nranks, int rank, uint32_t *state, uint64_t max_polls,
+                     void *stream);
 
 /* CUDA IPC plumbing for adt_unpack_multi (thin wrappers over cudaIpc*):
  * handle size in bytes; export the allocation holding dev_ptr (*offset_out =

@@ -23,12 +23,12 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 6
+ABI_VERSION = 7
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
-           "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
+           "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
            "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_device_sm_count")
 
 
@@ -117,6 +117,8 @@ def load() -> ctypes.CDLL:
         lib.adt_unpack_multi.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp]
         lib.adt_copy_multi.restype = ctypes.c_int
         lib.adt_copy_multi.argtypes = [vp, P(ctypes.c_void_p), ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp]
+        lib.adt_peer_barrier.restype = ctypes.c_int
+        lib.adt_peer_barrier.argtypes = [P(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, vp, ctypes.c_uint64, vp]
         lib.adt_ipc_handle_bytes.restype = ctypes.c_int
         lib.adt_ipc_handle_bytes.argtypes = []
         lib.adt_ipc_get_handle.restype = ctypes.c_int

@@ -228,6 +228,17 @@ def copy_multi(dst: torch.Tensor, sources: Sequence[int], offset: int, nbytes: i
     _lib.check(_lib.load().adt_copy_multi(dst.data_ptr(), arr, len(sources), offset, nbytes, stream_handle(stream)))
 
 
+def peer_barrier(flag_ptrs: Sequence[int], rank: int, state: torch.Tensor, max_polls: int = 1 << 24,
+                 stream: torch.cuda.Stream | None = None) -> None:
+    """adt_peer_barrier: stream-ordered barrier over peer memory. flag_ptrs[q]
+    = rank q's int32[nranks] epoch array mapped here; state = this rank's
+    int32[2] (epoch counter, timeout epoch)."""
+    if state.dtype != torch.int32 or not state.is_cuda or state.numel() < 2:
+        raise ValueError("state must be a CUDA int32 tensor of 2 entries")
+    _lib.check(_lib.load().adt_peer_barrier(_lib.pointer_array(flag_ptrs), len(flag_ptrs), rank, state.data_ptr(),
+                                            int(max_polls), stream_handle(stream)))
+
+
 def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
     """(CUDA IPC handle of the allocation holding `t`, t's byte offset inside it)."""
     lib = _lib.load()

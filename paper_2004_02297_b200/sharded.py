@@ -190,7 +190,10 @@ class ShardedWeightSync:
         self.velocities = None     # momentum buffers (only this rank's shard ranges are stepped)
         self._gpeer = None         # p2p: (bucket data_ptr, every rank's bucket address here)
         self._gopened = []
+        self._bopened = []         # p2p: peers' barrier flag arrays mapped here
         self._grecv = None         # nccl: all-to-all'd gradient slices of this rank's shard
+        if self.transport == "p2p":
+            self._init_barrier()
         self._plan(self.schedule.round_tos())
 
     # ------------------------------------------------------------- planning
@@ -268,7 +271,7 @@ class ShardedWeightSync:
     def __del__(self):
         try:
             self._close_peers()
-            for p in self._gopened:
+            for p in self._gopened + self._bopened:
                 engine.ipc_close(p)
         except Exception:
             pass
@@ -278,16 +281,38 @@ class ShardedWeightSync:
         return list(self.plan.round_tos)
 
     # ------------------------------------------------------------- one step
+    def _init_barrier(self) -> None:
+        """p2p: every rank's epoch-flag array, IPC-mapped into every rank, for
+        the device-side barrier (adt_peer_barrier)."""
+        self._flags = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+        self._bstate = torch.zeros(2, dtype=torch.int32, device=self.device)
+        handle = engine.ipc_handle(self._flags)
+        everyone = [None] * self.world
+        self.dist.all_gather_object(everyone, handle, group=self.group)
+        self._flag_ptrs = []
+        for q in range(self.world):
+            if q == self.rank:
+                self._flag_ptrs.append(self._flags.data_ptr())
+            else:
+                base = engine.ipc_open(everyone[q][0])
+                self._bopened.append(base)
+                self._flag_ptrs.append(base + everyone[q][1])
+
     def _barrier(self) -> None:
         """Stream-ordered cross-rank barrier: every rank's pack is complete
-        (and its previous unpack, by stream order) before anyone reads."""
-        if self.dist.get_backend(self.group) == "nccl":
-            if not hasattr(self, "_flag"):
-                self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
-            self.dist.all_reduce(self._flag, group=self.group)
-        else:  # gloo (tests): host-side
-            torch.cuda.current_stream().synchronize()
-            self.dist.barrier(group=self.group)
+        (and its previous unpack, by stream order) before anyone reads. One
+        32-thread kernel: each rank stores its epoch into every peer's flag
+        array over NVLink and waits for all of them in its own — no NCCL
+        launch, no host round trip, capturable in a CUDA graph."""
+        engine.peer_barrier(self._flag_ptrs, self.rank, self._bstate)
+
+    def check_barrier(self) -> None:
+        """Raise if a device barrier gave up waiting for a peer (its bounded
+        wait returns instead of hanging the GPU)."""
+        if self.transport == "p2p":
+            bad = int(self._bstate[1].item())
+            if bad:
+                raise RuntimeError(f"rank {self.rank}: peer barrier epoch {bad} timed out waiting for a peer")
 
     def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
         """pack shard (norm finalized into the send tail) -> exchange -> unpack."""
@@ -317,6 +342,7 @@ class ShardedWeightSync:
         return send[base:base + 8 * self.plan.max_pieces].view(torch.float64)
 
     def _norms(self) -> list[float]:
+        self.check_barrier()
         S, base, m = self.plan.send_bytes, self.plan.payload_cap, self.plan.max_pieces
         if self.transport == "nccl":
             g = self.recv[:S * self.world].view(self.world, S)[:, base:base + 8 * m].contiguous()

@@ -27,7 +27,7 @@ def lib():
 def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
         ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
-         "adt_unpack_multi", "adt_copy_multi", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
+         "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
          "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_device_sm_count"])
 
 
@@ -108,3 +108,8 @@ def test_validation_happens_before_any_device_work(lib):
                                  None) == lib.ADT_ERR_ALIGN
     assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, 16, None, None) \
         == lib.ADT_ERR_ARG
+    # peer barrier: rank outside [0, nranks), too many ranks, misaligned flags, zero poll budget
+    assert h.adt_peer_barrier(lib.pointer_array([16, 32]), 2, 2, 48, 10, None) == lib.ADT_ERR_ARG
+    assert h.adt_peer_barrier(lib.pointer_array([16] * 17), 17, 0, 48, 10, None) == lib.ADT_ERR_ARG
+    assert h.adt_peer_barrier(lib.pointer_array([16, 34]), 2, 0, 48, 10, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_peer_barrier(lib.pointer_array([16, 32]), 2, 0, 48, 0, None) == lib.ADT_ERR_ARG

@@ -127,3 +127,26 @@ def test_p2p_sync_two_processes_one_gpu():
         assert ok, (rank, notes[:5])
     assert res[0][3] == res[1][3] and len(res[0][3]) > 0   # identical norm bits on both ranks
     assert res[0][4] == res[1][4] and max(res[0][4]) > 1    # both escalated identically
+
+
+def test_peer_barrier_two_virtual_ranks_and_timeout(adt):
+    """adt_peer_barrier in one process: two 'ranks' on two streams meet (each
+    publishes into the other's flag array and waits for both); a lone rank
+    times out after its poll budget, records the epoch and returns."""
+    from paper_2004_02297_b200 import engine
+    flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    states = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    ptrs = [f.data_ptr() for f in flags]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(5):
+        for r in (1, 0):
+            engine.peer_barrier(ptrs, r, states[r], stream=streams[r])
+    torch.cuda.synchronize()
+    for r in range(2):
+        assert states[r].tolist() == [5, 0]
+        assert flags[r].tolist() == [5, 5]
+    lone = torch.zeros(2, dtype=torch.int32, device="cuda")
+    lone_flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    engine.peer_barrier([f.data_ptr() for f in lone_flags], 0, lone, max_polls=2000)
+    torch.cuda.synchronize()
+    assert lone.tolist() == [1, 1]             # epoch 1 published, and its wait timed out
