@@ -260,9 +260,12 @@ def main_ours(args):
         plan = sync.plan
         pack_bytes = sum((pc.hi - pc.lo) * (4 + plan.round_tos[pc.layer]) for pc in plan.pieces[rank])
         unpack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
-    kernels_per_step = 2 + (0 if args.no_norm else 1)  # pack, unpack, norm finalize
+    # ours per step: pack, unpack, norm finalize; p2p adds the peer barrier and the norm-tail gather
+    kernels_per_step = 2 + (0 if args.no_norm else 1)
+    if world > 1 and getattr(sync, "transport", "") == "p2p":
+        kernels_per_step += 1 + (0 if args.no_norm else 1)
     fused = not args.no_norm
-    run_step = sync.launch if (args.eager or world > 1) else sync.launch_graphed
+    run_step = sync.launch if args.eager else sync.launch_graphed
 
     for _ in range(args.warmup):
         run_step(fused)
@@ -289,7 +292,7 @@ def main_ours(args):
                 torch.sum(scratch, dim=0, out=sink)
                 ev[k][0].record(stream)
                 if split:
-                    run_step(fused, mid_event=ev[k][1])
+                    sync.launch_graphed(fused, mid_event=ev[k][1])
                 else:
                     run_step(fused)
                 ev[k][2].record(stream)
@@ -327,7 +330,7 @@ def main_ours(args):
             for _ in range(K):
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record(stream)
-                run_step(fused, mid_event=e1)
+                sync.launch(fused, mid_event=e1)
                 e2.record(stream)
                 torch.cuda.synchronize()
                 pk_list.append(e0.elapsed_time(e1))

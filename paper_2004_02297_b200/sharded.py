@@ -218,6 +218,8 @@ class ShardedWeightSync:
         lay = PackedLayout(tuple(pc.hi - pc.lo for pc in mine), tuple(self.plan.round_tos[pc.layer] for pc in mine),
                            tuple(pc.offset for pc in mine), self.plan.payload_cap)
         self.pack_table = engine.SegmentTable(views, lay)
+        if getattr(self, "_partials", None) is None or self._partials.numel() < self.pack_table.npartials:
+            self._partials = torch.empty(max(1, self.pack_table.npartials), dtype=torch.float64, device=self.device)
         outs, cnt, rs, offs, srcs = [], [], [], [], []
         for q in range(self.world):
             for pc in self.plan.pieces[q]:
@@ -230,6 +232,7 @@ class ShardedWeightSync:
         self.unpack_layout = PackedLayout(tuple(cnt), tuple(rs), tuple(offs), S * self.world)
         self.grad_ranges = shard_ranges(self.plan, self.counts)
         self._reduce_table = None
+        self._graphs = None
         self.unpack_table = engine.SegmentTable(outs, self.unpack_layout,
                                                 sources=srcs if self.transport == "p2p" else None)
 
@@ -328,14 +331,40 @@ class ShardedWeightSync:
             return
         slot = self._slot
         self._slot ^= 1
+        self._p2p_step(slot, fused_norm, mid_event)
+
+    def _p2p_step(self, slot: int, fused_norm: bool, mid_event=None) -> None:
         send = self.send[slot]
-        engine.pack(self.pack_table, send, self._tail(send) if fused_norm else None)
+        engine.pack(self.pack_table, send, self._tail(send) if fused_norm else None,
+                    partials=self._partials if fused_norm else None)
         self._barrier()
         if mid_event is not None:
             mid_event.record(torch.cuda.current_stream())
         if fused_norm:
             engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
         engine.unpack_multi(self.unpack_table, self._peer[slot])
+
+    def launch_graphed(self, fused_norm: bool) -> None:
+        """p2p: launch() replayed from CUDA graphs — every op of the step is a
+        device kernel (pack, the peer barrier with its device-side epoch, the
+        tail gather, the fused gather-unpack), so one graph per send slot
+        captures it and a step costs one graph launch. Other transports run
+        eagerly."""
+        if self.transport != "p2p":
+            self.launch(fused_norm)
+            return
+        key = (fused_norm, self.plan)
+        if getattr(self, "_graphs", None) is None or self._graphs[0] != key:
+            graphs = []
+            for slot in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._p2p_step(slot, fused_norm)
+                graphs.append(g)
+            self._graphs = (key, graphs)
+        slot = self._slot
+        self._slot ^= 1
+        self._graphs[1][slot].replay()
 
     def _tail(self, send: torch.Tensor) -> torch.Tensor:
         base = self.plan.payload_cap

@@ -150,3 +150,57 @@ def test_peer_barrier_two_virtual_ranks_and_timeout(adt):
     engine.peer_barrier([f.data_ptr() for f in lone_flags], 0, lone, max_polls=2000)
     torch.cuda.synchronize()
     assert lone.tolist() == [1, 1]             # epoch 1 published, and its wait timed out
+
+
+def _graphed_main(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2004_02297_b200.precision import FixedPrecision
+        from paper_2004_02297_b200.sharded import ShardedWeightSync
+        counts = [500, 3 * 4096 + 17, 25000]
+        rng = np.random.default_rng(5)
+        hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+        masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+
+        class Mixed(FixedPrecision):
+            def round_tos(self):
+                return [1, 3, 2]
+
+        sync = ShardedWeightSync(masters, Mixed(len(counts), 32), transport="p2p")
+        for _ in range(5):                      # both slots' graphs, replayed several times
+            sync.launch_graphed(True)
+        torch.cuda.synchronize()
+        sync.check_barrier()
+        ok = all(np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32),
+                                h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+                 for i, (h, r) in enumerate(zip(hosts, [1, 3, 2])))
+        norms = sync._norms()
+        ok &= all(abs(n - O.l2_norm(h)) <= 1e-6 * O.l2_norm(h) for n, h in zip(norms, hosts))
+        q.put((rank, ok, ""))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+
+
+def test_p2p_graphed_step_two_processes_one_gpu():
+    """ShardedWeightSync.launch_graphed: pack, device barrier, tail gather and
+    gather-unpack captured in one CUDA graph per send slot."""
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_graphed_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, note in res:
+        assert ok, (rank, note)
