@@ -681,8 +681,8 @@ def run_e2e_weightsync(args, dev_masters, rs, dev):
     def one():
         for m, h in zip(masters, host):
             m.copy_(h, non_blocking=True)
-        sync.launch(fused_norm=True)
-        sync._read_norms()  # D2H of the L float64 sums + host sync
+        sync.launch_graphed(fused_norm=True)   # the step's CUDA graph (as WeightSync.step)
+        sync.read_norms()                      # D2H of the L float64 sums + host sync
 
     for _ in range(3):
         one()

@@ -202,7 +202,9 @@ class WeightSync:
             rest()
         return g_pack, g_rest
 
-    def _read_norms(self) -> list[float]:
+    def read_norms(self) -> list[float]:
+        """Per-layer l2 norms (precision.l2_norm) of the masters as of the last
+        launch with the norm fused: one 8·L-byte device->host read + sync."""
         self._side.wait_stream(torch.cuda.current_stream())  # graphed finalize runs on the main stream's graph
         with torch.cuda.stream(self._side):  # queued behind the (eager) finalize
             self._host_sumsq.copy_(self.sumsq, non_blocking=True)
@@ -221,7 +223,7 @@ class WeightSync:
         res = SyncResult(round_tos=used)
         if not observe:
             return res
-        res.trace = self.schedule.observe_all(self._read_norms(), batch=batch - 1)
+        res.trace = self.schedule.observe_all(self.read_norms(), batch=batch - 1)
         new = self.schedule.round_tos()
         if new != used:
             self._plan(new)
@@ -310,7 +312,7 @@ class WeightSync:
         engine.unpack(self.unpack_table, self.packed, main)
         used = self.round_tos
         res = SyncResult(round_tos=used)
-        norms = self._read_norms()
+        norms = self.read_norms()
         bad = [i for i, n in enumerate(norms) if not math.isfinite(n)]
         if bad:
             raise NonFiniteParameters(f"layer {bad[0]} parameters left the finite range")
@@ -331,7 +333,7 @@ class WeightSync:
             main.wait_event(self._fin_done)
         engine.sumsq(self.pack_table, self.sumsq)
         self._side.wait_stream(main)
-        return self._read_norms()
+        return self.read_norms()
 
     def observe_final(self, batch: int) -> list[tuple]:
         """Norm-only pass over the masters (the observation after the last

@@ -256,7 +256,7 @@ def test_graphed_step_matches_eager(adt):
     sched = adt.FixedPrecision(len(masters), 24)
     a = adt.WeightSync(masters, sched)
     a.launch(fused_norm=True)
-    eager = (a.packed.clone(), [r.clone() for r in a.replicas], a._read_norms())
+    eager = (a.packed.clone(), [r.clone() for r in a.replicas], a.read_norms())
     b = adt.WeightSync(masters, sched)
     for _ in range(3):
         b.launch_graphed(fused_norm=True)
@@ -265,7 +265,7 @@ def test_graphed_step_matches_eager(adt):
         lo, hi = a.layout.span(i)
         assert torch.equal(b.packed[lo:hi], eager[0][lo:hi])
     assert all(torch.equal(x, y) for x, y in zip(b.replicas, eager[1]))
-    assert b._read_norms() == eager[2]
+    assert b.read_norms() == eager[2]
 
 
 # ------------------------------------------- fused SGD + pack
