@@ -8,8 +8,8 @@ reference (golden_reduce_sgd.npz, produced by the reference itself); AWP
 decisions identical; norms within 1e-6 relative.
 
 The multi-rank form (ShardedWeightSync.update, p2p transport: the peers'
-gradient buckets read over CUDA IPC inside the kernel) runs as two processes
-sharing cuda:0 — the boxes have one GPU.
+gradient buckets read over CUDA IPC inside the kernel, the device-side peer
+barrier) runs as 2 and 3 processes sharing cuda:0 — the boxes have one GPU.
 """
 
 import math
@@ -175,7 +175,7 @@ def _rank_main(rank, world, port, q):
         counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
         L = len(counts)
         hp = (0.05, 0.9, 5e-4)
-        sc = [48, 80]
+        sc = [48, 80, 17][:world]
         rng = np.random.default_rng(11)          # same stream on both ranks
         w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
         v_ref = [np.zeros(n, np.float32) for n in counts]
@@ -217,14 +217,15 @@ def _rank_main(rank, world, port, q):
         q.put((rank, False, [traceback.format_exc()], [], []))
 
 
-def test_sharded_update_p2p_two_processes_one_gpu():
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_update_p2p_processes_sharing_one_gpu(world):
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs])
@@ -232,5 +233,5 @@ def test_sharded_update_p2p_two_processes_one_gpu():
         p.join(timeout=60)
     for rank, ok, notes, _, _ in res:
         assert ok, (rank, notes[:5])
-    assert res[0][3] == res[1][3] and len(res[0][3]) > 0
-    assert res[0][4] == res[1][4] and max(res[0][4]) > 1
+    assert all(r[3] == res[0][3] for r in res) and len(res[0][3]) > 0   # identical norm bits on every rank
+    assert all(r[4] == res[0][4] for r in res) and max(res[0][4]) > 1
