@@ -39,6 +39,8 @@ from .precision import (  # noqa: F401
     UnknownLayer,
     change_rate,
     l2_norm,
+    l2_norm_many,
+    write_trace_csv,
 )
 from .sync import NonFiniteParameters, SyncResult, WeightSync  # noqa: F401
 

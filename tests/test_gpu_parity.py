@@ -398,3 +398,13 @@ def test_concurrent_host_threads_on_separate_streams(adt):
             assert packed[lo:hi].tobytes() == O.pack_vectorized(h, r)
             assert np.array_equal(outs[l].view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
             assert math.sqrt(ss[l]) == pytest.approx(O.l2_norm(h), rel=NORM_RTOL)
+
+
+def test_l2_norm_many_matches_per_layer_and_golden(adt, golden_norms):
+    xs = [x for x, _ in golden_norms]
+    got = adt.l2_norm_many(xs)
+    for (x, want), g in zip(golden_norms, got):
+        assert g == adt.l2_norm(x)
+        assert g == pytest.approx(want, rel=NORM_RTOL, abs=0.0) if want else g == 0.0
+    devs = [torch.from_numpy(np.asarray(x, np.float32)).cuda() for x in xs]
+    assert adt.l2_norm_many(devs) == got
