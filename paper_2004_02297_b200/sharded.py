@@ -384,7 +384,7 @@ class ShardedWeightSync:
         if observe is None:
             observe = self.adaptive and batch > 0
         used = self.round_tos
-        self.launch(fused_norm=observe)
+        self.launch_graphed(fused_norm=observe)   # p2p: one graph replay; nccl: eager
         res = SyncResult(round_tos=used)
         if not observe:
             return res
