@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 7
+#define ADT_ABI_VERSION 8
 
 /* status codes */
 #define ADT_OK 0
@@ -202,6 +202,75 @@ int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *con
                         const int64_t *sample_counts, int ncontrib, float lr, float momentum,
                         float weight_decay, uint8_t *packed, double *seg_sumsq, double *partials,
                         void *stream);
+
+/*
+ * Device-resident AWP step (single-device WeightSync(awp_on_device=True)).
+ * The reference decides widths on the host between two packs
+ * (precision.py:125-141, training.py:246-254, then :209-213); here the
+ * decision runs on the GPU so a whole step replays as one CUDA graph with no
+ * device->host read. Layers use capacity offsets (room for 4 bytes/weight,
+ * segs[l].round_to must be 4); the width in force for layer l is A[l]
+ * (device memory). Per step:
+ *   adt_pack_dyn(A) -> [adt_norm_finalize -> adt_awp_observe(-> B)] || adt_unpack_dyn(A)
+ *   -> adt_awp_fixup(A, B) -> copy B to A
+ * adt_awp_observe advances each group's state, writes one trace row per layer
+ * (TRACE_HEADER, precision.py:18) into a ring of ring_steps steps and stores
+ * the new widths in widths_out (B); the fixup re-packs (from the masters) and
+ * re-unpacks only the layers whose width rose.
+ */
+typedef struct adt_awp_config {
+    double threshold;        /* T (precision.py:46-54) */
+    int32_t interval;        /* INTERVAL */
+    int32_t step_bits;       /* N */
+    int32_t max_bits;
+    int32_t consecutive;     /* 0 = cumulative counter (the default) */
+} adt_awp_config;
+
+typedef struct adt_awp_group {   /* LayerPrecisionState, precision.py:67-74 */
+    double prev_norm;
+    double last_delta;
+    int32_t bits;
+    int32_t counter;
+    int32_t has_prev;            /* prev_norm is not None */
+    int32_t has_delta;           /* last_delta is not None */
+} adt_awp_group;
+
+typedef struct adt_awp_row {     /* (batch, layer, norm, delta, counter, bits) */
+    double norm;
+    double delta;                /* valid when has_delta */
+    int32_t batch;
+    int32_t layer;
+    int32_t counter;
+    int32_t bits;
+    int32_t has_delta;
+    int32_t pad;
+} adt_awp_row;
+
+typedef struct adt_awp_device {  /* all pointers: device memory */
+    adt_awp_group *groups;       /* [ngroups] */
+    const int32_t *members;      /* [nlayers] layer ids grouped by group, in layer order within a group */
+    const int32_t *member_start; /* [ngroups + 1] */
+    uint8_t *widths_out;         /* [nlayers] bytes per weight after this observation (1..4) */
+    void *reserved_ptr;          /* NULL */
+    adt_awp_row *ring;           /* [ring_steps * nlayers] trace rows, step slot = counter[0] % ring_steps */
+    int64_t *counter;            /* [2]: observations so far, batch label of the next observation */
+    int32_t nlayers;
+    int32_t ngroups;
+    int32_t ring_steps;
+    int32_t reserved;            /* 0 */
+} adt_awp_device;
+
+/* adt_pack (norm partials only, finalize separately) with the widths read from device memory. */
+int adt_pack_dyn(const adt_segment *segs, int nseg, uint8_t *packed, double *partials, const uint8_t *widths,
+                 void *stream);
+/* adt_unpack with the widths read from device memory. */
+int adt_unpack_dyn(const adt_segment *segs, int nseg, const uint8_t *packed, const uint8_t *widths, void *stream);
+/* One AWP observation of every layer from the finalized sums of squares. */
+int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg, void *stream);
+/* Re-pack + re-unpack of the layers with widths_new[l] != widths_prev[l]; masters[l] and
+ * replicas[l] share count / offset (capacity layout, round_to 4). */
+int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
+                  const uint8_t *widths_prev, const uint8_t *widths_new, void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

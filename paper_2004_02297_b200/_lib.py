@@ -23,13 +23,14 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 7
+ABI_VERSION = 8
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
            "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
-           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_device_sm_count")
+           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn",
+           "adt_awp_observe", "adt_awp_fixup", "adt_device_sm_count")
 
 
 class Segment(ctypes.Structure):
@@ -70,6 +71,37 @@ class GradSegment(ctypes.Structure):
         ("round_to", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
     ]
+
+
+class AwpConfig(ctypes.Structure):
+    """adt_awp_config (include/adt.h)."""
+
+    _fields_ = [("threshold", ctypes.c_double), ("interval", ctypes.c_int32), ("step_bits", ctypes.c_int32),
+                ("max_bits", ctypes.c_int32), ("consecutive", ctypes.c_int32)]
+
+
+class AwpGroup(ctypes.Structure):
+    """adt_awp_group: one LayerPrecisionState (32 bytes, device memory)."""
+
+    _fields_ = [("prev_norm", ctypes.c_double), ("last_delta", ctypes.c_double), ("bits", ctypes.c_int32),
+                ("counter", ctypes.c_int32), ("has_prev", ctypes.c_int32), ("has_delta", ctypes.c_int32)]
+
+
+class AwpRow(ctypes.Structure):
+    """adt_awp_row: one trace row (40 bytes, device memory)."""
+
+    _fields_ = [("norm", ctypes.c_double), ("delta", ctypes.c_double), ("batch", ctypes.c_int32),
+                ("layer", ctypes.c_int32), ("counter", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("has_delta", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class AwpDevice(ctypes.Structure):
+    """adt_awp_device: device pointers of the on-GPU controller."""
+
+    _fields_ = [("groups", ctypes.c_void_p), ("members", ctypes.c_void_p), ("member_start", ctypes.c_void_p),
+                ("widths_out", ctypes.c_void_p), ("reserved_ptr", ctypes.c_void_p), ("ring", ctypes.c_void_p),
+                ("counter", ctypes.c_void_p), ("nlayers", ctypes.c_int32), ("ngroups", ctypes.c_int32),
+                ("ring_steps", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class AdtError(RuntimeError):
@@ -134,6 +166,14 @@ def load() -> ctypes.CDLL:
         lib.adt_reduce_sgd_pack.argtypes = [P(GradSegment), ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int64),
                                             ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                             vp, vp, vp, vp]
+        lib.adt_pack_dyn.restype = ctypes.c_int
+        lib.adt_pack_dyn.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
+        lib.adt_unpack_dyn.restype = ctypes.c_int
+        lib.adt_unpack_dyn.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
+        lib.adt_awp_observe.restype = ctypes.c_int
+        lib.adt_awp_observe.argtypes = [vp, P(AwpDevice), P(AwpConfig), vp]
+        lib.adt_awp_fixup.restype = ctypes.c_int
+        lib.adt_awp_fixup.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_sumsq.restype = ctypes.c_int
         lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_device_sm_count.restype = ctypes.c_int

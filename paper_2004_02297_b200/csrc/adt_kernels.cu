@@ -28,6 +28,7 @@
 #include <dlfcn.h>
 
 #include "adt.h"
+#include <math_constants.h>
 
 namespace {
 
@@ -55,8 +56,17 @@ struct Table {
     // binary search over the whole table (~70 warp instructions for 161 layers).
     uint32_t hint_shift;
     uint8_t seg_hint[1024];
+    // Device-resident AWP (adt_pack_dyn / adt_unpack_dyn): per-layer widths read
+    // from device memory (chunk-relative) instead of round_to[], so a width
+    // change decided on the device needs no new launch table. nullptr = round_to[].
+    const uint8_t *dyn_r;
 };
 constexpr int kHints = 1024;
+
+template <int MAXSEG>
+__device__ __forceinline__ int width_of(const Table<MAXSEG> &T, int s) {
+    return T.dyn_r != nullptr ? static_cast<int>(T.dyn_r[s]) : static_cast<int>(T.round_to[s]);
+}
 
 // ----------------------------------------------------------- byte compaction
 // Word w of the layer is little-endian in memory (byte 3 = MSB). The payload
@@ -365,7 +375,7 @@ template <int MAXSEG, bool NORM, bool WRITE>
 __device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
-    const int r = T.round_to[s];
+    const int r = width_of(T, s);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g0 = warp * kWarpGroups + lane;                 // group of j = 0
     const uint4 *src = reinterpret_cast<const uint4 *>(T.weights[s]) + e0 / 4;
@@ -423,7 +433,7 @@ template <int MAXSEG>
 __device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
-    const int r = T.round_to[s];
+    const int r = width_of(T, s);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g0 = warp * kWarpGroups + lane;
     const uint8_t *src = T.srcs[T.src_idx[s]] + T.offset[s] + e0 * r;
@@ -592,7 +602,7 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
     const int s = find_segment(T, tile);
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
-    const int r = T.round_to[s];
+    const int r = width_of(T, s);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g0 = warp * kWarpGroups + lane;
     uint4 *wp = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
@@ -713,6 +723,138 @@ __global__ void __launch_bounds__(32) adt_peer_barrier_kernel(const __grid_const
     }
 }
 
+// ------------------------------------------------ device-resident AWP step
+// Algorithm 1 (precision.py:125-141) on the device, so the
+// width decision of a step needs no host round trip and the whole step
+// (pack -> [finalize -> observe] || unpack -> fixup) replays as one graph.
+// One CTA; thread g walks group g's layers in layer order (groups share one
+// state, observed sequentially as in the reference; independent groups run
+// in parallel). float64 arithmetic in the reference's operation order:
+// norm = sqrt(sum of squares) (IEEE, as math.sqrt), delta = (n - prev) / prev.
+constexpr int kAwpThreads = 256;
+__global__ void __launch_bounds__(kAwpThreads)
+adt_awp_observe_kernel(const double *__restrict__ seg_sumsq, const __grid_constant__ adt_awp_device D,
+                       const __grid_constant__ adt_awp_config C) {
+    __shared__ int64_t slot_batch[2];
+    if (threadIdx.x == 0) {
+        slot_batch[0] = D.counter[0] % D.ring_steps;
+        slot_batch[1] = D.counter[1];
+    }
+    __syncthreads();
+    adt_awp_row *rows = D.ring + slot_batch[0] * D.nlayers;
+    const int32_t batch = static_cast<int32_t>(slot_batch[1]);
+    for (int g = threadIdx.x; g < D.ngroups; g += blockDim.x) {
+        adt_awp_group st = D.groups[g];
+        const int32_t lo = D.member_start[g], hi = D.member_start[g + 1];
+        for (int32_t k = lo; k < hi; ++k) {
+            const int32_t l = D.members[k];
+            const double n = sqrt(seg_sumsq[l]);
+            if (st.has_prev) {
+                double delta;
+                if (st.prev_norm > 0.0) delta = __ddiv_rn(__dsub_rn(n, st.prev_norm), st.prev_norm);
+                else delta = (n == 0.0) ? 0.0 : CUDART_INF;
+                st.last_delta = delta;
+                st.has_delta = 1;
+                if (delta < C.threshold) st.counter += 1;        // NaN never counts
+                else if (C.consecutive) st.counter = 0;
+            } else {
+                st.has_delta = 0;
+            }
+            if (st.counter == C.interval) {                      // also on the first observation
+                st.bits = min(st.bits + C.step_bits, C.max_bits);
+                st.counter = 0;
+            }
+            st.prev_norm = n;
+            st.has_prev = 1;
+            adt_awp_row row;
+            row.norm = n;
+            row.delta = st.has_delta ? st.last_delta : 0.0;
+            row.batch = batch;
+            row.layer = l;
+            row.counter = st.counter;
+            row.bits = st.bits;
+            row.has_delta = st.has_delta;
+            row.pad = 0;
+            rows[l] = row;
+        }
+        D.groups[g] = st;
+        const uint8_t w = static_cast<uint8_t>((st.bits + 7) / 8);   // bits_to_round_to
+        for (int32_t k = lo; k < hi; ++k) D.widths_out[D.members[k]] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        D.counter[0] += 1;
+        D.counter[1] += 1;
+    }
+}
+
+// Re-pack of the layers whose width the observation just raised: their
+// payload was written (and speculatively unpacked) at the old width; read the
+// master tile again, store its top widths_new bytes into the packed buffer
+// and the matching replica words (the reference re-packs at the new widths
+// and unpacks that, training.py:209-225). CTAs stride over the tiles of the
+// escalated layers only; with no escalation every CTA scans the widths and exits.
+template <int MAXSEG>
+struct FixupTable {
+    Table<MAXSEG> T;                 // replicas (weights[]), offsets, tile map; packed_out = the packed buffer
+    uintptr_t masters[MAXSEG];
+    const uint8_t *widths_prev;
+    const uint8_t *widths_new;
+};
+
+template <int MAXSEG>
+__global__ void __launch_bounds__(kThreads)
+adt_awp_fixup_kernel(const __grid_constant__ FixupTable<MAXSEG> F) {
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    const Table<MAXSEG> &T = F.T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *ws = stage[warp];
+    uint32_t vt = blockIdx.x;                            // virtual tile index over escalated layers
+    for (int s = 0; s < T.nseg; ++s) {
+        const int r = F.widths_new[s];
+        const uint32_t nt = T.tile_begin[s + 1] - T.tile_begin[s];
+        if (r == F.widths_prev[s] || nt == 0) continue;
+        for (; vt < nt; vt += gridDim.x) {
+            const uint32_t local = vt;
+            const uint64_t e0 = static_cast<uint64_t>(local) * kTile;
+            const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
+            const uint32_t g0 = warp * kWarpGroups + lane;
+            const uint4 *src = reinterpret_cast<const uint4 *>(F.masters[s]) + e0 / 4;
+            const uint32_t *src1 = reinterpret_cast<const uint32_t *>(src);
+            const uint32_t keep = 0xFFFFFFFFu << (8 * (4 - r));
+            uint4 v[kVec];
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) {
+                const uint32_t g = g0 + 32 * k, i = g * 4;
+                if (i + 4 <= m) {
+                    v[k] = src[g];
+                } else {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
+                    v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+            store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
+            uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
+            uint32_t *dst1 = reinterpret_cast<uint32_t *>(dst);
+#pragma unroll
+            for (int k = 0; k < kVec; ++k) {
+                const uint32_t g = g0 + 32 * k, i = g * 4;
+                const uint4 o = make_uint4(v[k].x & keep, v[k].y & keep, v[k].z & keep, v[k].w & keep);
+                if (i + 4 <= m) {
+                    dst[g] = o;
+                } else {
+                    if (i + 0 < m) dst1[i + 0] = o.x;
+                    if (i + 1 < m) dst1[i + 1] = o.y;
+                    if (i + 2 < m) dst1[i + 2] = o.z;
+                }
+            }
+        }
+        vt -= nt;                                        // continue the stride in the next escalated layer
+    }
+}
+
 // ----------------------------------------------------------------- host side
 enum class Pass { Pack, PackNorm, Norm, Unpack, Finalize };
 
@@ -821,8 +963,9 @@ int validate(const adt_segment *segs, int nseg, const void *packed, bool need_pa
 template <int MAXSEG>
 int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc,
                  uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, bool finalize,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, const uint8_t *dyn_r = nullptr) {
     Table<MAXSEG> T;
+    T.dyn_r = dyn_r;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = (srcs != nullptr && i < nsrc) ? srcs[i] : nullptr;
     T.packed_out = pout;
     T.seg_sumsq = seg_sumsq;
@@ -842,7 +985,7 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *co
     fill_hints(T, nseg, acc);
     cudaError_t e = cudaSuccess;
     if (ntiles > 0 && pass != Pass::Finalize) {
-        if (use_tma_kernels()) {
+        if (use_tma_kernels() && dyn_r == nullptr) {
             e = launch_tma<MAXSEG>(pass, T, ntiles, stream);
         } else {
             const dim3 block(kThreads);
@@ -877,7 +1020,7 @@ constexpr int kLargeSeg = 256;
 // offsets of a chunk depend only on `segs`, so a separate finalize call
 // (adt_norm_finalize) walks exactly the chunks the pack pass wrote.
 int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc, uint8_t *pout,
-        double *seg_sumsq, double *partials, bool finalize, void *stream_v) {
+        double *seg_sumsq, double *partials, bool finalize, void *stream_v, const uint8_t *dyn_r = nullptr) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
     uint64_t partial_base = 0;
     int base = 0;
@@ -893,8 +1036,10 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs
         double *ss = seg_sumsq ? seg_sumsq + base : nullptr;
         double *pp = partials ? partials + partial_base : nullptr;
         const int st = cnt <= kSmallSeg
-            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream)
-            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles), finalize, stream);
+            ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles),
+                                      finalize, stream, dyn_r ? dyn_r + base : nullptr)
+            : launch_chunk<kLargeSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles),
+                                      finalize, stream, dyn_r ? dyn_r + base : nullptr);
         if (st != ADT_OK) return st;
         partial_base += tiles * kWarpsPerTile;
         base += cnt;
@@ -948,6 +1093,7 @@ template <int MAXSEG>
 int launch_sgd_chunk(const adt_sgd_segment *segs, const adt_grad_segment *gsegs, int nseg, const SgdArgs &A,
                      uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, cudaStream_t stream) {
     SgdTable<MAXSEG> T;
+    T.dyn_r = nullptr;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) {
         T.srcs[i] = A.srcs[i];
         T.scale[i] = A.scale[i];
@@ -1217,6 +1363,98 @@ int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *con
     if (any && (packed == nullptr)) return ADT_ERR_ARG;
     if (any && reinterpret_cast<uintptr_t>(packed) % 16) return ADT_ERR_ALIGN;
     return run_sgd(nullptr, segs, nseg, A, packed, seg_sumsq, partials, static_cast<cudaStream_t>(stream));
+}
+
+int adt_pack_dyn(const adt_segment *segs, int nseg, uint8_t *packed, double *partials, const uint8_t *widths,
+                 void *stream) {
+    const int v = validate(segs, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && widths == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (segs[i].round_to != 4) return ADT_ERR_ARG;   // capacity layout
+    return run(partials ? Pass::PackNorm : Pass::Pack, segs, nseg, nullptr, 0, packed, nullptr, partials, false,
+               stream, widths);
+}
+
+int adt_unpack_dyn(const adt_segment *segs, int nseg, const uint8_t *packed, const uint8_t *widths, void *stream) {
+    const int v = validate(segs, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && widths == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (segs[i].round_to != 4) return ADT_ERR_ARG;
+    const uint8_t *srcs[1] = {packed};
+    return run(Pass::Unpack, segs, nseg, srcs, 1, nullptr, nullptr, nullptr, false, stream, widths);
+}
+
+int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg, void *stream) {
+    if (seg_sumsq == nullptr || dev == nullptr || cfg == nullptr) return ADT_ERR_ARG;
+    const adt_awp_device &D = *dev;
+    if (D.nlayers < 1 || D.ngroups < 1 || D.ngroups > D.nlayers || D.ring_steps < 1 || D.reserved != 0) return ADT_ERR_ARG;
+    if (!D.groups || !D.members || !D.member_start || !D.widths_out || !D.ring || !D.counter || D.reserved_ptr)
+        return ADT_ERR_ARG;
+    if (cfg->interval < 1 || cfg->step_bits < 1 || cfg->max_bits < 1 || cfg->max_bits > 32) return ADT_ERR_ARG;
+    adt_awp_observe_kernel<<<1, kAwpThreads, 0, static_cast<cudaStream_t>(stream)>>>(seg_sumsq, D, *cfg);
+    return cuda_status(cudaGetLastError());
+}
+
+extern "C++" {
+namespace {
+template <int MAXSEG>
+int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
+                       const uint8_t *widths_prev, const uint8_t *widths_new, cudaStream_t stream) {
+    FixupTable<MAXSEG> F;
+    Table<MAXSEG> &T = F.T;
+    for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = nullptr;
+    T.packed_out = packed;
+    T.seg_sumsq = nullptr;
+    T.partials = nullptr;
+    T.dyn_r = nullptr;
+    T.nseg = nseg;
+    uint32_t acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+        T.tile_begin[i] = acc;
+        acc += static_cast<uint32_t>((replicas[i].count + kTile - 1) / kTile);
+        T.count[i] = replicas[i].count;
+        T.offset[i] = replicas[i].offset;
+        T.weights[i] = reinterpret_cast<uintptr_t>(replicas[i].weights);
+        T.round_to[i] = 4;
+        T.src_idx[i] = 0;
+        F.masters[i] = reinterpret_cast<uintptr_t>(masters[i].weights);
+    }
+    T.tile_begin[nseg] = acc;
+    fill_hints(T, nseg, acc);
+    F.widths_prev = widths_prev;
+    F.widths_new = widths_new;
+    int sms = 0;
+    if (sm_count_cached(&sms) != ADT_OK) return ADT_ERR_NO_DEVICE;
+    const uint32_t grid = max(1u, min(acc, static_cast<uint32_t>(4 * sms)));
+    adt_awp_fixup_kernel<MAXSEG><<<grid, kThreads, 0, stream>>>(F);
+    return cuda_status(cudaGetLastError());
+}
+}  // namespace
+}  // extern "C++"
+
+int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
+                  const uint8_t *widths_prev, const uint8_t *widths_new, void *stream) {
+    int v = validate(replicas, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    if ((v = validate(masters, nseg, packed, true)) != ADT_OK) return v;
+    if (nseg > 0 && (widths_prev == nullptr || widths_new == nullptr)) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (replicas[i].round_to != 4 || masters[i].count != replicas[i].count ||
+            masters[i].offset != replicas[i].offset)
+            return ADT_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int base = 0; base < nseg; base += kLargeSeg) {
+        const int cnt = min(kLargeSeg, nseg - base);
+        const int st = cnt <= kSmallSeg
+            ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, widths_prev + base,
+                                            widths_new + base, s)
+            : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, widths_prev + base,
+                                            widths_new + base, s);
+        if (st != ADT_OK) return st;
+    }
+    return ADT_OK;
 }
 
 int adt_device_sm_count(int *sm_count) {

@@ -296,3 +296,33 @@ def sm_count() -> int:
     v = ctypes.c_int(0)
     _lib.check(_lib.load().adt_device_sm_count(ctypes.byref(v)))
     return int(v.value)
+
+
+# ------------------------------------------------- device-resident AWP step
+def pack_dyn(table: SegmentTable, packed: torch.Tensor, widths: torch.Tensor, partials: torch.Tensor | None = None,
+             stream: torch.cuda.Stream | None = None) -> None:
+    """adt_pack_dyn: capacity-layout table (round_to 4), per-layer widths read
+    from the device uint8 tensor `widths`; optional norm partials."""
+    _lib.check(_lib.load().adt_pack_dyn(table.array, table.nseg, packed.data_ptr(),
+                                        partials.data_ptr() if partials is not None else None,
+                                        widths.data_ptr(), stream_handle(stream)))
+
+
+def unpack_dyn(table: SegmentTable, packed: torch.Tensor, widths: torch.Tensor,
+               stream: torch.cuda.Stream | None = None) -> None:
+    """adt_unpack_dyn: the inverse of pack_dyn at the same device widths."""
+    _lib.check(_lib.load().adt_unpack_dyn(table.array, table.nseg, packed.data_ptr(), widths.data_ptr(),
+                                          stream_handle(stream)))
+
+
+def awp_observe(sumsq: torch.Tensor, device_struct, config_struct, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_awp_observe: one device-side AWP observation of every layer."""
+    _lib.check(_lib.load().adt_awp_observe(sumsq.data_ptr(), ctypes.byref(device_struct), ctypes.byref(config_struct),
+                                           stream_handle(stream)))
+
+
+def awp_fixup(masters: SegmentTable, replicas: SegmentTable, packed: torch.Tensor, widths_prev: torch.Tensor,
+              widths_new: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_awp_fixup: re-pack + re-unpack the layers whose width rose."""
+    _lib.check(_lib.load().adt_awp_fixup(masters.array, replicas.array, masters.nseg, packed.data_ptr(),
+                                         widths_prev.data_ptr(), widths_new.data_ptr(), stream_handle(stream)))

@@ -46,10 +46,19 @@ class WeightSync:
     """Masters (CUDA float32 tensors, one per layer) -> packed bytes -> replicas."""
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None,
-                 replicas: Sequence[torch.Tensor] | None = None, graphed: bool = True):
+                 replicas: Sequence[torch.Tensor] | None = None, graphed: bool = True,
+                 awp_on_device: bool = False, trace_ring: int = 256):
         """graphed: step() replays its kernels from a CUDA graph captured once
         per packed layout (one graph launch instead of three ctypes launches
-        and the stream bookkeeping per step)."""
+        and the stream bookkeeping per step).
+
+        awp_on_device: the AWP decision runs on the GPU (adt_awp_observe) and a
+        whole step — pack, norm, decide, re-pack of escalated layers, unpack —
+        is one CUDA graph with no device->host read; step() returns at once
+        and the trace rows come back in batches through drain_trace() (at the
+        latest every `trace_ring` observations, automatically). Layers keep
+        fixed capacity offsets in the packed buffer (room for 4 bytes/weight);
+        each payload is still exactly the reference's n*r bytes."""
         engine.require_cuda()
         self.graphed = graphed
         self.masters = [m.detach().reshape(-1) for m in masters]
@@ -81,6 +90,71 @@ class WeightSync:
         self.layout = None
         self.packed = None
         self._plan(self.schedule.round_tos())
+        self.awp_on_device = bool(awp_on_device)
+        self._dawp = None
+        if self.awp_on_device:
+            self._init_device_awp(trace_ring)
+
+    # --------------------------------------------- device-resident AWP mode
+    def _init_device_awp(self, ring: int) -> None:
+        from .awp_device import DeviceAwp
+        if not self.adaptive:
+            raise ValueError("awp_on_device needs a PrecisionController schedule")
+        self._dawp = DeviceAwp(self.schedule, self.device, ring)
+        cap = PackedLayout.plan(self.counts, [4] * len(self.counts))
+        self.capacity_layout = cap
+        if self.packed.numel() < cap.nbytes:
+            self.packed = torch.empty(max(16, cap.nbytes), dtype=torch.uint8, device=self.device)
+        self._cap_pack = engine.SegmentTable(self.masters, cap)
+        self._cap_unpack = engine.SegmentTable(self.replicas, cap)
+        self._agraphs = {}
+        self._trace_log = []
+
+    def _device_step_kernels(self, observe: bool) -> None:
+        """pack(A) -> [finalize -> observe(-> B)] || unpack(A) -> fixup(A, B) -> A = B."""
+        d = self._dawp
+        main = torch.cuda.current_stream()
+        engine.pack_dyn(self._cap_pack, self.packed, d.widths, self._partials if observe else None, main)
+        if observe:
+            self._side.wait_stream(main)
+            engine.finalize(self._cap_pack, self._partials, self.sumsq, self._side)
+            engine.awp_observe(self.sumsq, d.struct, d.config, self._side)
+        engine.unpack_dyn(self._cap_unpack, self.packed, d.widths, main)
+        if observe:
+            main.wait_stream(self._side)
+            engine.awp_fixup(self._cap_pack, self._cap_unpack, self.packed, d.widths, d.widths_new, main)
+            d.widths.copy_(d.widths_new)
+
+    def _step_device(self, batch: int, observe: bool) -> SyncResult:
+        d = self._dawp
+        if observe and not d.label_set:
+            d.set_next_label(batch - 1)
+        if self.graphed:
+            g = self._agraphs.get(observe)
+            if g is None:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._device_step_kernels(observe)
+                self._agraphs[observe] = g
+            g.replay()
+        else:
+            self._device_step_kernels(observe)
+        if observe:
+            d.pending += 1
+            if d.pending >= d.ring_steps:
+                self._trace_log += d.drain()
+        return SyncResult(round_tos=None)
+
+    def drain_trace(self) -> list[tuple]:
+        """awp_on_device: every trace row (TRACE_HEADER) observed since the
+        last call, in order; synchronises and refreshes the host controller
+        (schedule.state(), round_tos) from the device."""
+        if not self.awp_on_device:
+            raise RuntimeError("drain_trace() is for awp_on_device=True (step() returns the rows otherwise)")
+        rows = self._trace_log + self._dawp.drain()
+        self._trace_log = []
+        return rows
 
     def _plan(self, round_tos):
         self._graphs = None
@@ -97,6 +171,8 @@ class WeightSync:
 
     @property
     def round_tos(self) -> list[int]:
+        if getattr(self, "_dawp", None) is not None:
+            return self._dawp.round_tos()            # device read
         return list(self.layout.round_tos)
 
     def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
@@ -215,6 +291,8 @@ class WeightSync:
         """One batch of weight distribution (see module doc for the ordering)."""
         if observe is None:
             observe = self.adaptive and batch > 0
+        if self.awp_on_device:
+            return self._step_device(batch, observe)
         used = self.round_tos
         if self.graphed:
             self.launch_graphed(fused_norm=observe)
@@ -244,6 +322,8 @@ class WeightSync:
         if a width escalated, W_{b+1} is re-packed (without updating again).
         The replicas then hold batch b+1's weights.
         """
+        if self.awp_on_device:
+            raise NotImplementedError("update() with awp_on_device: use step() around your own optimizer step")
         if len(grads) != len(self.masters):
             raise ValueError("one gradient tensor per layer")
         self._ensure_velocities()
@@ -265,6 +345,8 @@ class WeightSync:
         steps W and v, packs W' and fuses its norm; then the replicas are
         unpacked and AWP observes, exactly as update()."""
         from .grads import GradBucket
+        if self.awp_on_device:
+            raise NotImplementedError("gather_and_update() with awp_on_device: use step() around your own update")
         if not 1 <= len(contributions) <= 16:
             raise ValueError("gather_and_update takes 1..16 gradient contributions")
         buckets = []
@@ -338,6 +420,15 @@ class WeightSync:
     def observe_final(self, batch: int) -> list[tuple]:
         """Norm-only pass over the masters (the observation after the last
         update, training.py:246-254); returns its trace rows labelled `batch`."""
+        if self.awp_on_device:
+            d = self._dawp
+            rows = self.drain_trace()
+            engine.sumsq(self._cap_pack, self.sumsq)
+            d.set_next_label(batch)
+            engine.awp_observe(self.sumsq, d.struct, d.config)
+            self._trace_log = rows          # kept for the next drain_trace(); return only this observation
+            last = d.drain()
+            return last
         return self.schedule.observe_all(self._norm_pass(), batch=batch)
 
     def norms(self) -> list[float]:

@@ -28,7 +28,8 @@ def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
         ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
          "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
-         "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_device_sm_count"])
+         "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn",
+         "adt_awp_observe", "adt_awp_fixup", "adt_device_sm_count"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -113,3 +114,13 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_peer_barrier(lib.pointer_array([16] * 17), 17, 0, 48, 10, None) == lib.ADT_ERR_ARG
     assert h.adt_peer_barrier(lib.pointer_array([16, 34]), 2, 0, 48, 10, None) == lib.ADT_ERR_ALIGN
     assert h.adt_peer_barrier(lib.pointer_array([16, 32]), 2, 0, 48, 0, None) == lib.ADT_ERR_ARG
+    # device AWP: capacity layout required (round_to 4), widths pointer required, struct sizes
+    assert ctypes.sizeof(lib.AwpGroup) == 32 and ctypes.sizeof(lib.AwpRow) == 40
+    assert h.adt_pack_dyn(lib.segment_array([(16, 10, 0, 2)]), 1, 16, None, 32, None) == lib.ADT_ERR_ARG
+    assert h.adt_pack_dyn(lib.segment_array([(16, 10, 0, 4)]), 1, 16, None, None, None) == lib.ADT_ERR_ARG
+    assert h.adt_unpack_dyn(lib.segment_array([(16, 10, 0, 3)]), 1, 16, 32, None) == lib.ADT_ERR_ARG
+    dev = lib.AwpDevice()
+    cfg = lib.AwpConfig(-2e-3, 50, 8, 32, 0)
+    assert h.adt_awp_observe(16, ctypes.byref(dev), ctypes.byref(cfg), None) == lib.ADT_ERR_ARG   # empty device struct
+    m, r = lib.segment_array([(16, 10, 0, 4)]), lib.segment_array([(48, 10, 16, 4)])
+    assert h.adt_awp_fixup(m, r, 1, 16, 64, 80, None) == lib.ADT_ERR_ARG                        # offsets differ

@@ -408,3 +408,77 @@ def test_l2_norm_many_matches_per_layer_and_golden(adt, golden_norms):
         assert g == pytest.approx(want, rel=NORM_RTOL, abs=0.0) if want else g == 0.0
     devs = [torch.from_numpy(np.asarray(x, np.float32)).cuda() for x in xs]
     assert adt.l2_norm_many(devs) == got
+
+
+@pytest.mark.parametrize("graphed", [True, False])
+def test_lenet_awp_walk_device_controller(adt, golden_lenet, graphed):
+    """The same 200-batch LeNet walk with the AWP decision on the device
+    (WeightSync(awp_on_device=True): one graph per step, no host read per
+    step): identical widths, payloads, replicas and trace rows, read back in
+    batches (a 16-step trace ring forces several automatic drains)."""
+    steps = int(golden_lenet["steps"])
+    walk = list(O.lenet_walk(steps, seed=7))
+    L = len(walk[0][1])
+    cfg = adt.PrecisionConfig(threshold=-2e-3, interval=int(golden_lenet["interval"]), step_bits=8, initial_bits=8)
+    masters = [torch.from_numpy(w.copy()).cuda() for w in walk[0][1]]
+    sync = adt.WeightSync(masters, adt.PrecisionController(L, cfg), awp_on_device=True, trace_ring=16,
+                          graphed=graphed)
+    cap = sync.capacity_layout
+    for t in range(steps):
+        for m, w in zip(masters, walk[t][1]):
+            m.copy_(torch.from_numpy(w))
+        sync.step(batch=t)
+        if t % 7 == 0 or t == steps - 1:          # inspect some steps (each inspection synchronises)
+            rs = sync.round_tos
+            assert rs == list(golden_lenet["widths"][t]), t
+            host_packed = sync.packed.cpu().numpy()
+            for i in range(L):
+                lo = cap.offsets[i]
+                pay = host_packed[lo:lo + cap.counts[i] * rs[i]].tobytes()
+                assert hashlib.sha256(pay).digest() == golden_lenet["payload_sha"][t, i].tobytes(), (t, i)
+                rep = sync.replicas[i].cpu().numpy()
+                assert hashlib.sha256(rep.tobytes()).digest() == golden_lenet["unpacked_sha"][t, i].tobytes(), (t, i)
+    trace = sync.drain_trace()
+    for m, w in zip(masters, walk[steps][1]):
+        m.copy_(torch.from_numpy(w))
+    trace += sync.observe_final(batch=steps - 1)
+    assert len(trace) == steps * L
+    for k, (b, layer, norm, delta, counter, bits) in enumerate(trace):
+        t, i = divmod(k, L)
+        assert (b, layer) == (t, i)
+        assert bits == golden_lenet["bits"][t, i] and counter == golden_lenet["counter"][t, i], (t, i)
+        assert abs(norm - golden_lenet["norms"][t, i]) <= NORM_RTOL * golden_lenet["norms"][t, i]
+        gd = golden_lenet["delta"][t, i]
+        assert (delta is None and math.isnan(gd)) or abs(delta - gd) <= 1e-6 * max(abs(gd), 1e-3)
+    # the host controller mirrors the device state after the drain
+    assert sync.schedule.round_tos() == sync.round_tos
+
+
+def test_device_controller_groups_match_host_controller(adt):
+    """Grouped layers (shared state, observed in layer order) and consecutive
+    mode: device decisions and trace rows equal the host controller's bit for bit."""
+    rng = np.random.default_rng(12)
+    counts = [4096 + 3, 700, 9000, 50, 4096 * 2]
+    groups = [0, 0, 1, 2, 1]
+    kw = dict(threshold=-1e-3, interval=2, step_bits=6, initial_bits=8, max_bits=24, consecutive=True)
+    hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+    ma = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+    mb = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+    host_sync = adt.WeightSync(ma, adt.PrecisionController(len(counts), adt.PrecisionConfig(**kw), groups))
+    dev_sync = adt.WeightSync(mb, adt.PrecisionController(len(counts), adt.PrecisionConfig(**kw), groups),
+                              awp_on_device=True)
+    want = []
+    for t in range(40):
+        f = (1.0 + rng.uniform(-0.004, 0.002, len(counts))).astype(np.float32)
+        for i, (a, b) in enumerate(zip(ma, mb)):
+            a.mul_(float(f[i]))
+            b.mul_(float(f[i]))
+        want += host_sync.step(batch=t).trace
+        dev_sync.step(batch=t)
+        if t % 10 == 9:
+            assert dev_sync.round_tos == host_sync.round_tos, t
+            for x, y in zip(host_sync.replicas, dev_sync.replicas):
+                assert torch.equal(x, y), t
+    got = dev_sync.drain_trace()
+    assert got == want
+    assert max(host_sync.round_tos) > 1
