@@ -214,9 +214,10 @@ int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *con
  *   adt_pack_dyn(A) -> [adt_norm_finalize -> adt_awp_observe(-> B)] || adt_unpack_dyn(A)
  *   -> adt_awp_fixup(A, B) -> copy B to A
  * adt_awp_observe advances each group's state, writes one trace row per layer
- * (TRACE_HEADER, precision.py:18) into a ring of ring_steps steps and stores
- * the new widths in widths_out (B); the fixup re-packs (from the masters) and
- * re-unpacks only the layers whose width rose.
+ * (TRACE_HEADER, precision.py:18) into a ring of ring_steps steps, stores
+ * the new widths in widths_out (B) and lists the layers whose width rose; the
+ * fixup re-packs (from the masters) and re-unpacks only those (with none, its
+ * CTAs exit after one load).
  */
 typedef struct adt_awp_config {
     double threshold;        /* T (precision.py:46-54) */
@@ -250,8 +251,9 @@ typedef struct adt_awp_device {  /* all pointers: device memory */
     adt_awp_group *groups;       /* [ngroups] */
     const int32_t *members;      /* [nlayers] layer ids grouped by group, in layer order within a group */
     const int32_t *member_start; /* [ngroups + 1] */
-    uint8_t *widths_out;         /* [nlayers] bytes per weight after this observation (1..4) */
-    void *reserved_ptr;          /* NULL */
+    const uint8_t *widths_in;    /* [nlayers] bytes per weight the step's pack used (A) */
+    uint8_t *widths_out;         /* [nlayers] bytes per weight after this observation (B, 1..4) */
+    int32_t *escalated;          /* [nlayers + 1]: count, then the layers with B != A (any order) */
     adt_awp_row *ring;           /* [ring_steps * nlayers] trace rows, step slot = counter[0] % ring_steps */
     int64_t *counter;            /* [2]: observations so far, batch label of the next observation */
     int32_t nlayers;
@@ -267,10 +269,11 @@ int adt_pack_dyn(const adt_segment *segs, int nseg, uint8_t *packed, double *par
 int adt_unpack_dyn(const adt_segment *segs, int nseg, const uint8_t *packed, const uint8_t *widths, void *stream);
 /* One AWP observation of every layer from the finalized sums of squares. */
 int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg, void *stream);
-/* Re-pack + re-unpack of the layers with widths_new[l] != widths_prev[l]; masters[l] and
- * replicas[l] share count / offset (capacity layout, round_to 4). */
+/* Re-pack + re-unpack, at widths_new, of the layers listed in `escalated` (as written by
+ * adt_awp_observe); masters[l] and replicas[l] share count / offset (capacity layout,
+ * round_to 4). */
 int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
-                  const uint8_t *widths_prev, const uint8_t *widths_new, void *stream);
+                  const int32_t *escalated, const uint8_t *widths_new, void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

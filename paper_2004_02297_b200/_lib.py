@@ -99,7 +99,8 @@ class AwpDevice(ctypes.Structure):
     """adt_awp_device: device pointers of the on-GPU controller."""
 
     _fields_ = [("groups", ctypes.c_void_p), ("members", ctypes.c_void_p), ("member_start", ctypes.c_void_p),
-                ("widths_out", ctypes.c_void_p), ("reserved_ptr", ctypes.c_void_p), ("ring", ctypes.c_void_p),
+                ("widths_in", ctypes.c_void_p), ("widths_out", ctypes.c_void_p), ("escalated", ctypes.c_void_p),
+                ("ring", ctypes.c_void_p),
                 ("counter", ctypes.c_void_p), ("nlayers", ctypes.c_int32), ("ngroups", ctypes.c_int32),
                 ("ring_steps", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 

@@ -47,14 +47,15 @@ class DeviceAwp:
         self.groups = torch.zeros(self.ngroups * _GROUP_DT.itemsize, dtype=torch.uint8, device=device)
         self.widths = torch.empty(L, dtype=torch.uint8, device=device)       # A: in force for the next pack
         self.widths_new = torch.empty(L, dtype=torch.uint8, device=device)   # B: written by the observation
+        self.escalated = torch.zeros(L + 1, dtype=torch.int32, device=device)   # count, then layer ids
         self.ring = torch.zeros(self.ring_steps * L * _ROW_DT.itemsize, dtype=torch.uint8, device=device)
         self.counter = torch.zeros(2, dtype=torch.int64, device=device)
         cfg = controller.config
         self.config = _lib.AwpConfig(float(cfg.threshold), int(cfg.interval), int(cfg.step_bits), int(cfg.max_bits),
                                      int(bool(cfg.consecutive)))
         self.struct = _lib.AwpDevice(self.groups.data_ptr(), self.members.data_ptr(), self.member_start.data_ptr(),
-                                     self.widths_new.data_ptr(), None, self.ring.data_ptr(), self.counter.data_ptr(),
-                                     L, self.ngroups, self.ring_steps, 0)
+                                     self.widths.data_ptr(), self.widths_new.data_ptr(), self.escalated.data_ptr(),
+                                     self.ring.data_ptr(), self.counter.data_ptr(), L, self.ngroups, self.ring_steps, 0)
         self.drained = 0          # observations already read back
         self.pending = 0          # observations issued since the last drain
         self.label_set = False

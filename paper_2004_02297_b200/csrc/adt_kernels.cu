@@ -736,9 +736,11 @@ __global__ void __launch_bounds__(kAwpThreads)
 adt_awp_observe_kernel(const double *__restrict__ seg_sumsq, const __grid_constant__ adt_awp_device D,
                        const __grid_constant__ adt_awp_config C) {
     __shared__ int64_t slot_batch[2];
+    __shared__ int32_t n_esc;
     if (threadIdx.x == 0) {
         slot_batch[0] = D.counter[0] % D.ring_steps;
         slot_batch[1] = D.counter[1];
+        n_esc = 0;
     }
     __syncthreads();
     adt_awp_row *rows = D.ring + slot_batch[0] * D.nlayers;
@@ -779,10 +781,15 @@ adt_awp_observe_kernel(const double *__restrict__ seg_sumsq, const __grid_consta
         }
         D.groups[g] = st;
         const uint8_t w = static_cast<uint8_t>((st.bits + 7) / 8);   // bits_to_round_to
-        for (int32_t k = lo; k < hi; ++k) D.widths_out[D.members[k]] = w;
+        for (int32_t k = lo; k < hi; ++k) {
+            const int32_t l = D.members[k];
+            D.widths_out[l] = w;
+            if (w != D.widths_in[l]) D.escalated[1 + atomicAdd(&n_esc, 1)] = l;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        D.escalated[0] = n_esc;
         D.counter[0] += 1;
         D.counter[1] += 1;
     }
@@ -798,8 +805,9 @@ template <int MAXSEG>
 struct FixupTable {
     Table<MAXSEG> T;                 // replicas (weights[]), offsets, tile map; packed_out = the packed buffer
     uintptr_t masters[MAXSEG];
-    const uint8_t *widths_prev;
-    const uint8_t *widths_new;
+    const int32_t *escalated;        // count, then global layer ids
+    const uint8_t *widths_new;       // chunk-relative
+    int32_t base;                    // first global layer id of this chunk
 };
 
 template <int MAXSEG>
@@ -809,11 +817,14 @@ adt_awp_fixup_kernel(const __grid_constant__ FixupTable<MAXSEG> F) {
     const Table<MAXSEG> &T = F.T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t *ws = stage[warp];
+    const int32_t n_esc = F.escalated[0];                // usually 0: one load and out
     uint32_t vt = blockIdx.x;                            // virtual tile index over escalated layers
-    for (int s = 0; s < T.nseg; ++s) {
+    for (int32_t e = 0; e < n_esc; ++e) {
+        const int s = F.escalated[1 + e] - F.base;
+        if (s < 0 || s >= T.nseg) continue;              // another chunk's layer
         const int r = F.widths_new[s];
         const uint32_t nt = T.tile_begin[s + 1] - T.tile_begin[s];
-        if (r == F.widths_prev[s] || nt == 0) continue;
+        if (nt == 0) continue;
         for (; vt < nt; vt += gridDim.x) {
             const uint32_t local = vt;
             const uint64_t e0 = static_cast<uint64_t>(local) * kTile;
@@ -1390,7 +1401,8 @@ int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const ad
     if (seg_sumsq == nullptr || dev == nullptr || cfg == nullptr) return ADT_ERR_ARG;
     const adt_awp_device &D = *dev;
     if (D.nlayers < 1 || D.ngroups < 1 || D.ngroups > D.nlayers || D.ring_steps < 1 || D.reserved != 0) return ADT_ERR_ARG;
-    if (!D.groups || !D.members || !D.member_start || !D.widths_out || !D.ring || !D.counter || D.reserved_ptr)
+    if (!D.groups || !D.members || !D.member_start || !D.widths_in || !D.widths_out || !D.escalated || !D.ring ||
+        !D.counter)
         return ADT_ERR_ARG;
     if (cfg->interval < 1 || cfg->step_bits < 1 || cfg->max_bits < 1 || cfg->max_bits > 32) return ADT_ERR_ARG;
     adt_awp_observe_kernel<<<1, kAwpThreads, 0, static_cast<cudaStream_t>(stream)>>>(seg_sumsq, D, *cfg);
@@ -1401,7 +1413,7 @@ extern "C++" {
 namespace {
 template <int MAXSEG>
 int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
-                       const uint8_t *widths_prev, const uint8_t *widths_new, cudaStream_t stream) {
+                       const int32_t *escalated, const uint8_t *widths_new, int base, cudaStream_t stream) {
     FixupTable<MAXSEG> F;
     Table<MAXSEG> &T = F.T;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = nullptr;
@@ -1423,8 +1435,9 @@ int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, 
     }
     T.tile_begin[nseg] = acc;
     fill_hints(T, nseg, acc);
-    F.widths_prev = widths_prev;
+    F.escalated = escalated;
     F.widths_new = widths_new;
+    F.base = base;
     int sms = 0;
     if (sm_count_cached(&sms) != ADT_OK) return ADT_ERR_NO_DEVICE;
     const uint32_t grid = max(1u, min(acc, static_cast<uint32_t>(4 * sms)));
@@ -1435,11 +1448,11 @@ int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, 
 }  // extern "C++"
 
 int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
-                  const uint8_t *widths_prev, const uint8_t *widths_new, void *stream) {
+                  const int32_t *escalated, const uint8_t *widths_new, void *stream) {
     int v = validate(replicas, nseg, packed, true);
     if (v != ADT_OK) return v;
     if ((v = validate(masters, nseg, packed, true)) != ADT_OK) return v;
-    if (nseg > 0 && (widths_prev == nullptr || widths_new == nullptr)) return ADT_ERR_ARG;
+    if (nseg > 0 && (escalated == nullptr || widths_new == nullptr)) return ADT_ERR_ARG;
     for (int i = 0; i < nseg; ++i)
         if (replicas[i].round_to != 4 || masters[i].count != replicas[i].count ||
             masters[i].offset != replicas[i].offset)
@@ -1448,10 +1461,10 @@ int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int n
     for (int base = 0; base < nseg; base += kLargeSeg) {
         const int cnt = min(kLargeSeg, nseg - base);
         const int st = cnt <= kSmallSeg
-            ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, widths_prev + base,
-                                            widths_new + base, s)
-            : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, widths_prev + base,
-                                            widths_new + base, s);
+            ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, escalated,
+                                            widths_new + base, base, s)
+            : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, escalated,
+                                            widths_new + base, base, s);
         if (st != ADT_OK) return st;
     }
     return ADT_OK;

@@ -321,8 +321,8 @@ def awp_observe(sumsq: torch.Tensor, device_struct, config_struct, stream: torch
                                            stream_handle(stream)))
 
 
-def awp_fixup(masters: SegmentTable, replicas: SegmentTable, packed: torch.Tensor, widths_prev: torch.Tensor,
+def awp_fixup(masters: SegmentTable, replicas: SegmentTable, packed: torch.Tensor, escalated: torch.Tensor,
               widths_new: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
-    """adt_awp_fixup: re-pack + re-unpack the layers whose width rose."""
+    """adt_awp_fixup: re-pack + re-unpack the layers adt_awp_observe listed as escalated."""
     _lib.check(_lib.load().adt_awp_fixup(masters.array, replicas.array, masters.nseg, packed.data_ptr(),
-                                         widths_prev.data_ptr(), widths_new.data_ptr(), stream_handle(stream)))
+                                         escalated.data_ptr(), widths_new.data_ptr(), stream_handle(stream)))

@@ -111,7 +111,7 @@ class WeightSync:
         self._trace_log = []
 
     def _device_step_kernels(self, observe: bool) -> None:
-        """pack(A) -> [finalize -> observe(-> B)] || unpack(A) -> fixup(A, B) -> A = B."""
+        """pack(A) -> [finalize -> observe(-> B, escalated list)] || unpack(A) -> fixup -> A = B."""
         d = self._dawp
         main = torch.cuda.current_stream()
         engine.pack_dyn(self._cap_pack, self.packed, d.widths, self._partials if observe else None, main)
@@ -122,7 +122,7 @@ class WeightSync:
         engine.unpack_dyn(self._cap_unpack, self.packed, d.widths, main)
         if observe:
             main.wait_stream(self._side)
-            engine.awp_fixup(self._cap_pack, self._cap_unpack, self.packed, d.widths, d.widths_new, main)
+            engine.awp_fixup(self._cap_pack, self._cap_unpack, self.packed, d.escalated, d.widths_new, main)
             d.widths.copy_(d.widths_new)
 
     def _step_device(self, batch: int, observe: bool) -> SyncResult:

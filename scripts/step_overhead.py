@@ -49,8 +49,20 @@ def main(names):
         e.record()
         e.synchronize()
         dev_us = a.elapsed_time(e) / steps * 1e3
+        # the same step with the AWP decision on the device: no host read per step
+        dsync = adt.WeightSync(masters, adt.PrecisionController(L, cfg), awp_on_device=True)
+        for b in range(20):
+            dsync.step(batch=b)
+        dsync.drain_trace()
+        t0 = time.perf_counter()
+        for b in range(20, 20 + steps):
+            dsync.step(batch=b)
+        torch.cuda.synchronize()
+        dwall = (time.perf_counter() - t0) / steps * 1e6
+        rows = dsync.drain_trace()
+        assert len(rows) == steps * L
         print(f"{name:10s} layers {L:4d}  step() wall {wall:8.1f} us   controller {ctl:7.1f} us   "
-              f"device (graphed) {dev_us:7.1f} us")
+              f"device (graphed) {dev_us:7.1f} us   awp_on_device step() {dwall:7.1f} us")
 
 
 if __name__ == "__main__":
