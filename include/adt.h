@@ -267,6 +267,13 @@ int adt_pack_dyn(const adt_segment *segs, int nseg, uint8_t *packed, double *par
                  void *stream);
 /* adt_unpack with the widths read from device memory. */
 int adt_unpack_dyn(const adt_segment *segs, int nseg, const uint8_t *packed, const uint8_t *widths, void *stream);
+/* adt_sgd_pack / adt_reduce_sgd_pack (norm partials only) with the widths read from device memory. */
+int adt_sgd_pack_dyn(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
+                     uint8_t *packed, double *partials, const uint8_t *widths, void *stream);
+int adt_reduce_sgd_pack_dyn(const adt_grad_segment *segs, int nseg, const float *const *grads,
+                            const int64_t *sample_counts, int ncontrib, float lr, float momentum,
+                            float weight_decay, uint8_t *packed, double *partials, const uint8_t *widths,
+                            void *stream);
 /* One AWP observation of every layer from the finalized sums of squares. */
 int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg, void *stream);
 /* Re-pack + re-unpack, at widths_new, of the layers listed in `escalated` (as written by

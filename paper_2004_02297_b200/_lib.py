@@ -29,7 +29,7 @@ PARTIALS_PER_TILE = 8
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
            "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
-           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn",
+           "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn", "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn",
            "adt_awp_observe", "adt_awp_fixup", "adt_device_sm_count")
 
 
@@ -171,6 +171,13 @@ def load() -> ctypes.CDLL:
         lib.adt_pack_dyn.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack_dyn.restype = ctypes.c_int
         lib.adt_unpack_dyn.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
+        lib.adt_sgd_pack_dyn.restype = ctypes.c_int
+        lib.adt_sgd_pack_dyn.argtypes = [P(SgdSegment), ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                         vp, vp, vp, vp]
+        lib.adt_reduce_sgd_pack_dyn.restype = ctypes.c_int
+        lib.adt_reduce_sgd_pack_dyn.argtypes = [P(GradSegment), ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int64),
+                                                ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                                vp, vp, vp, vp]
         lib.adt_awp_observe.restype = ctypes.c_int
         lib.adt_awp_observe.argtypes = [vp, P(AwpDevice), P(AwpConfig), vp]
         lib.adt_awp_fixup.restype = ctypes.c_int

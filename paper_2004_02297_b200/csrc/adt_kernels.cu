@@ -1065,6 +1065,7 @@ struct SgdArgs {
     float scale[ADT_MAX_SOURCES];
     float total, lr, mu, wd;
     int nc;                                 // 0 = one pre-averaged gradient per segment
+    const uint8_t *widths;                  // device-resident widths (global layer index) or nullptr
 };
 
 template <int MAXSEG, int NC>
@@ -1102,9 +1103,10 @@ cudaError_t launch_sgd_nc(const SgdTable<MAXSEG> &T, int nc, uint32_t ntiles, cu
 // a byte offset into every gradient buffer otherwise).
 template <int MAXSEG>
 int launch_sgd_chunk(const adt_sgd_segment *segs, const adt_grad_segment *gsegs, int nseg, const SgdArgs &A,
-                     uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, cudaStream_t stream) {
+                     uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, cudaStream_t stream,
+                     int base) {
     SgdTable<MAXSEG> T;
-    T.dyn_r = nullptr;
+    T.dyn_r = A.widths != nullptr ? A.widths + base : nullptr;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) {
         T.srcs[i] = A.srcs[i];
         T.scale[i] = A.scale[i];
@@ -1166,8 +1168,8 @@ int run_sgd(const adt_sgd_segment *segs, const adt_grad_segment *gsegs, int nseg
         const adt_sgd_segment *sb = segs ? segs + base : nullptr;
         const adt_grad_segment *gb = gsegs ? gsegs + base : nullptr;
         const int st = cnt <= kSmallSeg
-            ? launch_sgd_chunk<kSmallSeg>(sb, gb, cnt, A, pout, ss, pp, static_cast<uint32_t>(tiles), stream)
-            : launch_sgd_chunk<kLargeSeg>(sb, gb, cnt, A, pout, ss, pp, static_cast<uint32_t>(tiles), stream);
+            ? launch_sgd_chunk<kSmallSeg>(sb, gb, cnt, A, pout, ss, pp, static_cast<uint32_t>(tiles), stream, base)
+            : launch_sgd_chunk<kLargeSeg>(sb, gb, cnt, A, pout, ss, pp, static_cast<uint32_t>(tiles), stream, base);
         if (st != ADT_OK) return st;
         partial_base += tiles * kWarpsPerTile;
         base += cnt;
@@ -1308,8 +1310,11 @@ int adt_sumsq(const adt_segment *segs, int nseg, double *seg_sumsq, double *part
     return run(Pass::Norm, segs, nseg, nullptr, 0, nullptr, seg_sumsq, partials, true, stream);
 }
 
-int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
-                 uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+}  // extern "C"
+
+namespace {
+int sgd_pack_impl(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
+                  uint8_t *packed, double *seg_sumsq, double *partials, const uint8_t *widths, void *stream) {
     if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
     if (nseg > 0 && seg_sumsq != nullptr && partials == nullptr) return ADT_ERR_ARG;
     bool any = false;
@@ -1333,12 +1338,13 @@ int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum
     A.mu = momentum;
     A.wd = weight_decay;
     A.nc = 0;
+    A.widths = widths;
     return run_sgd(segs, nullptr, nseg, A, packed, seg_sumsq, partials, static_cast<cudaStream_t>(stream));
 }
 
-int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *const *grads,
-                        const int64_t *sample_counts, int ncontrib, float lr, float momentum, float weight_decay,
-                        uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+int reduce_sgd_pack_impl(const adt_grad_segment *segs, int nseg, const float *const *grads,
+                         const int64_t *sample_counts, int ncontrib, float lr, float momentum, float weight_decay,
+                         uint8_t *packed, double *seg_sumsq, double *partials, const uint8_t *widths, void *stream) {
     if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
     if (ncontrib < 1 || ncontrib > ADT_MAX_SOURCES || grads == nullptr || sample_counts == nullptr)
         return ADT_ERR_ARG;
@@ -1357,6 +1363,7 @@ int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *con
     A.mu = momentum;
     A.wd = weight_decay;
     A.nc = ncontrib;
+    A.widths = widths;
     bool any = false;
     for (int i = 0; i < nseg; ++i) {
         const adt_grad_segment &g = segs[i];
@@ -1374,6 +1381,40 @@ int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *con
     if (any && (packed == nullptr)) return ADT_ERR_ARG;
     if (any && reinterpret_cast<uintptr_t>(packed) % 16) return ADT_ERR_ALIGN;
     return run_sgd(nullptr, segs, nseg, A, packed, seg_sumsq, partials, static_cast<cudaStream_t>(stream));
+}
+}  // namespace
+
+extern "C" {
+
+int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
+                 uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+    return sgd_pack_impl(segs, nseg, lr, momentum, weight_decay, packed, seg_sumsq, partials, nullptr, stream);
+}
+
+int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *const *grads,
+                        const int64_t *sample_counts, int ncontrib, float lr, float momentum, float weight_decay,
+                        uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+    return reduce_sgd_pack_impl(segs, nseg, grads, sample_counts, ncontrib, lr, momentum, weight_decay, packed,
+                                seg_sumsq, partials, nullptr, stream);
+}
+
+int adt_sgd_pack_dyn(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
+                     uint8_t *packed, double *partials, const uint8_t *widths, void *stream) {
+    if (nseg > 0 && (segs == nullptr || widths == nullptr)) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (segs[i].round_to != 4) return ADT_ERR_ARG;   // capacity layout
+    return sgd_pack_impl(segs, nseg, lr, momentum, weight_decay, packed, nullptr, partials, widths, stream);
+}
+
+int adt_reduce_sgd_pack_dyn(const adt_grad_segment *segs, int nseg, const float *const *grads,
+                            const int64_t *sample_counts, int ncontrib, float lr, float momentum,
+                            float weight_decay, uint8_t *packed, double *partials, const uint8_t *widths,
+                            void *stream) {
+    if (nseg > 0 && (segs == nullptr || widths == nullptr)) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (segs[i].round_to != 4) return ADT_ERR_ARG;
+    return reduce_sgd_pack_impl(segs, nseg, grads, sample_counts, ncontrib, lr, momentum, weight_decay, packed,
+                                nullptr, partials, widths, stream);
 }
 
 int adt_pack_dyn(const adt_segment *segs, int nseg, uint8_t *packed, double *partials, const uint8_t *widths,

@@ -326,3 +326,25 @@ def awp_fixup(masters: SegmentTable, replicas: SegmentTable, packed: torch.Tenso
     """adt_awp_fixup: re-pack + re-unpack the layers adt_awp_observe listed as escalated."""
     _lib.check(_lib.load().adt_awp_fixup(masters.array, replicas.array, masters.nseg, packed.data_ptr(),
                                          escalated.data_ptr(), widths_new.data_ptr(), stream_handle(stream)))
+
+
+def sgd_pack_dyn(table: SgdTable, lr: float, momentum: float, weight_decay: float, packed: torch.Tensor,
+                 widths: torch.Tensor, partials: torch.Tensor | None = None,
+                 stream: torch.cuda.Stream | None = None) -> None:
+    """adt_sgd_pack_dyn: the fused update + pack at device-resident widths (capacity layout)."""
+    _lib.check(_lib.load().adt_sgd_pack_dyn(table.array, table.nseg, float(lr), float(momentum), float(weight_decay),
+                                            packed.data_ptr(), partials.data_ptr() if partials is not None else None,
+                                            widths.data_ptr(), stream_handle(stream)))
+
+
+def reduce_sgd_pack_dyn(table: ReduceSgdTable, grads: Sequence[int], sample_counts: Sequence[int], lr: float,
+                        momentum: float, weight_decay: float, packed: torch.Tensor, widths: torch.Tensor,
+                        partials: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_reduce_sgd_pack_dyn: gradient combine + update + pack at device-resident widths."""
+    if len(grads) != len(sample_counts) or not 1 <= len(grads) <= _lib.MAX_SOURCES:
+        raise ValueError(f"need 1..{_lib.MAX_SOURCES} contributions with one sample count each")
+    counts = (ctypes.c_int64 * len(sample_counts))(*[int(c) for c in sample_counts])
+    _lib.check(_lib.load().adt_reduce_sgd_pack_dyn(
+        table.array, table.nseg, _lib.pointer_array(grads), counts, len(grads), float(lr), float(momentum),
+        float(weight_decay), packed.data_ptr(), partials.data_ptr() if partials is not None else None,
+        widths.data_ptr(), stream_handle(stream)))

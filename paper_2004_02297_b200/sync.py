@@ -146,6 +146,30 @@ class WeightSync:
                 self._trace_log += d.drain()
         return SyncResult(round_tos=None)
 
+    def _update_device(self, launch, batch: int) -> SyncResult:
+        """Device-AWP form of _update_step: the fused update + pack at the
+        device widths, then [finalize -> observe] || unpack -> fixup, with
+        no host read; the trace rows (labelled `batch`) and the finite-weights
+        check (NonFiniteParameters, from the rows' norms) come at the next
+        drain_trace()."""
+        d = self._dawp
+        main = torch.cuda.current_stream()
+        d.counter[1].fill_(int(batch))
+        d.label_set = True
+        launch(main)
+        self._side.wait_stream(main)
+        engine.finalize(self._cap_pack, self._partials, self.sumsq, self._side)
+        engine.awp_observe(self.sumsq, d.struct, d.config, self._side)
+        engine.unpack_dyn(self._cap_unpack, self.packed, d.widths, main)
+        main.wait_stream(self._side)
+        engine.awp_fixup(self._cap_pack, self._cap_unpack, self.packed, d.escalated, d.widths_new, main)
+        d.widths.copy_(d.widths_new)
+        self._check_finite = True
+        d.pending += 1
+        if d.pending >= d.ring_steps:
+            self._trace_log += d.drain()
+        return SyncResult(round_tos=None)
+
     def drain_trace(self) -> list[tuple]:
         """awp_on_device: every trace row (TRACE_HEADER) observed since the
         last call, in order; synchronises and refreshes the host controller
@@ -154,6 +178,10 @@ class WeightSync:
             raise RuntimeError("drain_trace() is for awp_on_device=True (step() returns the rows otherwise)")
         rows = self._trace_log + self._dawp.drain()
         self._trace_log = []
+        if getattr(self, "_check_finite", False):
+            bad = next((r for r in rows if not math.isfinite(r[2])), None)
+            if bad is not None:
+                raise NonFiniteParameters(f"layer {bad[1]} parameters left the finite range (batch {bad[0]})")
         return rows
 
     def _plan(self, round_tos):
@@ -322,12 +350,15 @@ class WeightSync:
         if a width escalated, W_{b+1} is re-packed (without updating again).
         The replicas then hold batch b+1's weights.
         """
-        if self.awp_on_device:
-            raise NotImplementedError("update() with awp_on_device: use step() around your own optimizer step")
         if len(grads) != len(self.masters):
             raise ValueError("one gradient tensor per layer")
         self._ensure_velocities()
         g = [t.detach().reshape(-1) for t in grads]
+        if self.awp_on_device:
+            table = engine.SgdTable(self.masters, self.velocities, g, self.capacity_layout)
+            d = self._dawp
+            return self._update_device(lambda main: engine.sgd_pack_dyn(
+                table, lr, momentum, weight_decay, self.packed, d.widths, self._partials, main), batch)
         table = engine.SgdTable(self.masters, self.velocities, g, self.layout)
 
         def launch(main):
@@ -345,8 +376,6 @@ class WeightSync:
         steps W and v, packs W' and fuses its norm; then the replicas are
         unpacked and AWP observes, exactly as update()."""
         from .grads import GradBucket
-        if self.awp_on_device:
-            raise NotImplementedError("gather_and_update() with awp_on_device: use step() around your own update")
         if not 1 <= len(contributions) <= 16:
             raise ValueError("gather_and_update takes 1..16 gradient contributions")
         buckets = []
@@ -365,13 +394,17 @@ class WeightSync:
                 raise ValueError("gradient bucket layer sizes differ from the masters")
             buckets.append(b)
         self._ensure_velocities()
-        key = self.layout
+        key = self.capacity_layout if self.awp_on_device else self.layout
         if self._reduce_table is None or self._reduce_table[0] != key:
             offs = [buckets[0].byte_offset(l) for l in range(len(self.masters))]
-            self._reduce_table = (key, engine.ReduceSgdTable(self.masters, self.velocities, offs, self.layout))
+            self._reduce_table = (key, engine.ReduceSgdTable(self.masters, self.velocities, offs, key))
         table = self._reduce_table[1]
         ptrs = [b.flat.data_ptr() for b in buckets]
         counts = [b.sample_count for b in buckets]
+        if self.awp_on_device:
+            d = self._dawp
+            return self._update_device(lambda main: engine.reduce_sgd_pack_dyn(
+                table, ptrs, counts, lr, momentum, weight_decay, self.packed, d.widths, self._partials, main), batch)
 
         def launch(main):
             engine.reduce_sgd_pack(table, ptrs, counts, lr, momentum, weight_decay, self.packed, None, main,

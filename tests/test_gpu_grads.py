@@ -235,3 +235,42 @@ def test_sharded_update_p2p_processes_sharing_one_gpu(world):
         assert ok, (rank, notes[:5])
     assert all(r[3] == res[0][3] for r in res) and len(res[0][3]) > 0   # identical norm bits on every rank
     assert all(r[4] == res[0][4] for r in res) and max(res[0][4]) > 1
+
+
+def test_device_awp_gather_and_update_matches_host(adt):
+    """gather_and_update with the AWP decision on the device (no host read per
+    step) vs the host-controller WeightSync: identical masters, replicas,
+    widths and trace rows; update() likewise."""
+    from paper_2004_02297_b200.grads import GradBucket
+    rng = np.random.default_rng(23)
+    counts = [500, 25000, 4096 * 3 + 7, 5000]
+    L = len(counts)
+    hp = (0.05, 0.9, 5e-4)
+    kw = dict(threshold=-2e-3, interval=3, step_bits=8, initial_bits=8)
+    w0 = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+    host = adt.WeightSync([torch.from_numpy(w.copy()).cuda() for w in w0],
+                          adt.PrecisionController(L, adt.PrecisionConfig(**kw)))
+    dev = adt.WeightSync([torch.from_numpy(w.copy()).cuda() for w in w0],
+                         adt.PrecisionController(L, adt.PrecisionConfig(**kw)), awp_on_device=True, trace_ring=8)
+    buckets = [GradBucket(counts, sample_count=c) for c in (64, 17, 40)]
+    want = []
+    for b in range(24):
+        for k, bk in enumerate(buckets):
+            bk.load([torch.from_numpy(np.float32(0.4 + 0.1 * k) * m.cpu().numpy()
+                                      + rng.standard_normal(n, dtype=np.float32) * np.float32(0.002)).cuda()
+                     for m, n in zip(host.masters, counts)])
+        want += host.gather_and_update(buckets, *hp, batch=b).trace
+        dev.gather_and_update(buckets, *hp, batch=b)
+        if b % 6 == 5:
+            assert dev.round_tos == host.round_tos, b
+            for x, y in zip(host.masters + host.replicas, dev.masters + dev.replicas):
+                assert torch.equal(x, y), b
+    got = dev.drain_trace()
+    assert got == want
+    assert max(host.round_tos) > 1
+    # update() (one pre-averaged gradient)
+    g = [torch.randn(n, device="cuda") * 0.01 for n in counts]
+    r1 = host.update(g, *hp, batch=24).trace
+    dev.update(g, *hp, batch=24)
+    assert dev.drain_trace() == r1
+    assert all(torch.equal(x, y) for x, y in zip(host.replicas, dev.replicas))
