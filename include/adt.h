@@ -282,6 +282,26 @@ int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const ad
 int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
                   const int32_t *escalated, const uint8_t *widths_new, void *stream);
 
+/* Multi-rank device AWP (ShardedWeightSync(transport="p2p", awp_on_device=True)): segments are
+ * layer pieces, seg_layer[i] the global layer of piece i (host array).
+ *   adt_unpack_multi_dyn: adt_unpack_multi with per-piece widths from device memory;
+ *   adt_awp_combine:      per-layer sums of squares from the gathered per-piece sums tails[k]
+ *                         (piece_layer[k], device, -1 = empty slot), added in k order
+ *                         (rank-major, as ShardPlan.combine_sumsq) — identical on every rank;
+ *   adt_awp_fixup_pieces: adt_awp_fixup for this rank's pieces (re-pack into its send buffer,
+ *                         write its replica pieces);
+ *   adt_awp_fixup_gather: re-unpack the escalated pieces of every rank from their (re-packed)
+ *                         send buffers, at widths_new (per piece). */
+int adt_unpack_multi_dyn(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
+                         const uint8_t *widths, void *stream);
+int adt_awp_combine(const double *tails, int npieces_total, const int32_t *piece_layer, int nlayers,
+                    double *seg_sumsq, void *stream);
+int adt_awp_fixup_pieces(const adt_segment *masters, const adt_segment *replicas, int nseg, const int32_t *seg_layer,
+                         uint8_t *packed, const int32_t *escalated, const uint8_t *widths_new, void *stream);
+int adt_awp_fixup_gather(const adt_segment *replicas, int nseg, const int32_t *seg_layer,
+                         const uint8_t *const *sources, int nsrc, const int32_t *escalated,
+                         const uint8_t *widths_new, void *stream);
+
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);
 

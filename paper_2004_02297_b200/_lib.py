@@ -30,7 +30,8 @@ PARTIALS_PER_TILE = 8
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
            "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
            "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn", "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn",
-           "adt_awp_observe", "adt_awp_fixup", "adt_device_sm_count")
+           "adt_awp_observe", "adt_awp_fixup", "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces",
+           "adt_awp_fixup_gather", "adt_device_sm_count")
 
 
 class Segment(ctypes.Structure):
@@ -182,6 +183,15 @@ def load() -> ctypes.CDLL:
         lib.adt_awp_observe.argtypes = [vp, P(AwpDevice), P(AwpConfig), vp]
         lib.adt_awp_fixup.restype = ctypes.c_int
         lib.adt_awp_fixup.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, vp, vp]
+        lib.adt_unpack_multi_dyn.restype = ctypes.c_int
+        lib.adt_unpack_multi_dyn.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp, vp]
+        lib.adt_awp_combine.restype = ctypes.c_int
+        lib.adt_awp_combine.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, vp, vp]
+        lib.adt_awp_fixup_pieces.restype = ctypes.c_int
+        lib.adt_awp_fixup_pieces.argtypes = [seg_p, seg_p, ctypes.c_int, P(ctypes.c_int32), vp, vp, vp, vp]
+        lib.adt_awp_fixup_gather.restype = ctypes.c_int
+        lib.adt_awp_fixup_gather.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_int32), P(ctypes.c_void_p), ctypes.c_int,
+                                             vp, vp, vp]
         lib.adt_sumsq.restype = ctypes.c_int
         lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_device_sm_count.restype = ctypes.c_int

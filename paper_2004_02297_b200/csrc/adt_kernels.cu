@@ -805,9 +805,10 @@ template <int MAXSEG>
 struct FixupTable {
     Table<MAXSEG> T;                 // replicas (weights[]), offsets, tile map; packed_out = the packed buffer
     uintptr_t masters[MAXSEG];
+    int32_t layer_of[MAXSEG];        // global layer id of each segment (a layer piece)
     const int32_t *escalated;        // count, then global layer ids
-    const uint8_t *widths_new;       // chunk-relative
-    int32_t base;                    // first global layer id of this chunk
+    const uint8_t *widths_new;       // per segment (chunk-relative)
+    int32_t gather;                  // 0: re-pack from masters + write replicas; 1: re-unpack from T.srcs
 };
 
 template <int MAXSEG>
@@ -818,51 +819,70 @@ adt_awp_fixup_kernel(const __grid_constant__ FixupTable<MAXSEG> F) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t *ws = stage[warp];
     const int32_t n_esc = F.escalated[0];                // usually 0: one load and out
-    uint32_t vt = blockIdx.x;                            // virtual tile index over escalated layers
+    uint32_t vt = blockIdx.x;                            // virtual tile index over the escalated segments
     for (int32_t e = 0; e < n_esc; ++e) {
-        const int s = F.escalated[1 + e] - F.base;
-        if (s < 0 || s >= T.nseg) continue;              // another chunk's layer
-        const int r = F.widths_new[s];
-        const uint32_t nt = T.tile_begin[s + 1] - T.tile_begin[s];
-        if (nt == 0) continue;
-        for (; vt < nt; vt += gridDim.x) {
-            const uint32_t local = vt;
-            const uint64_t e0 = static_cast<uint64_t>(local) * kTile;
-            const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
-            const uint32_t g0 = warp * kWarpGroups + lane;
-            const uint4 *src = reinterpret_cast<const uint4 *>(F.masters[s]) + e0 / 4;
-            const uint32_t *src1 = reinterpret_cast<const uint32_t *>(src);
-            const uint32_t keep = 0xFFFFFFFFu << (8 * (4 - r));
-            uint4 v[kVec];
+        const int32_t layer = F.escalated[1 + e];
+        for (int s = 0; s < T.nseg; ++s) {
+            if (F.layer_of[s] != layer) continue;        // segments of other layers / chunks
+            const int r = F.widths_new[s];
+            const uint32_t nt = T.tile_begin[s + 1] - T.tile_begin[s];
+            if (nt == 0) continue;
+            for (; vt < nt; vt += gridDim.x) {
+                if (F.gather) {                           // the owner re-packed it: read it again
+                    unpack_tile<MAXSEG>(T, T.tile_begin[s] + vt, s, ws);
+                    continue;
+                }
+                const uint64_t e0 = static_cast<uint64_t>(vt) * kTile;
+                const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
+                const uint32_t g0 = warp * kWarpGroups + lane;
+                const uint4 *src = reinterpret_cast<const uint4 *>(F.masters[s]) + e0 / 4;
+                const uint32_t *src1 = reinterpret_cast<const uint32_t *>(src);
+                const uint32_t keep = 0xFFFFFFFFu << (8 * (4 - r));
+                uint4 v[kVec];
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) {
-                const uint32_t g = g0 + 32 * k, i = g * 4;
-                if (i + 4 <= m) {
-                    v[k] = src[g];
-                } else {
-                    uint32_t w[4];
+                for (int k = 0; k < kVec; ++k) {
+                    const uint32_t g = g0 + 32 * k, i = g * 4;
+                    if (i + 4 <= m) {
+                        v[k] = src[g];
+                    } else {
+                        uint32_t w[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
-                    v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+                        for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
+                        v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+                store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
+                uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
+                uint32_t *dst1 = reinterpret_cast<uint32_t *>(dst);
+#pragma unroll
+                for (int k = 0; k < kVec; ++k) {
+                    const uint32_t g = g0 + 32 * k, i = g * 4;
+                    const uint4 o = make_uint4(v[k].x & keep, v[k].y & keep, v[k].z & keep, v[k].w & keep);
+                    if (i + 4 <= m) {
+                        dst[g] = o;
+                    } else {
+                        if (i + 0 < m) dst1[i + 0] = o.x;
+                        if (i + 1 < m) dst1[i + 1] = o.y;
+                        if (i + 2 < m) dst1[i + 2] = o.z;
+                    }
                 }
             }
-            store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
-            uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
-            uint32_t *dst1 = reinterpret_cast<uint32_t *>(dst);
-#pragma unroll
-            for (int k = 0; k < kVec; ++k) {
-                const uint32_t g = g0 + 32 * k, i = g * 4;
-                const uint4 o = make_uint4(v[k].x & keep, v[k].y & keep, v[k].z & keep, v[k].w & keep);
-                if (i + 4 <= m) {
-                    dst[g] = o;
-                } else {
-                    if (i + 0 < m) dst1[i + 0] = o.x;
-                    if (i + 1 < m) dst1[i + 1] = o.y;
-                    if (i + 2 < m) dst1[i + 2] = o.z;
-                }
-            }
+            vt -= nt;                                    // continue the stride in the next escalated segment
         }
-        vt -= nt;                                        // continue the stride in the next escalated layer
+    }
+}
+
+// Per-layer sums of squares from the ranks' per-piece sums (the norm tails
+// gathered from every rank), added in fixed (rank, piece) order — the same
+// order as sharded.ShardPlan.combine_sumsq, so every rank gets the same bits.
+__global__ void __launch_bounds__(256)
+adt_awp_combine_kernel(const double *__restrict__ tails, int npieces_total, const int32_t *__restrict__ piece_layer,
+                       int nlayers, double *__restrict__ seg_sumsq) {
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlayers; l += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int k = 0; k < npieces_total; ++k)
+            if (piece_layer[k] == l) acc += tails[k];
+        seg_sumsq[l] = acc;
     }
 }
 
@@ -1452,16 +1472,20 @@ int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const ad
 
 extern "C++" {
 namespace {
+// masters == nullptr: gather mode (re-unpack from `sources`, segment l's
+// payload in sources[replicas[l].reserved]); seg_layer == nullptr: segment i
+// is layer base + i.
 template <int MAXSEG>
 int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
-                       const int32_t *escalated, const uint8_t *widths_new, int base, cudaStream_t stream) {
+                       const uint8_t *const *sources, int nsrc, const int32_t *seg_layer, const int32_t *escalated,
+                       const uint8_t *widths_new, int base, cudaStream_t stream) {
     FixupTable<MAXSEG> F;
     Table<MAXSEG> &T = F.T;
-    for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = nullptr;
+    for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = (sources != nullptr && i < nsrc) ? sources[i] : nullptr;
     T.packed_out = packed;
     T.seg_sumsq = nullptr;
     T.partials = nullptr;
-    T.dyn_r = nullptr;
+    T.dyn_r = masters == nullptr ? widths_new : nullptr;
     T.nseg = nseg;
     uint32_t acc = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -1471,14 +1495,15 @@ int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, 
         T.offset[i] = replicas[i].offset;
         T.weights[i] = reinterpret_cast<uintptr_t>(replicas[i].weights);
         T.round_to[i] = 4;
-        T.src_idx[i] = 0;
-        F.masters[i] = reinterpret_cast<uintptr_t>(masters[i].weights);
+        T.src_idx[i] = static_cast<uint8_t>(masters == nullptr ? replicas[i].reserved : 0);
+        F.masters[i] = masters != nullptr ? reinterpret_cast<uintptr_t>(masters[i].weights) : 0;
+        F.layer_of[i] = seg_layer != nullptr ? seg_layer[i] : base + i;
     }
     T.tile_begin[nseg] = acc;
     fill_hints(T, nseg, acc);
     F.escalated = escalated;
     F.widths_new = widths_new;
-    F.base = base;
+    F.gather = masters == nullptr ? 1 : 0;
     int sms = 0;
     if (sm_count_cached(&sms) != ADT_OK) return ADT_ERR_NO_DEVICE;
     const uint32_t grid = max(1u, min(acc, static_cast<uint32_t>(4 * sms)));
@@ -1502,13 +1527,81 @@ int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int n
     for (int base = 0; base < nseg; base += kLargeSeg) {
         const int cnt = min(kLargeSeg, nseg - base);
         const int st = cnt <= kSmallSeg
-            ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, escalated,
-                                            widths_new + base, base, s)
-            : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, escalated,
-                                            widths_new + base, base, s);
+            ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, nullptr, 0, nullptr,
+                                            escalated, widths_new + base, base, s)
+            : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, nullptr, 0, nullptr,
+                                            escalated, widths_new + base, base, s);
         if (st != ADT_OK) return st;
     }
     return ADT_OK;
+}
+
+int adt_awp_fixup_pieces(const adt_segment *masters, const adt_segment *replicas, int nseg, const int32_t *seg_layer,
+                         uint8_t *packed, const int32_t *escalated, const uint8_t *widths_new, void *stream) {
+    int v = validate(replicas, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    if ((v = validate(masters, nseg, packed, true)) != ADT_OK) return v;
+    if (nseg > 0 && (escalated == nullptr || widths_new == nullptr || seg_layer == nullptr)) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (replicas[i].round_to != 4 || masters[i].count != replicas[i].count ||
+            masters[i].offset != replicas[i].offset || seg_layer[i] < 0)
+            return ADT_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int base = 0; base < nseg; base += kLargeSeg) {
+        const int cnt = min(kLargeSeg, nseg - base);
+        const int st = cnt <= kSmallSeg
+            ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, nullptr, 0, seg_layer + base,
+                                            escalated, widths_new + base, base, s)
+            : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, nullptr, 0, seg_layer + base,
+                                            escalated, widths_new + base, base, s);
+        if (st != ADT_OK) return st;
+    }
+    return ADT_OK;
+}
+
+int adt_awp_fixup_gather(const adt_segment *replicas, int nseg, const int32_t *seg_layer,
+                         const uint8_t *const *sources, int nsrc, const int32_t *escalated,
+                         const uint8_t *widths_new, void *stream) {
+    if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
+    const int v = validate(replicas, nseg, sources[0], false, nsrc);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && (escalated == nullptr || widths_new == nullptr || seg_layer == nullptr)) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (replicas[i].round_to != 4 || seg_layer[i] < 0 || sources[replicas[i].reserved] == nullptr)
+            return ADT_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int base = 0; base < nseg; base += kLargeSeg) {
+        const int cnt = min(kLargeSeg, nseg - base);
+        const int st = cnt <= kSmallSeg
+            ? launch_fixup_chunk<kSmallSeg>(nullptr, replicas + base, cnt, nullptr, sources, nsrc, seg_layer + base,
+                                            escalated, widths_new + base, base, s)
+            : launch_fixup_chunk<kLargeSeg>(nullptr, replicas + base, cnt, nullptr, sources, nsrc, seg_layer + base,
+                                            escalated, widths_new + base, base, s);
+        if (st != ADT_OK) return st;
+    }
+    return ADT_OK;
+}
+
+int adt_unpack_multi_dyn(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
+                         const uint8_t *widths, void *stream) {
+    if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nsrc; ++i)
+        if (reinterpret_cast<uintptr_t>(sources[i]) % 16) return ADT_ERR_ALIGN;
+    const int v = validate(segs, nseg, sources[0], false, nsrc);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && widths == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (segs[i].round_to != 4 || (segs[i].count > 0 && sources[segs[i].reserved] == nullptr)) return ADT_ERR_ARG;
+    return run(Pass::Unpack, segs, nseg, sources, nsrc, nullptr, nullptr, nullptr, false, stream, widths);
+}
+
+int adt_awp_combine(const double *tails, int npieces_total, const int32_t *piece_layer, int nlayers,
+                    double *seg_sumsq, void *stream) {
+    if (tails == nullptr || piece_layer == nullptr || seg_sumsq == nullptr || npieces_total < 0 || nlayers < 1)
+        return ADT_ERR_ARG;
+    adt_awp_combine_kernel<<<(nlayers + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        tails, npieces_total, piece_layer, nlayers, seg_sumsq);
+    return cuda_status(cudaGetLastError());
 }
 
 int adt_device_sm_count(int *sm_count) {

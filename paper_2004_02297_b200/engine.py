@@ -348,3 +348,42 @@ def reduce_sgd_pack_dyn(table: ReduceSgdTable, grads: Sequence[int], sample_coun
         table.array, table.nseg, _lib.pointer_array(grads), counts, len(grads), float(lr), float(momentum),
         float(weight_decay), packed.data_ptr(), partials.data_ptr() if partials is not None else None,
         widths.data_ptr(), stream_handle(stream)))
+
+
+def _int32_array(values) -> ctypes.Array:
+    arr = (ctypes.c_int32 * max(1, len(values)))()
+    for i, v in enumerate(values):
+        arr[i] = int(v)
+    return arr
+
+
+def unpack_multi_dyn(table: SegmentTable, sources: Sequence[int], widths: torch.Tensor,
+                     stream: torch.cuda.Stream | None = None) -> None:
+    """adt_unpack_multi_dyn: gather-unpack with per-piece widths from device memory."""
+    _lib.check(_lib.load().adt_unpack_multi_dyn(table.array, table.nseg, _lib.pointer_array(sources), len(sources),
+                                                widths.data_ptr(), stream_handle(stream)))
+
+
+def awp_combine(tails: torch.Tensor, piece_layer: torch.Tensor, nlayers: int, sumsq: torch.Tensor,
+                stream: torch.cuda.Stream | None = None) -> None:
+    """adt_awp_combine: per-layer sums from the gathered per-piece sums, rank-major order."""
+    _lib.check(_lib.load().adt_awp_combine(tails.data_ptr(), piece_layer.numel(), piece_layer.data_ptr(), nlayers,
+                                           sumsq.data_ptr(), stream_handle(stream)))
+
+
+def awp_fixup_pieces(masters: SegmentTable, replicas: SegmentTable, seg_layer: Sequence[int], packed: torch.Tensor,
+                     escalated: torch.Tensor, widths_new: torch.Tensor,
+                     stream: torch.cuda.Stream | None = None) -> None:
+    """adt_awp_fixup_pieces: re-pack this rank's escalated pieces into its send buffer."""
+    _lib.check(_lib.load().adt_awp_fixup_pieces(masters.array, replicas.array, masters.nseg, _int32_array(seg_layer),
+                                                packed.data_ptr(), escalated.data_ptr(), widths_new.data_ptr(),
+                                                stream_handle(stream)))
+
+
+def awp_fixup_gather(replicas: SegmentTable, seg_layer: Sequence[int], sources: Sequence[int],
+                     escalated: torch.Tensor, widths_new: torch.Tensor,
+                     stream: torch.cuda.Stream | None = None) -> None:
+    """adt_awp_fixup_gather: re-unpack every rank's escalated pieces from their send buffers."""
+    _lib.check(_lib.load().adt_awp_fixup_gather(replicas.array, replicas.nseg, _int32_array(seg_layer),
+                                                _lib.pointer_array(sources), len(sources), escalated.data_ptr(),
+                                                widths_new.data_ptr(), stream_handle(stream)))

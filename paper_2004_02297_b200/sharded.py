@@ -165,7 +165,13 @@ class ShardedWeightSync:
     """
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None,
-                 transport: str = "nccl"):
+                 transport: str = "nccl", awp_on_device: bool = False, trace_ring: int = 256):
+        """awp_on_device (p2p transport): every rank runs the AWP decision on
+        its GPU from the gathered per-piece sums (identical inputs, so
+        identical decisions), pieces keep capacity offsets in the send
+        buffers, and a step — pack, norm, barrier, gather-unpack, decide,
+        re-pack + re-gather of escalated pieces — is device work only (one
+        CUDA graph per send slot); trace rows come back via drain_trace()."""
         import torch.distributed as dist
         engine.require_cuda()
         if transport not in ("nccl", "p2p", "auto"):
@@ -194,7 +200,113 @@ class ShardedWeightSync:
         self._grecv = None         # nccl: all-to-all'd gradient slices of this rank's shard
         if self.transport == "p2p":
             self._init_barrier()
-        self._plan(self.schedule.round_tos())
+        self.awp_on_device = bool(awp_on_device)
+        self._dawp = None
+        if self.awp_on_device:
+            if self.transport != "p2p" or not self.adaptive:
+                raise ValueError("awp_on_device needs transport='p2p' and a PrecisionController schedule")
+            # capacity offsets: ownership and layout never change with the widths
+            self.plan = ShardPlan.plan(self.counts, [4] * len(self.counts), self.world)
+            self._owners_fixed = True
+            self._plan([4] * len(self.counts))
+            self._init_device_awp(trace_ring)
+        else:
+            self._plan(self.schedule.round_tos())
+
+    # --------------------------------------------- device-resident AWP mode
+    def _init_device_awp(self, ring: int) -> None:
+        from .awp_device import DeviceAwp
+        d = self._dawp = DeviceAwp(self.schedule, self.device, ring)
+        self._side = torch.cuda.Stream(device=self.device)
+        self._sumsq_dev = torch.zeros(len(self.counts), dtype=torch.float64, device=self.device)
+        mine = self.plan.pieces[self.rank]
+        self._mine_layers = [pc.layer for pc in mine]
+        self._all_layers = [pc.layer for q in range(self.world) for pc in self.plan.pieces[q]]
+        dev = self.device
+        self._idx_mine = torch.tensor(self._mine_layers, dtype=torch.int64, device=dev)
+        self._idx_all = torch.tensor(self._all_layers, dtype=torch.int64, device=dev)
+        n_m, n_a = max(1, len(mine)), max(1, len(self._all_layers))
+        self._pw_mine = torch.zeros(n_m, dtype=torch.uint8, device=dev)
+        self._pw_all = torch.zeros(n_a, dtype=torch.uint8, device=dev)
+        self._pw_mine_new = torch.zeros(n_m, dtype=torch.uint8, device=dev)
+        self._pw_all_new = torch.zeros(n_a, dtype=torch.uint8, device=dev)
+        # piece k of rank q sits at tails[q * max_pieces + k]; -1 marks an empty slot
+        m = self.plan.max_pieces
+        pl = [-1] * (self.world * m)
+        for q in range(self.world):
+            for k, pc in enumerate(self.plan.pieces[q]):
+                pl[q * m + k] = pc.layer
+        self._piece_layer = torch.tensor(pl, dtype=torch.int32, device=dev)
+        self._my_reps = engine.SegmentTable([self.replicas[pc.layer][pc.lo:pc.hi] for pc in mine],
+                                            self.pack_table.layout)
+        self._dgraphs = {}
+        self._trace_log = []
+
+    def _device_step_kernels(self, slot: int, observe: bool) -> None:
+        d = self._dawp
+        main = torch.cuda.current_stream()
+        send = self.send[slot]
+        torch.index_select(d.widths, 0, self._idx_mine, out=self._pw_mine[:len(self._mine_layers)])
+        torch.index_select(d.widths, 0, self._idx_all, out=self._pw_all[:len(self._all_layers)])
+        engine.pack_dyn(self.pack_table, send, self._pw_mine, self._partials if observe else None, main)
+        if observe:
+            engine.finalize(self.pack_table, self._partials, self._tail(send), main)
+        self._barrier()
+        if observe:
+            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
+            self._side.wait_stream(main)
+            m = self.plan.max_pieces
+            engine.awp_combine(self.tails[:self.world * 8 * m].view(torch.float64), self._piece_layer,
+                               len(self.counts), self._sumsq_dev, self._side)
+            engine.awp_observe(self._sumsq_dev, d.struct, d.config, self._side)
+        engine.unpack_multi_dyn(self.unpack_table, self._peer[slot], self._pw_all, main)
+        if observe:
+            main.wait_stream(self._side)
+            torch.index_select(d.widths_new, 0, self._idx_mine, out=self._pw_mine_new[:len(self._mine_layers)])
+            torch.index_select(d.widths_new, 0, self._idx_all, out=self._pw_all_new[:len(self._all_layers)])
+            engine.awp_fixup_pieces(self.pack_table, self._my_reps, self._mine_layers, send, d.escalated,
+                                    self._pw_mine_new, main)
+            self._barrier()
+            engine.awp_fixup_gather(self.unpack_table, self._all_layers, self._peer[slot], d.escalated,
+                                    self._pw_all_new, main)
+            d.widths.copy_(d.widths_new)
+
+    def _step_device(self, batch: int, observe: bool, graphed: bool = True) -> SyncResult:
+        d = self._dawp
+        if observe and not d.label_set:
+            d.set_next_label(batch - 1)
+        slot = self._slot
+        self._slot ^= 1
+        if graphed:
+            key = (slot, observe)
+            g = self._dgraphs.get(key)
+            if g is None:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._device_step_kernels(slot, observe)
+                self._dgraphs[key] = g
+            g.replay()
+        else:
+            self._device_step_kernels(slot, observe)
+        if observe:
+            d.pending += 1
+            if d.pending >= d.ring_steps:
+                self._trace_log += self._drain_device()
+        return SyncResult(round_tos=None)
+
+    def _drain_device(self) -> list[tuple]:
+        self.check_barrier()
+        return self._dawp.drain()
+
+    def drain_trace(self) -> list[tuple]:
+        """awp_on_device: the trace rows observed since the last call (every
+        rank gets the same rows); refreshes the host controller."""
+        if not self.awp_on_device:
+            raise RuntimeError("drain_trace() is for awp_on_device=True")
+        rows = self._trace_log + self._drain_device()
+        self._trace_log = []
+        return rows
 
     # ------------------------------------------------------------- planning
     def _plan(self, round_tos):
@@ -281,6 +393,8 @@ class ShardedWeightSync:
 
     @property
     def round_tos(self) -> list[int]:
+        if getattr(self, "_dawp", None) is not None:
+            return self._dawp.round_tos()            # device read
         return list(self.plan.round_tos)
 
     # ------------------------------------------------------------- one step
@@ -383,6 +497,8 @@ class ShardedWeightSync:
     def step(self, batch: int = 0, observe: bool | None = None) -> SyncResult:
         if observe is None:
             observe = self.adaptive and batch > 0
+        if self.awp_on_device:
+            return self._step_device(batch, observe)
         used = self.round_tos
         self.launch_graphed(fused_norm=observe)   # p2p: one graph replay; nccl: eager
         res = SyncResult(round_tos=used)

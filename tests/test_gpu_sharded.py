@@ -204,3 +204,76 @@ def test_p2p_graphed_step_two_processes_one_gpu():
         p.join(timeout=60)
     for rank, ok, note in res:
         assert ok, (rank, note)
+
+
+def _device_awp_main(rank, world, port, q, graphed):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2004_02297_b200 as adt
+        from paper_2004_02297_b200.sharded import ShardedWeightSync
+        counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
+        L = len(counts)
+        rng = np.random.default_rng(11)
+        hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+        masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+        kw = dict(threshold=-1e-3, interval=2, step_bits=8, initial_bits=8)
+        octl = O.OracleController(L, **kw)
+        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport="p2p",
+                                 awp_on_device=True, trace_ring=4)
+        ok, notes, want = True, [], []
+        for step in range(9):
+            res = sync._step_device(step, step > 0, graphed=graphed)
+            if step > 0:
+                for i, h in enumerate(hosts):
+                    octl.observe_layer(i, O.l2_norm(h))
+                    want.append((step - 1, i, octl.bits[i]))
+            torch.cuda.synchronize()
+            rs = [octl.round_to(i) for i in range(L)] if step > 0 else [1] * L
+            if sync.round_tos != rs:
+                ok = False
+                notes.append(f"step {step}: widths {sync.round_tos} != {rs}")
+            for i, (h, r) in enumerate(zip(hosts, rs)):
+                if not np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32),
+                                      h.view(np.uint32) & np.uint32(O.keep_mask(r))):
+                    ok = False
+                    notes.append(f"step {step} layer {i} r={r} replica mismatch")
+            for m, h in zip(masters, hosts):          # shrink 1%: delta < threshold -> escalations
+                h *= np.float32(0.99)
+                m.copy_(torch.from_numpy(h))
+            del res
+        rows = sync.drain_trace()
+        if [(b, l, bits) for b, l, _, _, _, bits in rows] != want:
+            ok = False
+            notes.append(f"trace {rows[:3]} vs {want[:3]}")
+        q.put((rank, ok, notes[:5], [r[2] for r in rows]))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, False, [traceback.format_exc()], []))
+
+
+@pytest.mark.parametrize("graphed", [False, True])
+def test_p2p_device_awp_two_processes_one_gpu(graphed):
+    """ShardedWeightSync(p2p, awp_on_device): the decision on every rank's
+    GPU from the gathered per-piece sums, escalated pieces re-packed by their
+    owner and re-gathered by everyone — replicas, widths and trace rows vs the
+    oracle, identical norms on both ranks."""
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_device_awp_main, args=(r, 2, port, q, graphed)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, notes, _ in res:
+        assert ok, (rank, notes)
+    assert res[0][3] == res[1][3] and len(res[0][3]) > 0
