@@ -242,13 +242,19 @@ class ShardedWeightSync:
         self._dgraphs = {}
         self._trace_log = []
 
-    def _device_step_kernels(self, slot: int, observe: bool) -> None:
+    def _device_step_kernels(self, slot: int, observe: bool, pack=None) -> None:
+        """pack(widths A) [-> norm tails] -> barrier -> [gather tails -> combine -> observe(-> B)]
+        || gather-unpack(A) -> re-pack own escalated pieces -> barrier -> re-gather them -> A = B.
+        `pack(send, widths, partials, stream)` replaces the plain pack (the DP update)."""
         d = self._dawp
         main = torch.cuda.current_stream()
         send = self.send[slot]
         torch.index_select(d.widths, 0, self._idx_mine, out=self._pw_mine[:len(self._mine_layers)])
         torch.index_select(d.widths, 0, self._idx_all, out=self._pw_all[:len(self._all_layers)])
-        engine.pack_dyn(self.pack_table, send, self._pw_mine, self._partials if observe else None, main)
+        if pack is None:
+            engine.pack_dyn(self.pack_table, send, self._pw_mine, self._partials if observe else None, main)
+        else:
+            pack(send, self._pw_mine, self._partials, main)
         if observe:
             engine.finalize(self.pack_table, self._partials, self._tail(send), main)
         self._barrier()
@@ -297,7 +303,12 @@ class ShardedWeightSync:
 
     def _drain_device(self) -> list[tuple]:
         self.check_barrier()
-        return self._dawp.drain()
+        rows = self._dawp.drain()
+        if getattr(self, "_check_finite", False):
+            bad = next((r for r in rows if not math.isfinite(r[2])), None)
+            if bad is not None:
+                raise NonFiniteParameters(f"layer {bad[1]} parameters left the finite range (batch {bad[0]})")
+        return rows
 
     def drain_trace(self) -> list[tuple]:
         """awp_on_device: the trace rows observed since the last call (every
@@ -578,6 +589,24 @@ class ShardedWeightSync:
                 [self.masters[pc.layer][pc.lo:pc.hi] for pc in mine],
                 [self.velocities[pc.layer][pc.lo:pc.hi] for pc in mine],
                 [4 * (offs[pc.layer] + pc.lo) - rel for pc in mine], self.pack_table.layout)
+        if self.awp_on_device:
+            d = self._dawp
+            d.counter[1].fill_(int(batch))       # trace label of this observation
+            d.label_set = True
+            slot = self._slot
+            self._slot ^= 1
+            table = self._reduce_table
+
+            def fused(send, widths, partials, stream):
+                self._barrier()                  # every rank's gradients are written
+                engine.reduce_sgd_pack_dyn(table, grads, sample_counts, lr, momentum, weight_decay, send, widths,
+                                           partials, stream)
+            self._device_step_kernels(slot, True, pack=fused)
+            self._check_finite = True
+            d.pending += 1
+            if d.pending >= d.ring_steps:
+                self._trace_log += self._drain_device()
+            return SyncResult(round_tos=None)
         S = self.plan.send_bytes
         if self.transport == "nccl":
             send, recv = self.send[0][:S], self.recv[:S * self.world]

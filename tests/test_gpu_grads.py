@@ -274,3 +274,78 @@ def test_device_awp_gather_and_update_matches_host(adt):
     dev.update(g, *hp, batch=24)
     assert dev.drain_trace() == r1
     assert all(torch.equal(x, y) for x, y in zip(host.replicas, dev.replicas))
+
+
+def _device_rank_main(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2004_02297_b200 as adt
+        from paper_2004_02297_b200.grads import GradBucket
+        from paper_2004_02297_b200.sharded import ShardedWeightSync
+        counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
+        L = len(counts)
+        hp = (0.05, 0.9, 5e-4)
+        sc = [48, 80, 17][:world]
+        rng = np.random.default_rng(11)
+        w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+        v_ref = [np.zeros(n, np.float32) for n in counts]
+        masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
+        kw = dict(threshold=-2e-3, interval=2, step_bits=8, initial_bits=8)
+        octl = O.OracleController(L, **kw)
+        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport="p2p",
+                                 awp_on_device=True, trace_ring=4)
+        bucket = GradBucket(counts)
+        ok, notes, want = True, [], []
+        for b in range(8):
+            grads = [[np.float32(0.5 + 0.2 * k) * w + rng.standard_normal(w.size, dtype=np.float32)
+                      * np.float32(0.002) for w in w_ref] for k in range(world)]
+            bucket.load([torch.from_numpy(x).cuda() for x in grads[rank]])
+            sync.update(bucket, sc, *hp, batch=b)
+            torch.cuda.synchronize()
+            for i in range(L):
+                w_ref[i], v_ref[i] = O.gather_and_update_weights(w_ref[i], v_ref[i], [g[i] for g in grads], sc, *hp)
+                octl.observe_layer(i, O.l2_norm(w_ref[i]))
+                want.append((b, i, octl.bits[i], octl.counter[i]))
+            rs = [octl.round_to(i) for i in range(L)]
+            if sync.round_tos != rs:
+                ok = False
+                notes.append(f"batch {b}: widths {sync.round_tos} != {rs}")
+            for i in range(L):
+                want_w = w_ref[i].view(np.uint32) & np.uint32(O.keep_mask(rs[i]))
+                if not np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want_w):
+                    ok = False
+                    notes.append(f"batch {b} layer {i} replica mismatch")
+        rows = sync.drain_trace()
+        if [(r[0], r[1], r[5], r[4]) for r in rows] != want:
+            ok = False
+            notes.append(f"trace {[(r[0], r[1], r[5], r[4]) for r in rows][:4]} vs {want[:4]}")
+        q.put((rank, ok, notes[:5], [r[2] for r in rows]))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, False, [traceback.format_exc()], []))
+
+
+def test_sharded_update_p2p_device_awp_two_processes():
+    """The whole data-parallel step with the AWP decision on the device:
+    fused gradient reduce over peer buckets + SGD + pack at device widths,
+    gathered norms, device decision, re-pack/re-gather of escalated pieces."""
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_device_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, notes, _ in res:
+        assert ok, (rank, notes)
+    assert res[0][3] == res[1][3] and len(res[0][3]) > 0
