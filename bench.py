@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-reduce", action="store_true",
                     help="skip the fused gradient-reduce + SGD + pack comparison (gradient return path)")
     ap.add_argument("--reduce-contribs", type=int, default=8, help="worker contributions for that comparison")
+    ap.add_argument("--no-awp-step", action="store_true",
+                    help="skip the per-step wall time of the AWP step (host vs device controller)")
     ap.add_argument("--l2", choices=["auto", "flush", "none"], default="auto",
                     help="flush L2 before every timed step (auto: when the FP32 masters are < 1.5x L2)")
     ap.add_argument("--transport", choices=["auto", "nccl", "p2p"], default="auto",
@@ -376,6 +378,9 @@ def main_ours(args):
     sgd = None
     if not args.no_sgd and world == 1:
         sgd = run_sgd_compare(masters, rs, dev)
+    awp = None
+    if not args.no_awp_step and world == 1:
+        awp = run_awp_step(masters)
     red = None
     if not args.no_reduce and world == 1:
         red = run_reduce_compare(masters, rs, dev, args.reduce_contribs)
@@ -406,7 +411,7 @@ def main_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
-            "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red, "dp_update": dp,
+            "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red, "dp_update": dp, "awp_step": awp,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -508,6 +513,35 @@ def run_sgd_compare(dev_masters, rs, dev, reps=20):
             "fused_GBps": (20 * n + pb) / (tf * 1e-3) / 1e9,
             "note": "fused: adt_sgd_pack (update + pack + norm, 20+r B/weight); unfused: torch in-place update "
                     "kernels + adt_pack"}
+
+
+def run_awp_step(dev_masters, steps=200):
+    """Wall-clock cost of one full AWP step through the public API
+    (WeightSync.step: pack + fused norm, unpack, observe, re-pack on
+    escalation) on this weight set: the AWP decision on the host (one 8·L-byte
+    read + Python Algorithm 1 per step) vs on the device (awp_on_device=True:
+    one graph replay per step, trace rows drained at the end)."""
+    import torch
+    import paper_2004_02297_b200 as adt
+    L = len(dev_masters)
+    cfg = adt.PrecisionConfig(threshold=-2e-3, interval=50, step_bits=8, initial_bits=8)
+    out = {}
+    for name, on_dev in (("host_controller_us", False), ("device_controller_us", True)):
+        masters = [m.clone() for m in dev_masters]
+        sync = adt.WeightSync(masters, adt.PrecisionController(L, cfg), awp_on_device=on_dev)
+        for b in range(10):
+            sync.step(batch=b)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for b in range(10, 10 + steps):
+            sync.step(batch=b)
+        if on_dev:
+            sync.drain_trace()
+        torch.cuda.synchronize()
+        out[name] = (time.perf_counter() - t0) / steps * 1e6
+        del sync, masters
+    out["note"] = "WeightSync.step wall time per step (widths start at 8 bits; interval 50)"
+    return out
 
 
 def run_reduce_compare(dev_masters, rs, dev, nc=8, reps=10):

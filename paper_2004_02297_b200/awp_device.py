@@ -93,10 +93,12 @@ class DeviceAwp:
         rows = []
         if n:
             ring = self.ring.cpu().numpy().view(_ROW_DT).reshape(self.ring_steps, self.nlayers)
-            for k in range(self.drained, count):
-                for r in ring[k % self.ring_steps]:
-                    rows.append((int(r["batch"]), int(r["layer"]), float(r["norm"]),
-                                 float(r["delta"]) if r["has_delta"] else None, int(r["counter"]), int(r["bits"])))
+            block = ring[[k % self.ring_steps for k in range(self.drained, count)]].reshape(-1)
+            deltas = block["delta"].tolist()
+            for i in np.flatnonzero(block["has_delta"] == 0).tolist():   # first observations only
+                deltas[i] = None
+            rows = list(zip(block["batch"].tolist(), block["layer"].tolist(), block["norm"].tolist(), deltas,
+                            block["counter"].tolist(), block["bits"].tolist()))
         self.drained = count
         self.pending = 0
         g = self.groups.cpu().numpy().view(_GROUP_DT)

@@ -9,13 +9,13 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_reference.json 2>&1
 for c in resnet50 vgg16 lenet; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-reduce > $OUT/bench_$c.json 2>&1; done
 for b in 8 16 24 32; do timeout 600 python bench.py --config 1b --bits $b --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 3 > $OUT/bench_1b_$b.json 2>&1; done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --quiet-extra --eager > $OUT/ncu_launch.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_ -s 6 -c 3 -o $OUT/prof_alexnet python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --quiet-extra --eager > $OUT/ncu_full.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --no-awp-step --quiet-extra --eager > $OUT/ncu_launch.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_ -s 6 -c 3 -o $OUT/prof_alexnet python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --no-awp-step --quiet-extra --eager > $OUT/ncu_full.log 2>&1
 tail -n 2 $OUT/pytest_gpu.log $OUT/smoke.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_sgd -c 1 -o $OUT/prof_sgd python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --no-h2d --no-reduce --quiet-extra --eager > $OUT/ncu_sgd.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_sgd -c 1 -o $OUT/prof_reduce python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --quiet-extra --eager > $OUT/ncu_reduce.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_ -s 6 -c 3 -o $OUT/prof_resnet50 python bench.py --config resnet50 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --quiet-extra --eager > $OUT/ncu_resnet.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_resnet50.csv python bench.py --config resnet50 --steps 5 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --quiet-extra --eager > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_ -s 6 -c 3 -o $OUT/prof_resnet50 python bench.py --config resnet50 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --no-awp-step --quiet-extra --eager > $OUT/ncu_resnet.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_resnet50.csv python bench.py --config resnet50 --steps 5 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --no-awp-step --quiet-extra --eager > /dev/null 2>&1
 timeout 600 python scripts/table2.py > $OUT/table2.md 2>&1
 ADT_KERNEL=tma timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu_tma.log 2>&1
 for t in memcheck racecheck synccheck initcheck; do timeout 600 compute-sanitizer --tool $t python scripts/sanitize_smoke.py > $OUT/sanitize_$t.log 2>&1; done
