@@ -57,6 +57,38 @@ def main():
         engine.reduce_sgd_pack(table, [b.flat.data_ptr() for b in buckets], [b.sample_count for b in buckets],
                                0.01, 0.9, 5e-4, packed, norms)
     torch.cuda.synchronize()
+    # device-resident AWP: dyn pack/unpack, observe, fixup with escalations every step (interval 1)
+    nz = [d for d in devs if d.numel()]
+    cfg = adt.PrecisionConfig(threshold=10.0, interval=1, step_bits=8, initial_bits=8)
+    ws = adt.WeightSync(nz, adt.PrecisionController(len(nz), cfg), awp_on_device=True, graphed=False, trace_ring=2)
+    for b in range(5):
+        ws.step(batch=b)
+    ws.gather_and_update([GradBucket([d.numel() for d in nz], sample_count=3).load([torch.randn_like(d) for d in nz])],
+                         lr=0.01, batch=5)
+    ws.drain_trace()
+    # peer barrier: two virtual ranks on two streams
+    flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    states = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for r in (1, 0):
+        engine.peer_barrier([f.data_ptr() for f in flags], r, states[r], stream=streams[r])
+    # multi-rank device-AWP kernels on local buffers: combine, dyn gather-unpack, fixup pieces / gather
+    lay4 = PackedLayout.plan([d.numel() for d in nz], [4] * len(nz))
+    tab = engine.SegmentTable(nz, lay4)
+    outs4 = [torch.empty_like(d) for d in nz]
+    otab = engine.SegmentTable(outs4, lay4, sources=[0] * len(nz))
+    buf = torch.zeros(lay4.nbytes, dtype=torch.uint8, device="cuda")
+    w = torch.full((len(nz),), 2, dtype=torch.uint8, device="cuda")
+    engine.pack_dyn(tab, buf, w)
+    engine.unpack_multi_dyn(otab, [buf.data_ptr()], w)
+    esc = torch.tensor([1, 0] + [0] * len(nz), dtype=torch.int32, device="cuda")
+    w3 = torch.full((len(nz),), 3, dtype=torch.uint8, device="cuda")
+    engine.awp_fixup_pieces(tab, engine.SegmentTable(outs4, lay4), list(range(len(nz))), buf, esc, w3)
+    engine.awp_fixup_gather(otab, list(range(len(nz))), [buf.data_ptr()], esc, w3)
+    tails = torch.rand(2 * len(nz), dtype=torch.float64, device="cuda")
+    pl = torch.tensor(list(range(len(nz))) * 2, dtype=torch.int32, device="cuda")
+    engine.awp_combine(tails, pl, len(nz), torch.empty(len(nz), dtype=torch.float64, device="cuda"))
+    torch.cuda.synchronize()
     print("sanitize smoke ok")
 
 
