@@ -35,7 +35,8 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = SOURCES + [os.path.join(ROOT, "include", "adt.h")]
+    deps = SOURCES + [os.path.join(ROOT, "include", "adt.h")] + \
+        [os.path.join(PKG, "csrc", f) for f in os.listdir(os.path.join(PKG, "csrc")) if f.endswith(".cuh")]
     return any(os.path.getmtime(p) > t for p in deps)
 
 

@@ -11,14 +11,20 @@
 //   * multi-tensor: one launch walks a per-layer descriptor table passed by
 //     value in kernel parameter space (__grid_constant__, up to 256 layers per
 //     launch); each CTA owns one 4096-weight tile of one layer and finds its
-//     layer with a uniform binary search over the tile prefix table;
+//     layer from a coarse tile->layer hint table in the same parameter block;
 //   * byte compaction with PRMT (__byte_perm): r = 1, 2, 4 are warp-coalesced
 //     32/64/128-bit stores straight from registers; r = 3 (12 bytes per 4
-//     weights) is staged through shared memory and written as 16-byte vectors;
+//     weights) and ragged tiles are staged per warp in shared memory and leave
+//     as one bulk async copy (cp.async.bulk);
 //   * the layer's float64 sum of squares is fused into the pack pass (every
-//     weight is read once); partials are per tile and the last CTA of a layer
-//     reduces them in a fixed order, so norms are run-to-run bit-identical
-//     (no floating-point atomics).
+//     weight is read once): one partial per warp slice, plain stores, summed
+//     in a fixed order by a small finalize kernel, so norms are run-to-run
+//     bit-identical (no floating-point atomics).
+//
+// One translation unit: this file (tables, tile helpers, pack / unpack /
+// finalize kernels, host launch code, C ABI) includes adt_sgd.cuh (fused
+// optimizer step + pack), adt_peer.cuh (peer-memory barrier and copies),
+// adt_awp.cuh (device-resident AWP) and adt_tma.cuh (the TMA A/B family).
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -526,146 +532,7 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
 }
 
 
-// ------------------------------------------------- fused SGD update + pack
-// the momentum-SGD step right before the path
-// (net.py:203-246, weight half of gather_and_update) fused with the pack and
-// the norm: one pass reads W, v and the gradient(s) and writes W', v' and W''s
-// packed bytes + norm partials, so the updated master is never re-read.
-//
-// NC = 0 (adt_sgd_pack): one pre-averaged gradient g.
-// NC >= 1 (adt_reduce_sgd_pack, the gradient return path): NC worker
-//   contributions g_c, read from NC source buffers (local, or peer ranks'
-//   gradient buckets mapped over NVLink — the reduce-scatter is this kernel's
-//   load stage), combined exactly as net.py:229-231:
-//     g = pairwise_sum(g_c * f32(count_c)) / f32(total)
-//   with pairwise_sum's association tree (net.py:186-200).
-// Then per weight, float32 with the reference's rounding at every operation
-// (no FMA contraction):
-//   g' = g + wd*W   (only when wd != 0)   v' = v*mu + g'   W' = W - lr*v'
-template <int MAXSEG>
-struct SgdTable : Table<MAXSEG> {
-    uintptr_t velocity[MAXSEG];
-    uintptr_t grad[MAXSEG];        // NC = 0: gradient address; NC >= 1: byte offset inside every srcs[c]
-    float scale[ADT_MAX_SOURCES];  // f32(sample_count_c)
-    float total;                   // f32(sum of sample counts)
-    float lr, momentum, weight_decay;
-};
-
-// net.py:186-200 on registers: adjacent pairs, level by level, an odd
-// leftover carried up unchanged. x[] is fully unrolled (constant indices).
-template <int LEN>
-struct Pairwise {
-    static __device__ __forceinline__ float run(float *x) {
-#pragma unroll
-        for (int i = 0; i < LEN / 2; ++i) x[i] = __fadd_rn(x[2 * i], x[2 * i + 1]);
-        if (LEN % 2) x[LEN / 2] = x[LEN - 1];
-        return Pairwise<(LEN + 1) / 2>::run(x);
-    }
-};
-template <>
-struct Pairwise<1> {
-    static __device__ __forceinline__ float run(float *x) { return x[0]; }
-};
-
-template <int NC, int MAXSEG>
-__device__ __forceinline__ uint32_t combine(const uint32_t *g, const SgdTable<MAXSEG> &T) {
-    if constexpr (NC == 0) {
-        return g[0];
-    } else {
-        float x[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) x[c] = __fmul_rn(__uint_as_float(g[c]), T.scale[c]);
-        return __float_as_uint(__fdiv_rn(Pairwise<NC>::run(x), T.total));
-    }
-}
-
-__device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb, float lr, float mu, float wd) {
-    const float w = __uint_as_float(wb);
-    float g = __uint_as_float(gb);
-    if (wd != 0.0f) g = __fadd_rn(g, __fmul_rn(wd, w));
-    const float v = __fadd_rn(__fmul_rn(__uint_as_float(vb), mu), g);
-    vb = __float_as_uint(v);
-    return __float_as_uint(__fsub_rn(w, __fmul_rn(lr, v)));
-}
-
-#ifndef ADT_SGD_MIN_BLOCKS
-#define ADT_SGD_MIN_BLOCKS 4
-#endif
-constexpr int sgd_min_blocks(int nc) { return nc == 0 ? ADT_SGD_MIN_BLOCKS : (nc <= 2 ? 3 : 2); }
-
-template <int MAXSEG, int NC>
-__global__ void __launch_bounds__(kThreads, sgd_min_blocks(NC))
-adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
-    constexpr int NG = NC > 0 ? NC : 1;
-    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
-    const uint32_t tile = blockIdx.x;
-    const int s = find_segment(T, tile);
-    const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
-    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
-    const int r = width_of(T, s);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t g0 = warp * kWarpGroups + lane;
-    uint4 *wp = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
-    uint4 *vp = reinterpret_cast<uint4 *>(T.velocity[s]) + e0 / 4;
-    const uint4 *gp[NG];
-#pragma unroll
-    for (int c = 0; c < NG; ++c)
-        gp[c] = reinterpret_cast<const uint4 *>((NC == 0 ? static_cast<uintptr_t>(0)
-                                                         : reinterpret_cast<uintptr_t>(T.srcs[c])) + T.grad[s]) + e0 / 4;
-    const float lr = T.lr, mu = T.momentum, wd = T.weight_decay;
-
-    uint4 w[kVec], v[kVec];
-    if (m == kTile) {
-#pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-            w[k] = __ldcs(wp + g0 + 32 * k);
-            v[k] = __ldcs(vp + g0 + 32 * k);
-        }
-#pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-            uint4 g[NG];
-#pragma unroll
-            for (int c = 0; c < NG; ++c) g[c] = __ldcs(gp[c] + g0 + 32 * k);
-            uint32_t gx[NG], gy[NG], gz[NG], gw[NG];
-#pragma unroll
-            for (int c = 0; c < NG; ++c) { gx[c] = g[c].x; gy[c] = g[c].y; gz[c] = g[c].z; gw[c] = g[c].w; }
-            w[k].x = sgd1(w[k].x, v[k].x, combine<NC>(gx, T), lr, mu, wd);
-            w[k].y = sgd1(w[k].y, v[k].y, combine<NC>(gy, T), lr, mu, wd);
-            w[k].z = sgd1(w[k].z, v[k].z, combine<NC>(gz, T), lr, mu, wd);
-            w[k].w = sgd1(w[k].w, v[k].w, combine<NC>(gw, T), lr, mu, wd);
-        }
-        // stores after every load: no load is ordered behind a possibly-aliasing store
-#pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-            wp[g0 + 32 * k] = w[k];
-            vp[g0 + 32 * k] = v[k];
-        }
-    } else {
-        uint32_t *w1 = reinterpret_cast<uint32_t *>(wp), *v1 = reinterpret_cast<uint32_t *>(vp);
-#pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-            const uint32_t i = (g0 + 32 * k) * 4;
-            uint32_t ww[4], vv[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                ww[j] = 0u;
-                vv[j] = 0u;
-                if (i + j < m) {
-                    uint32_t gg[NG];
-#pragma unroll
-                    for (int c = 0; c < NG; ++c) gg[c] = reinterpret_cast<const uint32_t *>(gp[c])[i + j];
-                    vv[j] = v1[i + j];
-                    ww[j] = sgd1(w1[i + j], vv[j], combine<NC>(gg, T), lr, mu, wd);
-                    w1[i + j] = ww[j];
-                    v1[i + j] = vv[j];
-                }
-            }
-            w[k] = make_uint4(ww[0], ww[1], ww[2], ww[3]);
-        }
-    }
-    store_packed(T.packed_out + T.offset[s] + e0 * r, w, m, r, warp, lane, g0, stage[warp]);
-    if (T.partials != nullptr) warp_partial(T.partials, tile, sumsq16(w));
-}
+#include "adt_sgd.cuh"
 
 }  // namespace
 
@@ -673,218 +540,8 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
 
 namespace {
 
-// ------------------------------------------------------- small peer copies
-// dst[q*bytes + i] = srcs[q][offset + i]: gathers each rank's norm tail (a few
-// dozen bytes) out of its peer-mapped send buffer.
-struct SrcList {
-    const uint8_t *p[ADT_MAX_SOURCES];
-};
-__global__ void adt_copy_multi_param_kernel(uint8_t *dst, const __grid_constant__ SrcList S, uint64_t offset,
-                                            uint64_t bytes) {
-    const uint8_t *src = S.p[blockIdx.x] + offset;
-    for (uint64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[blockIdx.x * bytes + i] = src[i];
-}
-
-// ------------------------------------------------ stream-ordered peer barrier
-// One warp. Lane q publishes this rank's new epoch into rank q's flag array
-// (peer memory over NVLink, release at system scope after a system fence, so
-// every write of the kernels before it on this stream is visible to the peers
-// first), then waits until every rank's epoch has arrived in the local array
-// (acquire at system scope: the kernels after it on this stream see the
-// peers' writes). The epoch comes from a device counter, so the barrier is
-// CUDA-graph capturable. The wait is bounded: on timeout the epoch is written
-// to state[1] and the kernel exits (the host raises; no hung GPU).
-struct FlagList {
-    uint32_t *p[ADT_MAX_SOURCES];
-};
-__global__ void __launch_bounds__(32) adt_peer_barrier_kernel(const __grid_constant__ FlagList F, int nranks,
-                                                              int rank, uint32_t *state, uint64_t max_polls) {
-    const int lane = threadIdx.x;
-    uint32_t epoch = 0;
-    if (lane == 0) epoch = state[0] + 1u;
-    epoch = __shfl_sync(0xFFFFFFFFu, epoch, 0);
-    __threadfence_system();
-    if (lane < nranks) {
-        uint32_t *dst = F.p[lane] + rank;
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
-    }
-    const uint32_t *mine = F.p[rank];
-    bool done = false;
-    for (uint64_t it = 0; it < max_polls; ++it) {
-        uint32_t v = epoch;
-        if (lane < nranks) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + lane) : "memory");
-        done = __all_sync(0xFFFFFFFFu, static_cast<int32_t>(v - epoch) >= 0);
-        if (done) break;
-        __nanosleep(64);
-    }
-    if (lane == 0) {
-        state[0] = epoch;
-        if (!done) state[1] = epoch;
-    }
-}
-
-// ------------------------------------------------ device-resident AWP step
-// Algorithm 1 (precision.py:125-141) on the device, so the
-// width decision of a step needs no host round trip and the whole step
-// (pack -> [finalize -> observe] || unpack -> fixup) replays as one graph.
-// One CTA; thread g walks group g's layers in layer order (groups share one
-// state, observed sequentially as in the reference; independent groups run
-// in parallel). float64 arithmetic in the reference's operation order:
-// norm = sqrt(sum of squares) (IEEE, as math.sqrt), delta = (n - prev) / prev.
-constexpr int kAwpThreads = 256;
-__global__ void __launch_bounds__(kAwpThreads)
-adt_awp_observe_kernel(const double *__restrict__ seg_sumsq, const __grid_constant__ adt_awp_device D,
-                       const __grid_constant__ adt_awp_config C) {
-    __shared__ int64_t slot_batch[2];
-    __shared__ int32_t n_esc;
-    if (threadIdx.x == 0) {
-        slot_batch[0] = D.counter[0] % D.ring_steps;
-        slot_batch[1] = D.counter[1];
-        n_esc = 0;
-    }
-    __syncthreads();
-    adt_awp_row *rows = D.ring + slot_batch[0] * D.nlayers;
-    const int32_t batch = static_cast<int32_t>(slot_batch[1]);
-    for (int g = threadIdx.x; g < D.ngroups; g += blockDim.x) {
-        adt_awp_group st = D.groups[g];
-        const int32_t lo = D.member_start[g], hi = D.member_start[g + 1];
-        for (int32_t k = lo; k < hi; ++k) {
-            const int32_t l = D.members[k];
-            const double n = sqrt(seg_sumsq[l]);
-            if (st.has_prev) {
-                double delta;
-                if (st.prev_norm > 0.0) delta = __ddiv_rn(__dsub_rn(n, st.prev_norm), st.prev_norm);
-                else delta = (n == 0.0) ? 0.0 : CUDART_INF;
-                st.last_delta = delta;
-                st.has_delta = 1;
-                if (delta < C.threshold) st.counter += 1;        // NaN never counts
-                else if (C.consecutive) st.counter = 0;
-            } else {
-                st.has_delta = 0;
-            }
-            if (st.counter == C.interval) {                      // also on the first observation
-                st.bits = min(st.bits + C.step_bits, C.max_bits);
-                st.counter = 0;
-            }
-            st.prev_norm = n;
-            st.has_prev = 1;
-            adt_awp_row row;
-            row.norm = n;
-            row.delta = st.has_delta ? st.last_delta : 0.0;
-            row.batch = batch;
-            row.layer = l;
-            row.counter = st.counter;
-            row.bits = st.bits;
-            row.has_delta = st.has_delta;
-            row.pad = 0;
-            rows[l] = row;
-        }
-        D.groups[g] = st;
-        const uint8_t w = static_cast<uint8_t>((st.bits + 7) / 8);   // bits_to_round_to
-        for (int32_t k = lo; k < hi; ++k) {
-            const int32_t l = D.members[k];
-            D.widths_out[l] = w;
-            if (w != D.widths_in[l]) D.escalated[1 + atomicAdd(&n_esc, 1)] = l;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        D.escalated[0] = n_esc;
-        D.counter[0] += 1;
-        D.counter[1] += 1;
-    }
-}
-
-// Re-pack of the layers whose width the observation just raised: their
-// payload was written (and speculatively unpacked) at the old width; read the
-// master tile again, store its top widths_new bytes into the packed buffer
-// and the matching replica words (the reference re-packs at the new widths
-// and unpacks that, training.py:209-225). CTAs stride over the tiles of the
-// escalated layers only; with no escalation every CTA scans the widths and exits.
-template <int MAXSEG>
-struct FixupTable {
-    Table<MAXSEG> T;                 // replicas (weights[]), offsets, tile map; packed_out = the packed buffer
-    uintptr_t masters[MAXSEG];
-    int32_t layer_of[MAXSEG];        // global layer id of each segment (a layer piece)
-    const int32_t *escalated;        // count, then global layer ids
-    const uint8_t *widths_new;       // per segment (chunk-relative)
-    int32_t gather;                  // 0: re-pack from masters + write replicas; 1: re-unpack from T.srcs
-};
-
-template <int MAXSEG>
-__global__ void __launch_bounds__(kThreads)
-adt_awp_fixup_kernel(const __grid_constant__ FixupTable<MAXSEG> F) {
-    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
-    const Table<MAXSEG> &T = F.T;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *ws = stage[warp];
-    const int32_t n_esc = F.escalated[0];                // usually 0: one load and out
-    uint32_t vt = blockIdx.x;                            // virtual tile index over the escalated segments
-    for (int32_t e = 0; e < n_esc; ++e) {
-        const int32_t layer = F.escalated[1 + e];
-        for (int s = 0; s < T.nseg; ++s) {
-            if (F.layer_of[s] != layer) continue;        // segments of other layers / chunks
-            const int r = F.widths_new[s];
-            const uint32_t nt = T.tile_begin[s + 1] - T.tile_begin[s];
-            if (nt == 0) continue;
-            for (; vt < nt; vt += gridDim.x) {
-                if (F.gather) {                           // the owner re-packed it: read it again
-                    unpack_tile<MAXSEG>(T, T.tile_begin[s] + vt, s, ws);
-                    continue;
-                }
-                const uint64_t e0 = static_cast<uint64_t>(vt) * kTile;
-                const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
-                const uint32_t g0 = warp * kWarpGroups + lane;
-                const uint4 *src = reinterpret_cast<const uint4 *>(F.masters[s]) + e0 / 4;
-                const uint32_t *src1 = reinterpret_cast<const uint32_t *>(src);
-                const uint32_t keep = 0xFFFFFFFFu << (8 * (4 - r));
-                uint4 v[kVec];
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) {
-                    const uint32_t g = g0 + 32 * k, i = g * 4;
-                    if (i + 4 <= m) {
-                        v[k] = src[g];
-                    } else {
-                        uint32_t w[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) w[j] = (i + j < m) ? src1[i + j] : 0u;
-                        v[k] = make_uint4(w[0], w[1], w[2], w[3]);
-                    }
-                }
-                store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
-                uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
-                uint32_t *dst1 = reinterpret_cast<uint32_t *>(dst);
-#pragma unroll
-                for (int k = 0; k < kVec; ++k) {
-                    const uint32_t g = g0 + 32 * k, i = g * 4;
-                    const uint4 o = make_uint4(v[k].x & keep, v[k].y & keep, v[k].z & keep, v[k].w & keep);
-                    if (i + 4 <= m) {
-                        dst[g] = o;
-                    } else {
-                        if (i + 0 < m) dst1[i + 0] = o.x;
-                        if (i + 1 < m) dst1[i + 1] = o.y;
-                        if (i + 2 < m) dst1[i + 2] = o.z;
-                    }
-                }
-            }
-            vt -= nt;                                    // continue the stride in the next escalated segment
-        }
-    }
-}
-
-// Per-layer sums of squares from the ranks' per-piece sums (the norm tails
-// gathered from every rank), added in fixed (rank, piece) order — the same
-// order as sharded.ShardPlan.combine_sumsq, so every rank gets the same bits.
-__global__ void __launch_bounds__(256)
-adt_awp_combine_kernel(const double *__restrict__ tails, int npieces_total, const int32_t *__restrict__ piece_layer,
-                       int nlayers, double *__restrict__ seg_sumsq) {
-    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlayers; l += gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int k = 0; k < npieces_total; ++k)
-            if (piece_layer[k] == l) acc += tails[k];
-        seg_sumsq[l] = acc;
-    }
-}
+#include "adt_peer.cuh"
+#include "adt_awp.cuh"
 
 // ----------------------------------------------------------------- host side
 enum class Pass { Pack, PackNorm, Norm, Unpack, Finalize };
