@@ -21,3 +21,5 @@ ADT_KERNEL=tma timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu
 for t in memcheck racecheck synccheck initcheck; do timeout 600 compute-sanitizer --tool $t python scripts/sanitize_smoke.py > $OUT/sanitize_$t.log 2>&1; done
 ADT_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 --transport p2p --config lenet > $OUT/bench_n2_gloo_p2p.log 2>&1
 tail -n 2 $OUT/pytest_gpu_tma.log $OUT/sanitize_*.log
+python scripts/step_overhead.py > $OUT/step_overhead.txt 2>&1
+timeout 600 python -m paper_2004_02297_b200 bench-codec --sizes 1000000,67108864 --workers 1,2,8 > $OUT/bench_codec.txt 2>&1
