@@ -482,3 +482,28 @@ def test_device_controller_groups_match_host_controller(adt):
     got = dev_sync.drain_trace()
     assert got == want
     assert max(host_sync.round_tos) > 1
+
+
+def test_device_controller_beyond_one_launch_table(adt):
+    """300 layers (two launch chunks for every dyn kernel and the fixup) with
+    escalations every other step: device AWP equals the host controller."""
+    rng = np.random.default_rng(13)
+    counts = [int(x) for x in rng.integers(1, 3000, 300)]
+    kw = dict(threshold=-5e-4, interval=2, step_bits=8, initial_bits=8)
+    hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+    ma = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+    mb = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+    host_sync = adt.WeightSync(ma, adt.PrecisionController(len(counts), adt.PrecisionConfig(**kw)))
+    dev_sync = adt.WeightSync(mb, adt.PrecisionController(len(counts), adt.PrecisionConfig(**kw)), awp_on_device=True)
+    want = []
+    for t in range(7):
+        f = (1.0 - rng.uniform(0.0, 0.002, len(counts))).astype(np.float32)
+        for i, (a, b) in enumerate(zip(ma, mb)):
+            a.mul_(float(f[i]))
+            b.mul_(float(f[i]))
+        want += host_sync.step(batch=t).trace
+        dev_sync.step(batch=t)
+    assert dev_sync.drain_trace() == want
+    assert dev_sync.round_tos == host_sync.round_tos and max(host_sync.round_tos) > 1
+    for x, y in zip(host_sync.replicas, dev_sync.replicas):
+        assert torch.equal(x, y)
