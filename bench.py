@@ -408,6 +408,8 @@ def main_ours(args):
     if not args.no_e2e and world == 1:
         e2e = run_e2e_weightsync(args, masters, rs, dev)
         e2e_dropin = run_e2e(args, masters, rs, dev)
+    elif not args.no_e2e and world > 1:
+        e2e = run_e2e_sharded(args, sync, counts, rs, dev, backend)
 
     h2d = None
     if not args.no_h2d and world == 1:
@@ -730,6 +732,47 @@ def run_e2e(args, dev_masters, rs, dev):
     return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt * 1e3, "steps": steps,
             "note": "drop-in per-layer pack_vectorized + unpack + l2_norm on host NumPy arrays; wall clock"}
+
+
+def run_e2e_sharded(args, sync, counts, rs, dev, backend):
+    """N > 1 end to end through ShardedWeightSync: every step each rank copies
+    the FP32 master pieces it owns from pinned host memory (the paper's CPU
+    masters, sharded), runs the step (pack with the norm, exchange,
+    gather-unpack of every replica) and reads the per-layer norms back (the
+    AWP input). Wall time per step, max over ranks; value = the whole job's
+    algorithmic bytes per step / time, as the device-timed value."""
+    import torch
+    import torch.distributed as dist
+    mine = sync.plan.pieces[sync.rank]
+    views = [sync.masters[pc.layer][pc.lo:pc.hi] for pc in mine]
+    host = [v.cpu().pin_memory() for v in views]
+    h2d = sum(h.numel() * 4 for h in host)
+    world = sync.world
+
+    def one():
+        for v, h in zip(views, host):
+            v.copy_(h, non_blocking=True)
+        sync.launch_graphed(True)
+        sync._norms()                      # D2H of the gathered norm tails + host sync
+
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    t = torch.tensor([dt, float(h2d)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    dt = float(tmax[0].item())
+    byts = sum((4 + r) * n for n, r in zip(counts, rs)) * (1 + world)
+    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(t[1].item()),
+            "d2h_bytes_per_step": 8 * world * sync.plan.max_pieces * world, "ms_per_step": dt * 1e3,
+            "note": "ShardedWeightSync from pinned host FP32 master shards; wall clock, max over ranks"}
 
 
 def run_e2e_weightsync(args, dev_masters, rs, dev):
