@@ -24,7 +24,7 @@ from typing import BinaryIO, Sequence
 import numpy as np
 import torch
 
-from . import engine
+from . import engine, hostio
 from .layout import PackedLayout, align_up
 
 WORD_BYTES = 4
@@ -103,7 +103,7 @@ class PackedBlock:
 
     def payload_bytes(self) -> bytes:
         if self.on_device:
-            return self.payload.cpu().numpy().tobytes()
+            return hostio.to_bytes(self.payload)
         return self.payload
 
     def to_host(self) -> "PackedBlock":
@@ -150,7 +150,7 @@ def _device_words(weights) -> tuple[torch.Tensor, bool]:
     host = np.ascontiguousarray(weights, dtype=np.float32).reshape(-1)
     if host.size == 0:
         return torch.empty(0, dtype=torch.float32, device="cuda"), False
-    return torch.from_numpy(host).to("cuda"), False
+    return hostio.to_device(host), False
 
 
 def _pack_device(flat: torch.Tensor, r: int) -> torch.Tensor:
@@ -169,7 +169,7 @@ def pack(weights, round_to: int) -> PackedBlock:
     payload = _pack_device(flat, r)
     if on_dev:
         return PackedBlock(r, flat.numel(), payload)
-    return PackedBlock(r, flat.numel(), payload.cpu().numpy().tobytes())
+    return PackedBlock(r, flat.numel(), hostio.to_bytes(payload))
 
 
 def pack_vectorized(weights, round_to: int) -> PackedBlock:
@@ -209,9 +209,9 @@ def unpack(block: PackedBlock):
     else:
         with warnings.catch_warnings():  # read-only bytes: the view is only ever read (copied to the device)
             warnings.simplefilter("ignore", UserWarning)
-            src = torch.frombuffer(block.payload, dtype=torch.uint8).to("cuda")
+            src = hostio.to_device(np.frombuffer(block.payload, dtype=np.uint8))
     engine.unpack(engine.SegmentTable([out], layout), src)
-    return out if block.on_device else out.cpu().numpy()
+    return out if block.on_device else hostio.to_numpy_f32(out)
 
 
 # ------------------------------------------------------------ container

@@ -1,0 +1,131 @@
+"""Host <-> device copies for the drop-in per-layer API (host NumPy in, `bytes`
+/ NumPy out, as the reference's codec.py:116-197 and precision.py:25-28).
+
+A pageable `torch.from_numpy(x).cuda()` runs at ~11 GB/s and `.cpu().numpy()
+.tobytes()` at ~1-2 GB/s on the B200 boxes: the latter pays the DMA through a
+driver bounce buffer plus a single-threaded copy into freshly allocated
+(page-faulting) memory. Large transfers here go through a reused pinned
+staging buffer, in chunks: DMA at PCIe speed, and the host-side copy into or
+out of the caller's memory split over worker threads (NumPy and ctypes copies
+release the GIL, and page faults of a fresh output are taken in parallel).
+The results are the same objects the reference returns: a new `bytes`, a new
+writable float32 array.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+SMALL = 1 << 20            # below this, plain torch copies
+CHUNK = 64 << 20           # staging chunk (bytes)
+_init_lock = threading.Lock()   # lazy creation of the pool / staging buffers
+_use_lock = threading.Lock()    # one user of the staging buffers at a time
+_staging: dict = {}        # device index -> pinned uint8 tensor of CHUNK bytes
+_pool = None
+
+_PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
+_PyBytes_FromStringAndSize.restype = ctypes.py_object
+_PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+_PyBytes_AsString = ctypes.pythonapi.PyBytes_AsString
+_PyBytes_AsString.restype = ctypes.c_void_p
+_PyBytes_AsString.argtypes = [ctypes.py_object]
+
+
+def _workers() -> ThreadPoolExecutor:
+    global _pool
+    if _pool is None:
+        with _init_lock:
+            if _pool is None:
+                _pool = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+    return _pool
+
+
+def _stage(device: torch.device) -> list:
+    """Two pinned CHUNK-byte buffers per device (double buffering) and their events."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    with _init_lock:
+        st = _staging.get(idx)
+        if st is None:
+            st = _staging[idx] = [(torch.empty(CHUNK, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+                                  for _ in range(2)]
+        return st
+
+
+def _parallel_memmove(dst: int, src: int, nbytes: int) -> None:
+    n = max(1, min(16, nbytes >> 22))          # >= 4 MiB per thread
+    step = -(-nbytes // n)
+    futs = [_workers().submit(ctypes.memmove, dst + i * step, src + i * step, min(step, nbytes - i * step))
+            for i in range(n) if i * step < nbytes]
+    for f in futs:
+        f.result()
+
+
+def to_device(host: np.ndarray, device: torch.device | str = "cuda") -> torch.Tensor:
+    """A contiguous host array -> a new CUDA tensor of the same dtype (flattened).
+    Chunk k+1 is copied into one pinned buffer while chunk k's DMA drains the other."""
+    dev = torch.device(device)
+    host = np.ascontiguousarray(host).reshape(-1)
+    if host.nbytes < SMALL:
+        return torch.from_numpy(host).to(dev)
+    out = torch.empty(host.size, dtype=torch.from_numpy(host[:1]).dtype, device=dev)
+    raw_out = out.view(torch.uint8)
+    src = host.ctypes.data
+    bufs = _stage(out.device)
+    stream = torch.cuda.current_stream(out.device)
+    with _use_lock:
+        for k, pos in enumerate(range(0, host.nbytes, CHUNK)):
+            n = min(CHUNK, host.nbytes - pos)
+            buf, done = bufs[k & 1]
+            done.synchronize()                  # this buffer's previous DMA has finished
+            _parallel_memmove(buf.data_ptr(), src + pos, n)
+            raw_out[pos:pos + n].copy_(buf[:n], non_blocking=True)
+            done.record(stream)
+        stream.synchronize()
+    return out
+
+
+def _from_device(dev_bytes: torch.Tensor, dst: int) -> None:
+    """Chunk k+1's DMA into one pinned buffer overlaps the copy of chunk k out of the other."""
+    bufs = _stage(dev_bytes.device)
+    stream = torch.cuda.current_stream(dev_bytes.device)
+    total = dev_bytes.numel()
+    chunks = list(range(0, total, CHUNK))
+    with _use_lock:
+        def issue(k):
+            pos = chunks[k]
+            buf, done = bufs[k & 1]
+            buf[:min(CHUNK, total - pos)].copy_(dev_bytes[pos:pos + CHUNK], non_blocking=True)
+            done.record(stream)
+        issue(0)
+        for k, pos in enumerate(chunks):
+            if k + 1 < len(chunks):
+                issue(k + 1)
+            buf, done = bufs[k & 1]
+            done.synchronize()
+            _parallel_memmove(dst + pos, buf.data_ptr(), min(CHUNK, total - pos))
+
+
+def to_bytes(dev_u8: torch.Tensor) -> bytes:
+    """A CUDA uint8 tensor -> a new `bytes` object holding its contents."""
+    flat = dev_u8.reshape(-1)
+    if flat.numel() < SMALL:
+        return flat.cpu().numpy().tobytes()
+    out = _PyBytes_FromStringAndSize(None, flat.numel())   # uninitialised, filled below (sole owner)
+    _from_device(flat.contiguous(), _PyBytes_AsString(out))
+    return out
+
+
+def to_numpy_f32(dev_f32: torch.Tensor) -> np.ndarray:
+    """A CUDA float32 tensor -> a new writable float32 NumPy array."""
+    flat = dev_f32.reshape(-1)
+    if flat.numel() * 4 < SMALL:
+        return flat.cpu().numpy()
+    out = np.empty(flat.numel(), dtype=np.float32)
+    _from_device(flat.contiguous().view(torch.uint8), out.ctypes.data)
+    return out
