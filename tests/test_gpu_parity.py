@@ -507,3 +507,25 @@ def test_device_controller_beyond_one_launch_table(adt):
     assert dev_sync.round_tos == host_sync.round_tos and max(host_sync.round_tos) > 1
     for x, y in zip(host_sync.replicas, dev_sync.replicas):
         assert torch.equal(x, y)
+
+
+def test_host_staging_chunks_and_round_trips(adt):
+    """hostio: sizes across the small-copy threshold and several 64 MiB staging
+    chunks (odd tails), both directions, then the drop-in host API on a
+    multi-chunk layer against the C oracle."""
+    from oracle import c_oracle as C
+    from paper_2004_02297_b200 import hostio
+    rng = np.random.default_rng(41)
+    for nbytes in (17, (1 << 20) + 3, 3 * hostio.CHUNK + 12345):
+        x = rng.integers(0, 256, nbytes, dtype=np.uint8)
+        d = hostio.to_device(x)
+        assert torch.equal(d.cpu(), torch.from_numpy(x))
+        assert hostio.to_bytes(d) == x.tobytes()
+    f = rng.standard_normal(2 * hostio.CHUNK // 4 + 777, dtype=np.float32)
+    assert np.array_equal(hostio.to_numpy_f32(hostio.to_device(f)), f)
+    w = rng.integers(0, 1 << 32, 40_000_003, dtype=np.uint32).view(np.float32)
+    for r in (1, 3, 4):
+        blk = adt.pack_vectorized(w, r)
+        assert blk.payload == C.pack(w, r)
+        back = adt.unpack(blk)
+        assert back.flags.writeable and np.array_equal(back.view(np.uint32), w.view(np.uint32) & np.uint32(O.keep_mask(r)))
