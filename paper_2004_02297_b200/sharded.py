@@ -1,18 +1,26 @@
-"""Multi-GPU weight distribution: shard-pack -> all-gather packed bytes -> unpack.
+"""Multi-GPU weight distribution: shard-pack -> exchange packed bytes -> unpack.
 
 The reference simulates data-parallel workers in one process and only
 *accounts* the bytes each worker would receive (training.py:214-225,
-transfer.py:143-174). Here every rank is one GPU (torchrun, NCCL over
-NVLink 5): rank p packs its contiguous shard of the concatenated layers at
-the AWP widths (norm partials fused into the same read), one
-`all_gather_into_tensor` (ncclAllGather on uint8) moves ONLY packed bytes,
-and every rank unpacks the whole gathered stream into its full FP32 replica.
+transfer.py:143-174). Here every rank is one GPU (torchrun): rank p packs its
+contiguous shard of the concatenated layers at the AWP widths (norm partials
+fused into the same read), only packed bytes cross NVLink, and every rank
+unpacks the whole stream into its full FP32 replica. Two transports:
+
+* p2p (default on one node, `transport="auto"`): every rank's send buffers are
+  mapped into every other rank (CUDA IPC); after a device-side barrier
+  (adt_peer_barrier) each rank's unpack kernel reads its peers' payloads over
+  NVLink directly (adt_unpack_multi) — the gather and the unpack are one pass;
+* nccl: `all_gather_into_tensor` (ncclAllGather, uint8) into a receive
+  buffer, then the unpack (the fallback when the GPUs are not peers).
 
 Send buffer of rank p (S_max bytes, identical size on every rank):
     [piece payloads, 16-B aligned | pad | float64 sum of squares per piece]
-The norm tail rides the same collective, so every rank combines the per-piece
-sums in fixed rank order and sees bit-identical norms -> identical AWP
-decisions on every rank with no extra collective.
+Every rank combines the per-piece sums from all tails in fixed rank order and
+sees bit-identical norms -> identical AWP decisions with no extra collective
+(SURVEY.md §8e). The same class runs the data-parallel update (the gradient
+return path, `update`) and, with `awp_on_device=True`, takes the AWP decision
+on every GPU so that a step involves no host round trip.
 
 Shards are balanced by packed bytes Σ n·r and cut at multiples of the
 4096-weight tile inside a layer, so every piece starts 16-B aligned on both
