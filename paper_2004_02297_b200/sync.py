@@ -206,6 +206,7 @@ class WeightSync:
     def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
         """The device work of one step on the current stream, no host sync:
         pack (+ norm partials), [side stream: finalize -> self.sumsq], unpack."""
+        self._host_widths_only()
         main = torch.cuda.current_stream()
         if fused_norm:
             if self._fin_pending:
@@ -221,12 +222,18 @@ class WeightSync:
             mid_event.record(main)
         engine.unpack(self.unpack_table, self.packed, main)
 
+    def _host_widths_only(self) -> None:
+        if getattr(self, "awp_on_device", False):
+            raise RuntimeError("launch()/launch_graphed()/phase_ms() use the host-planned widths; with "
+                               "awp_on_device=True the widths live on the device: use step()")
+
     def launch_graphed(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
         """launch() replayed from CUDA graphs captured once per layout: one
         graph [pack -> fork(finalize on the side branch) | unpack -> join], or,
         when the caller wants the pack/unpack split (`mid_event`), two graphs
         with the event recorded between them. Removes the per-step host launch
         cost (ctypes + stream bookkeeping): LeNet 39.6 -> 18.7 us per step."""
+        self._host_widths_only()
         split = mid_event is not None
         key = (fused_norm, split, self.layout)
         if self._graphs is None or self._graphs[0] != key:
@@ -242,6 +249,7 @@ class WeightSync:
         back-to-back copies of that phase in one CUDA graph timed by two events
         outside it (event nodes inside a graph cost several us each, which would
         distort short kernels): (pack ms, finalize||unpack ms). Synchronizes."""
+        self._host_widths_only()
         key = ("phase", fused_norm, reps, self.layout)
         if getattr(self, "_timed", None) is None or self._timed[0] != key:
             self.launch(fused_norm)
