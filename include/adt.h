@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 8
+#define ADT_ABI_VERSION 9
 
 /* status codes */
 #define ADT_OK 0
@@ -135,6 +135,16 @@ int adt_unpack(const adt_segment *segs, int nseg, const uint8_t *packed, void *s
  */
 int adt_unpack_multi(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
                      void *stream);
+
+/* adt_unpack_multi with two options: widths != NULL reads each segment's width
+ * from device memory (capacity layout, round_to 4, as adt_unpack_multi_dyn);
+ * start_seg >= 0 rotates the tile walk to begin just before segment start_seg
+ * (the caller's own first piece), so that ranks reading each other's buffers
+ * at the same moment pull from different peers rather than all draining one
+ * owner's NVLink port in lockstep. Results do not depend on either option's
+ * scheduling. */
+int adt_unpack_multi_ex(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
+                        const uint8_t *widths, int start_seg, void *stream);
 
 /* dst[q*bytes .. (q+1)*bytes) = sources[q][offset .. offset+bytes) for q < nsrc
  * (small peer reads, e.g. every rank's norm tail). */

@@ -23,12 +23,12 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 8
+ABI_VERSION = 9
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
 EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize",
-           "adt_unpack", "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
+           "adt_unpack", "adt_unpack_multi", "adt_unpack_multi_ex", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
            "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn", "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn",
            "adt_awp_observe", "adt_awp_fixup", "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces",
            "adt_awp_fixup_gather", "adt_device_sm_count")
@@ -147,6 +147,8 @@ def load() -> ctypes.CDLL:
         lib.adt_pack.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack.restype = ctypes.c_int
         lib.adt_unpack.argtypes = [seg_p, ctypes.c_int, vp, vp]
+        lib.adt_unpack_multi_ex.restype = ctypes.c_int
+        lib.adt_unpack_multi_ex.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp, ctypes.c_int, vp]
         lib.adt_unpack_multi.restype = ctypes.c_int
         lib.adt_unpack_multi.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp]
         lib.adt_copy_multi.restype = ctypes.c_int

@@ -66,6 +66,7 @@ struct Table {
     // from device memory (chunk-relative) instead of round_to[], so a width
     // change decided on the device needs no new launch table. nullptr = round_to[].
     const uint8_t *dyn_r;
+    uint32_t tile_rot;           // unpack: the tile walk starts rotated by this many tiles (< ntiles)
 };
 constexpr int kHints = 1024;
 
@@ -511,7 +512,11 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     // pack pass wrote last — the part still resident in the 126 MB L2 —
     // before it is evicted.
     if (!ADT_PERSISTENT) {
-        const uint32_t tile = ADT_UNPACK_REVERSE ? ntiles - 1 - blockIdx.x : blockIdx.x;
+        // Rotated walk (adt_unpack_multi_ex): each rank starts right before its
+        // own pieces, so at any moment the ranks pull from different peers
+        // instead of all draining the same owner's NVLink port in lockstep.
+        uint32_t tile = (ADT_UNPACK_REVERSE ? ntiles - 1 - blockIdx.x : blockIdx.x) + T.tile_rot;
+        if (tile >= ntiles) tile -= ntiles;
         unpack_tile<MAXSEG>(T, tile, find_segment(T, tile), ws);
         return;
     }
@@ -651,9 +656,10 @@ int validate(const adt_segment *segs, int nseg, const void *packed, bool need_pa
 template <int MAXSEG>
 int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc,
                  uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, bool finalize,
-                 cudaStream_t stream, const uint8_t *dyn_r = nullptr) {
+                 cudaStream_t stream, const uint8_t *dyn_r = nullptr, int start_seg = -1) {
     Table<MAXSEG> T;
     T.dyn_r = dyn_r;
+    T.tile_rot = 0;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = (srcs != nullptr && i < nsrc) ? srcs[i] : nullptr;
     T.packed_out = pout;
     T.seg_sumsq = seg_sumsq;
@@ -671,6 +677,7 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *co
     }
     T.tile_begin[nseg] = acc;
     fill_hints(T, nseg, acc);
+    if (start_seg >= 0 && start_seg < nseg && T.tile_begin[start_seg] < acc) T.tile_rot = T.tile_begin[start_seg];
     cudaError_t e = cudaSuccess;
     if (ntiles > 0 && pass != Pass::Finalize) {
         if (use_tma_kernels() && dyn_r == nullptr) {
@@ -708,7 +715,8 @@ constexpr int kLargeSeg = 256;
 // offsets of a chunk depend only on `segs`, so a separate finalize call
 // (adt_norm_finalize) walks exactly the chunks the pack pass wrote.
 int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc, uint8_t *pout,
-        double *seg_sumsq, double *partials, bool finalize, void *stream_v, const uint8_t *dyn_r = nullptr) {
+        double *seg_sumsq, double *partials, bool finalize, void *stream_v, const uint8_t *dyn_r = nullptr,
+        int start_seg = -1) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
     uint64_t partial_base = 0;
     int base = 0;
@@ -725,9 +733,9 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs
         double *pp = partials ? partials + partial_base : nullptr;
         const int st = cnt <= kSmallSeg
             ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles),
-                                      finalize, stream, dyn_r ? dyn_r + base : nullptr)
+                                      finalize, stream, dyn_r ? dyn_r + base : nullptr, start_seg - base)
             : launch_chunk<kLargeSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles),
-                                      finalize, stream, dyn_r ? dyn_r + base : nullptr);
+                                      finalize, stream, dyn_r ? dyn_r + base : nullptr, start_seg - base);
         if (st != ADT_OK) return st;
         partial_base += tiles * kWarpsPerTile;
         base += cnt;
@@ -784,6 +792,7 @@ int launch_sgd_chunk(const adt_sgd_segment *segs, const adt_grad_segment *gsegs,
                      int base) {
     SgdTable<MAXSEG> T;
     T.dyn_r = A.widths != nullptr ? A.widths + base : nullptr;
+    T.tile_rot = 0;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) {
         T.srcs[i] = A.srcs[i];
         T.scale[i] = A.scale[i];
@@ -1143,6 +1152,7 @@ int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, 
     T.seg_sumsq = nullptr;
     T.partials = nullptr;
     T.dyn_r = masters == nullptr ? widths_new : nullptr;
+    T.tile_rot = 0;
     T.nseg = nseg;
     uint32_t acc = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -1237,6 +1247,21 @@ int adt_awp_fixup_gather(const adt_segment *replicas, int nseg, const int32_t *s
         if (st != ADT_OK) return st;
     }
     return ADT_OK;
+}
+
+int adt_unpack_multi_ex(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
+                        const uint8_t *widths, int start_seg, void *stream) {
+    if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nsrc; ++i)
+        if (reinterpret_cast<uintptr_t>(sources[i]) % 16) return ADT_ERR_ALIGN;
+    const int v = validate(segs, nseg, sources[0], false, nsrc);
+    if (v != ADT_OK) return v;
+    for (int i = 0; i < nseg; ++i) {
+        if (segs[i].count > 0 && sources[segs[i].reserved] == nullptr) return ADT_ERR_ARG;
+        if (widths != nullptr && segs[i].round_to != 4) return ADT_ERR_ARG;   // capacity layout
+    }
+    return run(Pass::Unpack, segs, nseg, sources, nsrc, nullptr, nullptr, nullptr, false, stream, widths,
+               start_seg < nseg ? start_seg : -1);
 }
 
 int adt_unpack_multi_dyn(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,

@@ -212,11 +212,17 @@ def unpack(table: SegmentTable, packed: torch.Tensor, stream: torch.cuda.Stream 
     _lib.check(_lib.load().adt_unpack(table.array, table.nseg, packed.data_ptr(), stream_handle(stream)))
 
 
-def unpack_multi(table: SegmentTable, sources: Sequence[int], stream: torch.cuda.Stream | None = None) -> None:
-    """adt_unpack_multi: layer l's payload read from sources[table source index]
-    (raw device addresses: local buffers or peer buffers mapped by ipc_open)."""
+def unpack_multi(table: SegmentTable, sources: Sequence[int], stream: torch.cuda.Stream | None = None,
+                 start_seg: int = -1) -> None:
+    """adt_unpack_multi(_ex): layer l's payload read from sources[table source index]
+    (raw device addresses: local buffers or peer buffers mapped by ipc_open);
+    start_seg >= 0 rotates the tile walk to start just before that segment."""
     arr = _lib.pointer_array(sources)
-    _lib.check(_lib.load().adt_unpack_multi(table.array, table.nseg, arr, len(sources), stream_handle(stream)))
+    if start_seg >= 0:
+        _lib.check(_lib.load().adt_unpack_multi_ex(table.array, table.nseg, arr, len(sources), None, int(start_seg),
+                                                   stream_handle(stream)))
+    else:
+        _lib.check(_lib.load().adt_unpack_multi(table.array, table.nseg, arr, len(sources), stream_handle(stream)))
 
 
 def copy_multi(dst: torch.Tensor, sources: Sequence[int], offset: int, nbytes: int,
@@ -358,10 +364,11 @@ def _int32_array(values) -> ctypes.Array:
 
 
 def unpack_multi_dyn(table: SegmentTable, sources: Sequence[int], widths: torch.Tensor,
-                     stream: torch.cuda.Stream | None = None) -> None:
-    """adt_unpack_multi_dyn: gather-unpack with per-piece widths from device memory."""
-    _lib.check(_lib.load().adt_unpack_multi_dyn(table.array, table.nseg, _lib.pointer_array(sources), len(sources),
-                                                widths.data_ptr(), stream_handle(stream)))
+                     stream: torch.cuda.Stream | None = None, start_seg: int = -1) -> None:
+    """adt_unpack_multi_ex with device widths: gather-unpack with per-piece
+    widths from device memory (and an optional rotated tile walk)."""
+    _lib.check(_lib.load().adt_unpack_multi_ex(table.array, table.nseg, _lib.pointer_array(sources), len(sources),
+                                               widths.data_ptr(), int(start_seg), stream_handle(stream)))
 
 
 def awp_combine(tails: torch.Tensor, piece_layer: torch.Tensor, nlayers: int, sumsq: torch.Tensor,

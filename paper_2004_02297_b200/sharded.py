@@ -273,7 +273,7 @@ class ShardedWeightSync:
             engine.awp_combine(self.tails[:self.world * 8 * m].view(torch.float64), self._piece_layer,
                                len(self.counts), self._sumsq_dev, self._side)
             engine.awp_observe(self._sumsq_dev, d.struct, d.config, self._side)
-        engine.unpack_multi_dyn(self.unpack_table, self._peer[slot], self._pw_all, main)
+        engine.unpack_multi_dyn(self.unpack_table, self._peer[slot], self._pw_all, main, start_seg=self._unpack_start)
         if observe:
             main.wait_stream(self._side)
             torch.index_select(d.widths_new, 0, self._idx_mine, out=self._pw_mine_new[:len(self._mine_layers)])
@@ -361,6 +361,9 @@ class ShardedWeightSync:
                 offs.append(pc.offset if self.transport == "p2p" else q * S + pc.offset)
                 srcs.append(q if self.transport == "p2p" else 0)
         self.unpack_layout = PackedLayout(tuple(cnt), tuple(rs), tuple(offs), S * self.world)
+        # p2p: this rank's gather-unpack walk starts just before its own pieces, so
+        # at any moment the ranks pull from different peers (not one owner in lockstep)
+        self._unpack_start = sum(len(self.plan.pieces[q]) for q in range(self.rank))
         self.grad_ranges = shard_ranges(self.plan, self.counts)
         self._reduce_table = None
         self._graphs = None
@@ -475,7 +478,7 @@ class ShardedWeightSync:
             mid_event.record(torch.cuda.current_stream())
         if fused_norm:
             engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
-        engine.unpack_multi(self.unpack_table, self._peer[slot])
+        engine.unpack_multi(self.unpack_table, self._peer[slot], start_seg=self._unpack_start)
 
     def launch_graphed(self, fused_norm: bool) -> None:
         """p2p: launch() replayed from CUDA graphs — every op of the step is a
@@ -632,7 +635,7 @@ class ShardedWeightSync:
         else:
             self._barrier()                      # every shard is stepped and packed
             engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
-            engine.unpack_multi(self.unpack_table, self._peer[slot])
+            engine.unpack_multi(self.unpack_table, self._peer[slot], start_seg=self._unpack_start)
         used = self.round_tos
         res = SyncResult(round_tos=used)
         norms = self._norms()

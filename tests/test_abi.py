@@ -27,7 +27,7 @@ def lib():
 def test_header_declares_the_expected_surface():
     assert declared_functions() == sorted(
         ["adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", "adt_norm_finalize", "adt_unpack",
-         "adt_unpack_multi", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
+         "adt_unpack_multi", "adt_unpack_multi_ex", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle", "adt_ipc_open",
          "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn",
          "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn", "adt_awp_observe", "adt_awp_fixup",
          "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces", "adt_awp_fixup_gather",

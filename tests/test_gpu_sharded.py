@@ -56,10 +56,15 @@ def test_unpack_multi_virtual_ranks(adt):
             offs.append(pc.offset)
             srcs.append(q)
     lay = PackedLayout(tuple(cnt), tuple(rr), tuple(offs), plan.send_bytes)
-    engine.unpack_multi(engine.SegmentTable(views, lay, sources=srcs), [b.data_ptr() for b in bufs])
-    torch.cuda.synchronize()
-    for h, r, o in zip(hosts, rs, outs):
-        assert np.array_equal(o.cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+    table = engine.SegmentTable(views, lay, sources=srcs)
+    # the rotated walk (each rank starting before its own pieces) changes only the order
+    for start in (-1, 0, 1, len(views) // 2, len(views) - 1, len(views) + 3):
+        for o in outs:
+            o.fill_(float("nan"))
+        engine.unpack_multi(table, [b.data_ptr() for b in bufs], start_seg=start)
+        torch.cuda.synchronize()
+        for h, r, o in zip(hosts, rs, outs):
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r))), start
 
 
 def _free_port():
