@@ -1,5 +1,6 @@
-import sys
+"""`python -m paper_2004_02297_b200 ...` runs the codec command line (cli.py)."""
 
 from .cli import main
 
-sys.exit(main())
+if __name__ == "__main__":
+    raise SystemExit(main())
