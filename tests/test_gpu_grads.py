@@ -163,7 +163,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, transport="p2p"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
@@ -182,7 +182,7 @@ def _rank_main(rank, world, port, q):
         masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
         kw = dict(threshold=-2e-3, interval=2, step_bits=8, initial_bits=8)
         octl = O.OracleController(L, **kw)
-        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport="p2p")
+        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport=transport)
         bucket = GradBucket(counts)
         ok, notes, seen = True, [], []
         for b in range(8):
@@ -217,15 +217,17 @@ def _rank_main(rank, world, port, q):
         q.put((rank, False, [traceback.format_exc()], [], []))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_update_p2p_processes_sharing_one_gpu(world):
+@pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (2, "nccl"), (3, "nccl")])
+def test_sharded_update_processes_sharing_one_gpu(world, transport):
+    """transport="nccl": the all_to_all gradient exchange + all-gather path,
+    run over gloo with CUDA tensors (NCCL refuses two ranks on one device)."""
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs])

@@ -75,7 +75,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, transport="p2p"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
@@ -88,7 +88,7 @@ def _rank_main(rank, world, port, q):
         hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
         masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
         cfg = adt.PrecisionConfig(threshold=-1e-3, interval=1, step_bits=8, initial_bits=8)
-        sync = ShardedWeightSync(masters, adt.PrecisionController(len(counts), cfg), transport="p2p")
+        sync = ShardedWeightSync(masters, adt.PrecisionController(len(counts), cfg), transport=transport)
         ok, notes, norms_seen = True, [], []
         for step in range(4):
             res = sync.step(batch=step)
@@ -115,14 +115,17 @@ def _rank_main(rank, world, port, q):
         q.put((rank, False, [repr(e)], [], []))
 
 
-def test_p2p_sync_two_processes_one_gpu():
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_sync_two_processes_one_gpu(transport):
+    """transport="nccl" runs its all-gather code path over gloo here (CUDA
+    tensors; NCCL itself refuses two ranks on one device)."""
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=240) for _ in procs])
