@@ -66,7 +66,7 @@ class DeviceAwp:
         """Copy the host controller's state (and widths) to the device."""
         g = np.zeros(self.ngroups, _GROUP_DT)
         for gid, i in self.gindex.items():
-            st = self.controller._states[gid]
+            st = self.controller.group_state(gid)
             g[i] = (st.prev_norm if st.prev_norm is not None else 0.0,
                     st.last_delta if st.last_delta is not None else 0.0,
                     st.bits, st.interval_counter, int(st.prev_norm is not None), int(st.last_delta is not None))
@@ -103,7 +103,7 @@ class DeviceAwp:
         self.pending = 0
         g = self.groups.cpu().numpy().view(_GROUP_DT)
         for gid, i in self.gindex.items():
-            st = self.controller._states[gid]
+            st = self.controller.group_state(gid)
             st.bits = int(g[i]["bits"])
             st.interval_counter = int(g[i]["counter"])
             st.prev_norm = float(g[i]["prev_norm"]) if g[i]["has_prev"] else None

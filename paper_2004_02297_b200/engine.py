@@ -150,7 +150,11 @@ def reduce_sgd_pack(table: ReduceSgdTable, grads: Sequence[int], sample_counts: 
 
 
 class _Scratch:
-    """Per (device, stream) norm scratch: the float64 partials of one pass."""
+    """Per (device, stream) norm scratch: the float64 partials of one pass.
+    Entries live for the process: a buffer handed to a kernel on stream S must
+    not return to the caching allocator while S may still use it (it was
+    allocated on whatever stream was current), and there is one per stream in
+    use — a handful."""
 
     _lock = threading.Lock()
     _cache: dict = {}
@@ -161,9 +165,13 @@ class _Scratch:
         with cls._lock:
             cur = cls._cache.get(key)
             if cur is None or cur.numel() < max(1, n):
+                if cur is not None:
+                    cls._retired.append(cur)           # possibly still in use on `stream`
                 cur = torch.empty(max(1, n), dtype=torch.float64, device=device)
                 cls._cache[key] = cur
             return cur
+
+    _retired: list = []
 
 
 def _device_of(table: SegmentTable) -> torch.device:
