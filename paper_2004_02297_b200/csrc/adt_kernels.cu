@@ -300,21 +300,49 @@ __device__ __forceinline__ void warp_store_bytes(const uint32_t *ws, uint8_t *ds
 // Write a tile's packed bytes (the r top bytes of each of the thread's 16 words).
 // r = 1/2/4 full tiles: coalesced 32/64/128-bit stores straight from registers;
 // r = 3 and ragged tiles: the warp's span via its staging words, 16-B vectors.
+#ifndef ADT_PACK_EVICT_LAST
+#define ADT_PACK_EVICT_LAST 0   // A/B: packed-stream stores with an L2 evict_last policy
+#endif
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_keep(uint32_t *a, uint32_t x, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(x), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(uint2 *a, uint2 x, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(a), "r"(x.x), "r"(x.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(uint4 *a, uint4 x, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(x.x), "r"(x.y), "r"(x.z),
+                 "r"(x.w), "l"(pol) : "memory");
+}
+template <typename V>
+__device__ __forceinline__ void st_packed(V *a, V x) {
+    if (ADT_PACK_EVICT_LAST) st_keep(a, x, l2_keep_policy());
+    else *a = x;
+}
+
 __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec], uint32_t m, int r, int warp,
                                              int lane, uint32_t g0, uint32_t *ws) {
     if (!ADT_PACK_STAGE_ALL && m == kTile && r != 3) {
         if (r == 1) {
             uint32_t *d = reinterpret_cast<uint32_t *>(dst);
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); d[g0 + 32 * k] = o[0]; }
+            for (int k = 0; k < kVec; ++k) { uint32_t o[1]; pack_r1(v[k], o); st_packed(d + g0 + 32 * k, o[0]); }
         } else if (r == 2) {
             uint2 *d = reinterpret_cast<uint2 *>(dst);
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); d[g0 + 32 * k] = make_uint2(o[0], o[1]); }
+            for (int k = 0; k < kVec; ++k) { uint32_t o[2]; pack_r2(v[k], o); st_packed(d + g0 + 32 * k, make_uint2(o[0], o[1])); }
         } else {
             uint4 *d = reinterpret_cast<uint4 *>(dst);
 #pragma unroll
-            for (int k = 0; k < kVec; ++k) { uint32_t o[4]; pack_r4(v[k], o); d[g0 + 32 * k] = make_uint4(o[0], o[1], o[2], o[3]); }
+            for (int k = 0; k < kVec; ++k) {
+                uint32_t o[4];
+                pack_r4(v[k], o);
+                st_packed(d + g0 + 32 * k, make_uint4(o[0], o[1], o[2], o[3]));
+            }
         }
         return;
     }
@@ -349,10 +377,18 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
     if (lo < nbytes) {
         const uint32_t mine = min(span, nbytes - lo), n16 = mine & ~15u;
         if (lane == 0 && n16) {
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
-                         "cp.async.bulk.commit_group;\n\t"
-                         "cp.async.bulk.wait_group.read 0;" ::"l"(dst + lo),
-                         "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ws))), "r"(n16) : "memory");
+            if (ADT_PACK_EVICT_LAST) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n\t"
+                             "cp.async.bulk.commit_group;\n\t"
+                             "cp.async.bulk.wait_group.read 0;" ::"l"(dst + lo),
+                             "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ws))), "r"(n16), "l"(l2_keep_policy())
+                             : "memory");
+            } else {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                             "cp.async.bulk.commit_group;\n\t"
+                             "cp.async.bulk.wait_group.read 0;" ::"l"(dst + lo),
+                             "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ws))), "r"(n16) : "memory");
+            }
         }
         const uint8_t *s1 = reinterpret_cast<const uint8_t *>(ws);
         for (uint32_t i = n16 + lane; i < mine; i += 32) dst[lo + i] = s1[i];
@@ -433,6 +469,9 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
 #ifndef ADT_UNPACK_MIN_BLOCKS
 #define ADT_UNPACK_MIN_BLOCKS 5
 #endif
+#ifndef ADT_UNPACK_STCS
+#define ADT_UNPACK_STCS 1      // replica stores evict-first (A/B: VGG-16 204.7 -> 199.3 us, profiles/r01_ab_layer_hint.md)
+#endif
 #ifndef ADT_UNPACK_REVERSE
 #define ADT_UNPACK_REVERSE 1   // A/B: AlexNet step 132.7 -> 127.2 us (profiles/r01_ab_unpack_order.md)
 #endif
@@ -471,7 +510,10 @@ __device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t til
             for (int k = 0; k < kVec; ++k) out[k] = unpack_r4(w[k]);
         }
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) dst[g0 + 32 * k] = out[k];
+        for (int k = 0; k < kVec; ++k) {
+            if (ADT_UNPACK_STCS) __stcs(dst + g0 + 32 * k, out[k]);   // evict-first: keep the packed stream in L2
+            else dst[g0 + 32 * k] = out[k];
+        }
         return;
     }
 
