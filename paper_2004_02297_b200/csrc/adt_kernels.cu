@@ -470,7 +470,7 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
 #define ADT_UNPACK_MIN_BLOCKS 5
 #endif
 #ifndef ADT_UNPACK_STCS
-#define ADT_UNPACK_STCS 1      // replica stores evict-first (A/B: VGG-16 204.7 -> 199.3 us, profiles/r01_ab_layer_hint.md)
+#define ADT_UNPACK_STCS 2      // replica stores evict-first, direct (1) and staged (2) paths (profiles/r01_ab_layer_hint.md)
 #endif
 #ifndef ADT_UNPACK_REVERSE
 #define ADT_UNPACK_REVERSE 1   // A/B: AlexNet step 132.7 -> 127.2 us (profiles/r01_ab_unpack_order.md)
@@ -534,7 +534,8 @@ __device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t til
         if (g * 4 >= m) break;
         const uint4 o = unpack_words(r, ws + gl * r);
         if (g * 4 + 4 <= m) {
-            dst[g] = o;
+            if (ADT_UNPACK_STCS >= 2) __stcs(dst + g, o);
+            else dst[g] = o;
         } else {
             if (g * 4 + 0 < m) dst1[g * 4 + 0] = o.x;
             if (g * 4 + 1 < m) dst1[g * 4 + 1] = o.y;
