@@ -264,8 +264,8 @@ def _device_awp_main(rank, world, port, q, graphed):
         q.put((rank, False, [traceback.format_exc()], []))
 
 
-@pytest.mark.parametrize("graphed", [False, True])
-def test_p2p_device_awp_two_processes_one_gpu(graphed):
+@pytest.mark.parametrize("graphed,world", [(False, 2), (True, 2), (True, 8)])
+def test_p2p_device_awp_processes_sharing_one_gpu(graphed, world):
     """ShardedWeightSync(p2p, awp_on_device): the decision on every rank's
     GPU from the gathered per-piece sums, escalated pieces re-packed by their
     owner and re-gathered by everyone — replicas, widths and trace rows vs the
@@ -276,7 +276,7 @@ def test_p2p_device_awp_two_processes_one_gpu(graphed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_device_awp_main, args=(r, 2, port, q, graphed)) for r in range(2)]
+    procs = [ctx.Process(target=_device_awp_main, args=(r, world, port, q, graphed)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs])
@@ -284,4 +284,4 @@ def test_p2p_device_awp_two_processes_one_gpu(graphed):
         p.join(timeout=60)
     for rank, ok, notes, _ in res:
         assert ok, (rank, notes)
-    assert res[0][3] == res[1][3] and len(res[0][3]) > 0
+    assert all(r[3] == res[0][3] for r in res) and len(res[0][3]) > 0
