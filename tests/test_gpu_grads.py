@@ -175,8 +175,8 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
         L = len(counts)
         hp = (0.05, 0.9, 5e-4)
-        sc = [48, 80, 17][:world]
-        rng = np.random.default_rng(11)          # same stream on both ranks
+        sc = [48, 80, 17, 5, 64, 33, 9, 21][:world]
+        rng = np.random.default_rng(11)          # same stream on every rank
         w_ref = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
         v_ref = [np.zeros(n, np.float32) for n in counts]
         masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
@@ -217,7 +217,7 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         q.put((rank, False, [traceback.format_exc()], [], []))
 
 
-@pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (2, "nccl"), (3, "nccl")])
+@pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (8, "p2p"), (2, "nccl"), (3, "nccl")])
 def test_sharded_update_processes_sharing_one_gpu(world, transport):
     """transport="nccl": the all_to_all gradient exchange + all-gather path,
     run over gloo with CUDA tensors (NCCL refuses two ranks on one device)."""
