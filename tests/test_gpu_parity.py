@@ -529,3 +529,29 @@ def test_host_staging_chunks_and_round_trips(adt):
         assert blk.payload == C.pack(w, r)
         back = adt.unpack(blk)
         assert back.flags.writeable and np.array_equal(back.view(np.uint32), w.view(np.uint32) & np.uint32(O.keep_mask(r)))
+
+
+def test_measured_profile_shape(adt):
+    """transfer.measured_profile: the reference's profile_report phases with
+    measured device times (the Table-2 rows) — every phase present, positive,
+    and the weight-stream byte ratio equal to the reference ledger arithmetic."""
+    from paper_2004_02297_b200 import transfer
+    rng = np.random.default_rng(3)
+    counts = [20 * 25, 50 * 20 * 25, 500 * 800, 10 * 500]
+    masters = [torch.from_numpy(rng.standard_normal(n, dtype=np.float32)).cuda() for n in counts]
+
+    class W(adt.FixedPrecision):
+        def round_tos(self):
+            return [1, 2, 3, 4]
+
+    sync = adt.WeightSync(masters, W(len(counts), 32))
+    prof = transfer.measured_profile(sync)
+    ph = prof["phases"]
+    for key in ("pack", "unpack", "l2_norm", "to_worker"):
+        assert key in ph
+    assert ph["pack"]["device_s"] > 0 and ph["unpack"]["device_s"] > 0
+    assert ph["to_worker"]["raw_fp32_h2d_s"] > ph["to_worker"]["packed_h2d_s"] > 0
+    raw = sum(4 * n for n in counts)
+    wire = sum(14 + n * r for n, r in zip(counts, [1, 2, 3, 4]))
+    assert prof["weight_stream"]["raw_bytes"] == raw and prof["weight_stream"]["wire_bytes"] == wire
+    assert prof["weight_stream"]["ratio"] == pytest.approx(raw / wire)
