@@ -66,3 +66,53 @@ def test_multi_tensor_pack_unpack_norms(adt, counts, seed):
         assert np.array_equal(outs[i].cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
         ref = O.l2_norm(h)
         assert abs(np.sqrt(ss[i]) - ref) <= 1e-6 * ref
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(counts=st.lists(st.integers(0, 20000), min_size=1, max_size=10), world=st.integers(1, 8),
+       seed=st.integers(0, 2 ** 31))
+def test_virtual_ranks_shard_pack_gather_unpack(adt, counts, world, seed):
+    """Any layer set, widths and world size: every virtual rank packs its
+    ShardPlan pieces (device kernel, norm tail fused) into its own send
+    buffer; the rotated gather-unpack over all buffers rebuilds every replica
+    as the reference would, and the rank-order norm combine matches."""
+    from paper_2004_02297_b200 import engine
+    from paper_2004_02297_b200.layout import PackedLayout
+    from paper_2004_02297_b200.sharded import ShardPlan
+    rng = np.random.default_rng(seed)
+    rs = [int(x) for x in rng.integers(1, 5, len(counts))]
+    hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+    devs = [torch.from_numpy(h).cuda() for h in hosts]
+    plan = ShardPlan.plan(counts, rs, world)
+    S = plan.send_bytes
+    bufs = [torch.zeros(S, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    for q in range(world):
+        mine = plan.pieces[q]
+        if not mine:
+            continue
+        lay = PackedLayout(tuple(pc.hi - pc.lo for pc in mine), tuple(rs[pc.layer] for pc in mine),
+                           tuple(pc.offset for pc in mine), plan.payload_cap)
+        tail = bufs[q][plan.payload_cap:plan.payload_cap + 8 * plan.max_pieces].view(torch.float64)
+        engine.pack(engine.SegmentTable([devs[pc.layer][pc.lo:pc.hi] for pc in mine], lay), bufs[q], tail)
+    outs = [torch.full_like(d, float("nan")) for d in devs]
+    views, cnt, rr, offs, srcs = [], [], [], [], []
+    for q in range(world):
+        for pc in plan.pieces[q]:
+            views.append(outs[pc.layer][pc.lo:pc.hi])
+            cnt.append(pc.hi - pc.lo)
+            rr.append(rs[pc.layer])
+            offs.append(pc.offset)
+            srcs.append(q)
+    if views:
+        lay = PackedLayout(tuple(cnt), tuple(rr), tuple(offs), S)
+        start = sum(len(plan.pieces[q]) for q in range(world // 2))
+        engine.unpack_multi(engine.SegmentTable(views, lay, sources=srcs), [b.data_ptr() for b in bufs],
+                            start_seg=start)
+    torch.cuda.synchronize()
+    for h, r, o in zip(hosts, rs, outs):
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+    tails = [b[plan.payload_cap:plan.payload_cap + 8 * plan.max_pieces].view(torch.float64).cpu().tolist()
+             for b in bufs]
+    for h, s in zip(hosts, plan.combine_sumsq(tails)):
+        ref = O.l2_norm(h) ** 2
+        assert abs(s - ref) <= 1e-9 * max(ref, 1e-30)
