@@ -555,3 +555,28 @@ def test_measured_profile_shape(adt):
     wire = sum(14 + n * r for n, r in zip(counts, [1, 2, 3, 4]))
     assert prof["weight_stream"]["raw_bytes"] == raw and prof["weight_stream"]["wire_bytes"] == wire
     assert prof["weight_stream"]["ratio"] == pytest.approx(raw / wire)
+
+
+def test_trace_csv_byte_identical_across_reruns(adt):
+    """test_acceptance.py:206-215: a rerun writes a byte-identical trace.csv
+    (fixed-order reductions, no float atomics) — host and device AWP alike."""
+    import io
+    walk = list(O.lenet_walk(40, seed=11))
+    L = len(walk[0][1])
+    cfg = dict(threshold=-2e-3, interval=3, step_bits=8, initial_bits=8)
+
+    def run(on_device):
+        masters = [torch.from_numpy(w.copy()).cuda() for w in walk[0][1]]
+        sync = adt.WeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**cfg)), awp_on_device=on_device)
+        rows = []
+        for t in range(40):
+            for m, w in zip(masters, walk[t][1]):
+                m.copy_(torch.from_numpy(w))
+            rows += sync.step(batch=t).trace
+        rows += sync.drain_trace() if on_device else []
+        buf = io.StringIO()
+        adt.write_trace_csv(buf, rows)
+        return buf.getvalue()
+
+    a, b, c = run(False), run(False), run(True)
+    assert a == b == c and len(a.splitlines()) == 1 + 39 * L
