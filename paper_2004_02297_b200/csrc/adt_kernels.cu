@@ -469,6 +469,9 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
 #ifndef ADT_UNPACK_MIN_BLOCKS
 #define ADT_UNPACK_MIN_BLOCKS 5
 #endif
+#ifndef ADT_FIXUP_CTAS_PER_SM
+#define ADT_FIXUP_CTAS_PER_SM 4   // adt_awp_fixup grid (its CTAs exit after one load when nothing escalated)
+#endif
 #ifndef ADT_UNPACK_STCS
 #define ADT_UNPACK_STCS 2      // replica stores evict-first, direct (1) and staged (2) paths (profiles/r01_ab_layer_hint.md)
 #endif
@@ -1216,7 +1219,7 @@ int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, 
     F.gather = masters == nullptr ? 1 : 0;
     int sms = 0;
     if (sm_count_cached(&sms) != ADT_OK) return ADT_ERR_NO_DEVICE;
-    const uint32_t grid = max(1u, min(acc, static_cast<uint32_t>(4 * sms)));
+    const uint32_t grid = max(1u, min(acc, static_cast<uint32_t>(ADT_FIXUP_CTAS_PER_SM * sms)));
     adt_awp_fixup_kernel<MAXSEG><<<grid, kThreads, 0, stream>>>(F);
     return cuda_status(cudaGetLastError());
 }
