@@ -206,8 +206,10 @@ class ShardedWeightSync:
         self._gopened = []
         self._bopened = []         # p2p: peers' barrier flag arrays mapped here
         self._grecv = None         # nccl: all-to-all'd gradient slices of this rank's shard
-        if self.transport == "p2p":
-            self._init_barrier()
+        if self.transport == "p2p" and not self._init_barrier():
+            if transport == "p2p":
+                raise RuntimeError("transport='p2p': a rank could not map its peers' memory (CUDA IPC)")
+            self.transport = "nccl"              # "auto": every rank saw the same vote
         self.awp_on_device = bool(awp_on_device)
         self._dawp = None
         if self.awp_on_device:
@@ -420,22 +422,36 @@ class ShardedWeightSync:
         return list(self.plan.round_tos)
 
     # ------------------------------------------------------------- one step
-    def _init_barrier(self) -> None:
+    def _init_barrier(self) -> bool:
         """p2p: every rank's epoch-flag array, IPC-mapped into every rank, for
-        the device-side barrier (adt_peer_barrier)."""
+        the device-side barrier (adt_peer_barrier). This is the first peer
+        mapping; every rank votes on its success, so a failure on any rank
+        returns False everywhere (no rank is left waiting in a collective)."""
         self._flags = torch.zeros(self.world, dtype=torch.int32, device=self.device)
         self._bstate = torch.zeros(2, dtype=torch.int32, device=self.device)
         handle = engine.ipc_handle(self._flags)
         everyone = [None] * self.world
         self.dist.all_gather_object(everyone, handle, group=self.group)
         self._flag_ptrs = []
-        for q in range(self.world):
-            if q == self.rank:
-                self._flag_ptrs.append(self._flags.data_ptr())
-            else:
-                base = engine.ipc_open(everyone[q][0])
-                self._bopened.append(base)
-                self._flag_ptrs.append(base + everyone[q][1])
+        ok = True
+        try:
+            for q in range(self.world):
+                if q == self.rank:
+                    self._flag_ptrs.append(self._flags.data_ptr())
+                else:
+                    base = engine.ipc_open(everyone[q][0])
+                    self._bopened.append(base)
+                    self._flag_ptrs.append(base + everyone[q][1])
+        except RuntimeError:
+            ok = False
+        votes = [None] * self.world
+        self.dist.all_gather_object(votes, ok, group=self.group)
+        if all(votes):
+            return True
+        for p in self._bopened:
+            engine.ipc_close(p)
+        self._bopened, self._flag_ptrs = [], []
+        return False
 
     def _barrier(self) -> None:
         """Stream-ordered cross-rank barrier: every rank's pack is complete

@@ -83,6 +83,14 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_2004_02297_b200 as adt
         from paper_2004_02297_b200.sharded import ShardedWeightSync
+        if transport == "auto-ipcfail":           # rank 1 cannot map peer memory
+            transport = "auto"
+            if rank == 1:
+                from paper_2004_02297_b200 import _lib, engine
+
+                def refuse(handle):
+                    raise _lib.AdtError(-1, "peer mapping refused (test)")
+                engine.ipc_open = refuse
         counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
         rng = np.random.default_rng(11)
         hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
@@ -108,6 +116,9 @@ def _rank_main(rank, world, port, q, transport="p2p"):
             for m, h in zip(masters, hosts):
                 h *= np.float32(0.99)
                 m.copy_(torch.from_numpy(h))
+        if transport == "auto" and sync.transport != "nccl":
+            ok = False
+            notes.append(f"transport {sync.transport} after a failed peer mapping")
         q.put((rank, ok, notes, norms_seen, sync.round_tos))
         dist.barrier()
         dist.destroy_process_group()
@@ -115,10 +126,11 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         q.put((rank, False, [repr(e)], [], []))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "auto-ipcfail"])
 def test_sync_two_processes_one_gpu(transport):
     """transport="nccl" runs its all-gather code path over gloo here (CUDA
-    tensors; NCCL itself refuses two ranks on one device)."""
+    tensors; NCCL itself refuses two ranks on one device). "auto-ipcfail":
+    one rank's peer mapping fails -> every rank falls back to the all-gather."""
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
