@@ -60,9 +60,12 @@ class ShardPlan:
     payload_cap: int                        # bytes reserved for payloads (16-B multiple)
     max_pieces: int
     send_bytes: int                          # S_max: payload_cap + 8 * max_pieces
+    align: int = 16                          # piece offsets are multiples of this
 
     @staticmethod
-    def plan(counts: Sequence[int], round_tos: Sequence[int], world: int) -> "ShardPlan":
+    def plan(counts: Sequence[int], round_tos: Sequence[int], world: int, align: int = 16) -> "ShardPlan":
+        """align = 48 (SPLIT_ALIGN) makes every piece splittable at any 48-B
+        multiple of the send buffer (chunk_segments)."""
         counts = tuple(int(c) for c in counts)
         round_tos = tuple(int(r) for r in round_tos)
         if world < 1:
@@ -92,13 +95,13 @@ class ShardPlan:
             off, lst = 0, []
             for layer, lo, hi in per_rank[p]:
                 lst.append(Piece(layer, lo, hi, off))
-                off = align_up(off + (hi - lo) * round_tos[layer])
+                off = align_up(off + (hi - lo) * round_tos[layer], align)
             cap = max(cap, off)
             pieces.append(tuple(lst))
         max_pieces = max(1, max(len(x) for x in pieces))
-        cap = align_up(max(cap, 16))
+        cap = align_up(max(cap, 16), align)
         return ShardPlan(counts, round_tos, world, tuple(pieces), cap, max_pieces,
-                         align_up(cap + 8 * max_pieces))
+                         align_up(cap + 8 * max_pieces), align)
 
     def with_widths(self, round_tos: Sequence[int]) -> "ShardPlan":
         """The same ownership (every rank keeps its (layer, lo, hi) pieces) at
@@ -111,12 +114,12 @@ class ShardPlan:
             off, lst = 0, []
             for pc in lst0:
                 lst.append(Piece(pc.layer, pc.lo, pc.hi, off))
-                off = align_up(off + (pc.hi - pc.lo) * round_tos[pc.layer])
+                off = align_up(off + (pc.hi - pc.lo) * round_tos[pc.layer], self.align)
             cap = max(cap, off)
             pieces.append(tuple(lst))
-        cap = align_up(max(cap, 16))
+        cap = align_up(max(cap, 16), self.align)
         return ShardPlan(self.counts, round_tos, self.world, tuple(pieces), cap, self.max_pieces,
-                         align_up(cap + 8 * self.max_pieces))
+                         align_up(cap + 8 * self.max_pieces), self.align)
 
     def rank_payload_bytes(self, rank: int) -> int:
         return sum((pc.hi - pc.lo) * self.round_tos[pc.layer] for pc in self.pieces[rank])
@@ -129,6 +132,55 @@ class ShardPlan:
             for k, pc in enumerate(self.pieces[q]):
                 out[pc.layer] += float(tails[q][k])
         return out
+
+
+SPLIT_ALIGN = 48     # a multiple of 4r bytes for r = 1..4 and of 16
+
+
+@dataclass(frozen=True)
+class ChunkedGather:
+    """The nccl transport's send buffer cut into byte ranges gathered one
+    after another, so the unpack of chunk c overlaps the gather of chunk c+1.
+
+    bounds[c] .. bounds[c+1] is chunk c of every rank's send buffer (the same
+    cut on every rank; the payload split in near-equal SPLIT_ALIGN multiples,
+    the norm tail in the last chunk). Chunk c is gathered rank-major into
+    region[c] .. region[c+1] of the receive buffer. segments[c] lists the
+    parts of the pieces whose packed bytes lie in chunk c:
+    (rank, layer, lo, hi, round_to, byte offset in the receive buffer)."""
+    bounds: tuple[int, ...]
+    region: tuple[int, ...]
+    segments: tuple[tuple[tuple[int, int, int, int, int, int], ...], ...]
+
+    @staticmethod
+    def cut(plan: ShardPlan, chunks: int) -> "ChunkedGather":
+        if plan.align % SPLIT_ALIGN:
+            raise ValueError(f"chunked gather needs a plan with piece offsets aligned to {SPLIT_ALIGN} B")
+        S, cap = plan.send_bytes, plan.payload_cap
+        step = align_up(-(-cap // max(1, chunks)), SPLIT_ALIGN)
+        bounds = [0] + [c * step for c in range(1, max(1, chunks)) if c * step < cap] + [S]
+        region = [0]
+        for c in range(len(bounds) - 1):
+            region.append(region[-1] + plan.world * (bounds[c + 1] - bounds[c]))
+        segs = [[] for _ in range(len(bounds) - 1)]
+        for q in range(plan.world):
+            for pc in plan.pieces[q]:
+                r = plan.round_tos[pc.layer]
+                a, e = pc.offset, pc.offset + (pc.hi - pc.lo) * r
+                for c in range(len(bounds) - 1):
+                    b0, b1 = bounds[c], bounds[c + 1]
+                    s, t = max(a, b0), min(e, b1)
+                    if s < t:    # s - a, t - a: multiples of 4r (or the piece end)
+                        segs[c].append((q, pc.layer, pc.lo + (s - a) // r, pc.lo + (t - a) // r, r,
+                                        region[c] + q * (b1 - b0) + (s - b0)))
+        return ChunkedGather(tuple(bounds), tuple(region), tuple(tuple(x) for x in segs))
+
+    def tails(self, recv: torch.Tensor, plan: ShardPlan) -> torch.Tensor:
+        """(world, 8 * max_pieces) uint8 view of every rank's gathered norm tail."""
+        b = self.bounds[-2]
+        width = self.bounds[-1] - b
+        return recv[self.region[-2]:self.region[-1]].view(plan.world, width)[
+            :, plan.payload_cap - b:plan.payload_cap - b + 8 * plan.max_pieces]
 
 
 def peer_transport(dist, group=None) -> str:
@@ -173,13 +225,18 @@ class ShardedWeightSync:
     """
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None,
-                 transport: str = "nccl", awp_on_device: bool = False, trace_ring: int = 256):
+                 transport: str = "nccl", awp_on_device: bool = False, trace_ring: int = 256,
+                 nccl_chunks: int = 4):
         """awp_on_device (p2p transport): every rank runs the AWP decision on
         its GPU from the gathered per-piece sums (identical inputs, so
         identical decisions), pieces keep capacity offsets in the send
         buffers, and a step — pack, norm, barrier, gather-unpack, decide,
         re-pack + re-gather of escalated pieces — is device work only (one
-        CUDA graph per send slot); trace rows come back via drain_trace()."""
+        CUDA graph per send slot); trace rows come back via drain_trace().
+
+        nccl_chunks (nccl transport): the packed send buffers are gathered in
+        this many byte ranges (ChunkedGather), each unpacked as soon as it
+        lands, so the unpack overlaps the rest of the all-gather."""
         import torch.distributed as dist
         engine.require_cuda()
         if transport not in ("nccl", "p2p", "auto"):
@@ -210,6 +267,11 @@ class ShardedWeightSync:
             if transport == "p2p":
                 raise RuntimeError("transport='p2p': a rank could not map its peers' memory (CUDA IPC)")
             self.transport = "nccl"              # "auto": every rank saw the same vote
+        if nccl_chunks < 1:
+            raise ValueError("nccl_chunks must be >= 1")
+        self.nccl_chunks = int(nccl_chunks)
+        self._align = SPLIT_ALIGN if self.transport == "nccl" else 16
+        self._chunked = None
         self.awp_on_device = bool(awp_on_device)
         self._dawp = None
         if self.awp_on_device:
@@ -335,12 +397,12 @@ class ShardedWeightSync:
         if getattr(self, "_owners_fixed", False):
             self.plan = self.plan.with_widths(round_tos)
         else:
-            self.plan = ShardPlan.plan(self.counts, round_tos, self.world)
+            self.plan = ShardPlan.plan(self.counts, round_tos, self.world, self._align)
         S = self.plan.send_bytes
         if self.send is None or self.send[0].numel() < S:
             widest = [4] * len(self.counts)
             cap = max(S, (self.plan.with_widths(widest) if getattr(self, "_owners_fixed", False)
-                          else ShardPlan.plan(self.counts, widest, self.world)).send_bytes)
+                          else ShardPlan.plan(self.counts, widest, self.world, self._align)).send_bytes)
             self._alloc(cap)
         if self.transport == "p2p":
             need = self.world * 8 * self.plan.max_pieces
@@ -371,6 +433,17 @@ class ShardedWeightSync:
         self._graphs = None
         self.unpack_table = engine.SegmentTable(outs, self.unpack_layout,
                                                 sources=srcs if self.transport == "p2p" else None)
+        if self.transport == "nccl" and self.world > 1:
+            self._chunked = ChunkedGather.cut(self.plan, self.nccl_chunks)
+            self._chunk_tables = []
+            for segs in self._chunked.segments:
+                if not segs:
+                    self._chunk_tables.append(None)
+                    continue
+                lay = PackedLayout(tuple(hi - lo for _, _, lo, hi, _, _ in segs), tuple(r for *_, r, _ in segs),
+                                   tuple(off for *_, off in segs), S * self.world)
+                self._chunk_tables.append(engine.SegmentTable(
+                    [self.replicas[layer][lo:hi] for _, layer, lo, hi, _, _ in segs], lay))
 
     def _alloc(self, cap: int) -> None:
         nslots = 2 if self.transport == "p2p" else 1
@@ -473,17 +546,37 @@ class ShardedWeightSync:
         """pack shard (norm finalized into the send tail) -> exchange -> unpack."""
         S = self.plan.send_bytes
         if self.transport == "nccl":
-            send, recv = self.send[0][:S], self.recv[:S * self.world]
+            send = self.send[0][:S]
             engine.pack(self.pack_table, send, self._tail(send) if fused_norm else None)
-            if self.world > 1:
-                self.dist.all_gather_into_tensor(recv, send, group=self.group)
-            if mid_event is not None:
-                mid_event.record(torch.cuda.current_stream())
-            engine.unpack(self.unpack_table, recv)
+            self._gather_unpack(send, mid_event)
             return
         slot = self._slot
         self._slot ^= 1
         self._p2p_step(slot, fused_norm, mid_event)
+
+    def _gather_unpack(self, send: torch.Tensor, mid_event=None) -> None:
+        """nccl transport: all-gather the packed send buffers chunk by chunk
+        (every chunk's collective is queued at once, so they run back to back
+        on NCCL's stream) and unpack each chunk on this stream as soon as its
+        gather completes: the unpack of chunk c overlaps the gather of c+1.
+        mid_event (if given) is recorded once the gathers are queued."""
+        stream = torch.cuda.current_stream()
+        if self.world == 1:                      # recv is the send buffer
+            if mid_event is not None:
+                mid_event.record(stream)
+            engine.unpack(self.unpack_table, self.recv)
+            return
+        ch, recv = self._chunked, self.recv
+        works = [self.dist.all_gather_into_tensor(recv[ch.region[c]:ch.region[c + 1]],
+                                                  send[ch.bounds[c]:ch.bounds[c + 1]],
+                                                  group=self.group, async_op=True)
+                 for c in range(len(ch.bounds) - 1)]
+        if mid_event is not None:
+            mid_event.record(stream)
+        for work, table in zip(works, self._chunk_tables):
+            work.wait()                          # this stream waits for chunk c's gather
+            if table is not None:
+                engine.unpack(table, recv)
 
     def _p2p_step(self, slot: int, fused_norm: bool, mid_event=None) -> None:
         send = self.send[slot]
@@ -526,7 +619,8 @@ class ShardedWeightSync:
         self.check_barrier()
         S, base, m = self.plan.send_bytes, self.plan.payload_cap, self.plan.max_pieces
         if self.transport == "nccl":
-            g = self.recv[:S * self.world].view(self.world, S)[:, base:base + 8 * m].contiguous()
+            g = (self._chunked.tails(self.recv, self.plan) if self.world > 1
+                 else self.recv[:S].view(1, S)[:, base:base + 8 * m]).contiguous()
         else:
             g = self.tails[:self.world * 8 * m].view(self.world, 8 * m)
         tails = g.view(torch.float64).view(self.world, m).cpu().tolist()
@@ -636,7 +730,7 @@ class ShardedWeightSync:
             return SyncResult(round_tos=None)
         S = self.plan.send_bytes
         if self.transport == "nccl":
-            send, recv = self.send[0][:S], self.recv[:S * self.world]
+            send = self.send[0][:S]
         else:
             slot = self._slot
             self._slot ^= 1
@@ -645,9 +739,7 @@ class ShardedWeightSync:
         engine.reduce_sgd_pack(self._reduce_table, grads, sample_counts, lr, momentum, weight_decay, send,
                                self._tail(send))
         if self.transport == "nccl":
-            if self.world > 1:
-                self.dist.all_gather_into_tensor(recv, send, group=self.group)
-            engine.unpack(self.unpack_table, recv)
+            self._gather_unpack(send)
         else:
             self._barrier()                      # every shard is stepped and packed
             engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)

@@ -96,7 +96,11 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
         masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
         cfg = adt.PrecisionConfig(threshold=-1e-3, interval=1, step_bits=8, initial_bits=8)
-        sync = ShardedWeightSync(masters, adt.PrecisionController(len(counts), cfg), transport=transport)
+        chunks = 4
+        if transport.startswith("nccl") and transport != "nccl":   # "nccl<k>": k gather chunks
+            transport, chunks = "nccl", int(transport[4:])
+        sync = ShardedWeightSync(masters, adt.PrecisionController(len(counts), cfg), transport=transport,
+                                 nccl_chunks=chunks)
         ok, notes, norms_seen = True, [], []
         for step in range(4):
             res = sync.step(batch=step)
@@ -126,10 +130,11 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         q.put((rank, False, [repr(e)], [], []))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl", "auto-ipcfail"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "nccl1", "nccl7", "auto-ipcfail"])
 def test_sync_two_processes_one_gpu(transport):
     """transport="nccl" runs its all-gather code path over gloo here (CUDA
-    tensors; NCCL itself refuses two ranks on one device). "auto-ipcfail":
+    tensors; NCCL itself refuses two ranks on one device) in 4 chunks ("nccl1",
+    "nccl7": 1 / 7 chunks, the unpack of each overlapping the next gather). "auto-ipcfail":
     one rank's peer mapping fails -> every rank falls back to the all-gather."""
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():

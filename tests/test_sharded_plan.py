@@ -195,3 +195,60 @@ def test_gloo_alltoall_gradient_shards_match_reference_combine(world):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res)
+
+
+# ------------------------------------------- chunked all-gather (nccl transport)
+@pytest.mark.parametrize("name,world,chunks", [("lenet", 2, 4), ("resnet50", 3, 4), ("resnet50", 8, 7),
+                                               ("ragged", 2, 1), ("ragged", 4, 5), ("ragged", 5, 64)])
+def test_chunked_gather_reassembles_every_piece(name, world, chunks):
+    """Simulate the chunk-by-chunk all-gather in NumPy: every unpack segment
+    of every chunk must address exactly its piece's packed bytes in the
+    owner's send buffer, the parts must tile each piece in order, and every
+    kernel-side alignment (16-B packed offsets, 4-weight FP32 starts) holds."""
+    from paper_2004_02297_b200.sharded import SPLIT_ALIGN, ChunkedGather
+    if name == "ragged":
+        counts = [5, 4096 * 3 + 7, 1, 70000, 16, 4096 * 9 + 4095, 12345]
+    else:
+        counts = workloads.counts_of(name)
+    rs = [(i % 4) + 1 for i in range(len(counts))]
+    plan = ShardPlan.plan(counts, rs, world, SPLIT_ALIGN)
+    check_plan(plan, counts, rs)
+    assert all(pc.offset % SPLIT_ALIGN == 0 for x in plan.pieces for pc in x)
+    ch = ChunkedGather.cut(plan, chunks)
+    S = plan.send_bytes
+    assert ch.bounds[0] == 0 and ch.bounds[-1] == S and list(ch.bounds) == sorted(set(ch.bounds))
+    assert all(b % SPLIT_ALIGN == 0 for b in ch.bounds[:-1]) and ch.bounds[-2] < max(plan.payload_cap, 1)
+    assert ch.region[-1] == world * S
+    sends = [((np.arange(S, dtype=np.int64) * 7 + q * 13) % 251).astype(np.uint8) for q in range(world)]
+    recv = np.zeros(world * S, np.uint8)
+    for c in range(len(ch.bounds) - 1):                 # the chunk's rank-major all-gather
+        b0, b1 = ch.bounds[c], ch.bounds[c + 1]
+        for q in range(world):
+            recv[ch.region[c] + q * (b1 - b0):ch.region[c] + (q + 1) * (b1 - b0)] = sends[q][b0:b1]
+    parts = {}
+    for segs in ch.segments:
+        for q, layer, lo, hi, r, off in segs:
+            assert off % 16 == 0 and lo % 4 == 0 and hi > lo
+            parts.setdefault((q, layer), []).append((lo, hi, r, off))
+    for q in range(world):
+        for pc in plan.pieces[q]:
+            got = parts.pop((q, pc.layer))
+            r = plan.round_tos[pc.layer]
+            pos = pc.lo
+            for lo, hi, rr, off in got:                 # chunk order = stream order
+                assert lo == pos and rr == r
+                want = sends[q][pc.offset + (lo - pc.lo) * r:pc.offset + (hi - pc.lo) * r]
+                assert np.array_equal(recv[off:off + (hi - lo) * r], want)
+                pos = hi
+            assert pos == pc.hi
+    assert not parts
+    tails = ch.tails(torch.from_numpy(recv), plan).numpy()
+    base, m = plan.payload_cap, plan.max_pieces
+    for q in range(world):
+        assert np.array_equal(tails[q], sends[q][base:base + 8 * m])
+
+
+def test_chunked_gather_refuses_unsplittable_plan():
+    from paper_2004_02297_b200.sharded import ChunkedGather
+    with pytest.raises(ValueError):
+        ChunkedGather.cut(ShardPlan.plan([100, 200], [3, 1], 2), 4)
