@@ -14,6 +14,8 @@ import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+from hypothesis import given, settings
+from hypothesis import strategies as st
 
 from paper_2004_02297_b200 import workloads
 from paper_2004_02297_b200.sharded import ShardPlan
@@ -205,12 +207,23 @@ def test_chunked_gather_reassembles_every_piece(name, world, chunks):
     of every chunk must address exactly its piece's packed bytes in the
     owner's send buffer, the parts must tile each piece in order, and every
     kernel-side alignment (16-B packed offsets, 4-weight FP32 starts) holds."""
-    from paper_2004_02297_b200.sharded import SPLIT_ALIGN, ChunkedGather
     if name == "ragged":
         counts = [5, 4096 * 3 + 7, 1, 70000, 16, 4096 * 9 + 4095, 12345]
     else:
         counts = workloads.counts_of(name)
-    rs = [(i % 4) + 1 for i in range(len(counts))]
+    check_chunked(counts, [(i % 4) + 1 for i in range(len(counts))], world, chunks)
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.lists(st.integers(1, 40000), min_size=1, max_size=9), st.data(),
+       st.integers(1, 9), st.integers(1, 12))
+def test_chunked_gather_property(counts, data, world, chunks):
+    rs = data.draw(st.lists(st.integers(1, 4), min_size=len(counts), max_size=len(counts)))
+    check_chunked(counts, rs, world, chunks)
+
+
+def check_chunked(counts, rs, world, chunks):
+    from paper_2004_02297_b200.sharded import SPLIT_ALIGN, ChunkedGather
     plan = ShardPlan.plan(counts, rs, world, SPLIT_ALIGN)
     check_plan(plan, counts, rs)
     assert all(pc.offset % SPLIT_ALIGN == 0 for x in plan.pieces for pc in x)
