@@ -64,10 +64,24 @@ __device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb,
     return __float_as_uint(__fsub_rn(w, __fmul_rn(lr, v)));
 }
 
+#ifndef ADT_SGD_HOIST_MAX_NC
+#define ADT_SGD_HOIST_MAX_NC 4      // whole-tile gradient prefetch up to this many contributions
+#endif
+#ifndef ADT_SGD_HOIST2_MAX_NC
+#define ADT_SGD_HOIST2_MAX_NC 7     // two k-steps ahead up to this many (8: spills, no gain)
+#endif
+__host__ __device__ constexpr int sgd_hoist(int nc) {
+    return (nc >= 1 && nc <= ADT_SGD_HOIST_MAX_NC) ? kVec : (nc >= 1 && nc <= ADT_SGD_HOIST2_MAX_NC) ? 2 : 1;
+}
 #ifndef ADT_SGD_MIN_BLOCKS
 #define ADT_SGD_MIN_BLOCKS 4
 #endif
-constexpr int sgd_min_blocks(int nc) { return nc == 0 ? ADT_SGD_MIN_BLOCKS : (nc <= 2 ? 3 : 2); }
+#ifndef ADT_SGD_NC2_MIN_BLOCKS
+#define ADT_SGD_NC2_MIN_BLOCKS 2
+#endif
+constexpr int sgd_min_blocks(int nc) {
+    return nc == 0 ? ADT_SGD_MIN_BLOCKS : nc == 1 ? 3 : nc == 2 ? ADT_SGD_NC2_MIN_BLOCKS : 2;
+}
 
 template <int MAXSEG, int NC>
 __global__ void __launch_bounds__(kThreads, sgd_min_blocks(NC))
@@ -97,18 +111,30 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
             w[k] = __ldcs(wp + g0 + 32 * k);
             v[k] = __ldcs(vp + g0 + 32 * k);
         }
+        // Gradient loads are issued kH k-steps at a time ahead of their combines
+        // (the IEEE division's slow-path call keeps the compiler from hoisting
+        // the next k's loads above it on its own): the whole tile for few
+        // contributions, two k-steps for a few more, one beyond (NC loads per
+        // k-step are already in flight), within the register budget.
+        constexpr int kH = sgd_hoist(NC);
 #pragma unroll
-        for (int k = 0; k < kVec; ++k) {
-            uint4 g[NG];
+        for (int kb = 0; kb < kVec; kb += kH) {
+            uint4 g[kH][NG];
 #pragma unroll
-            for (int c = 0; c < NG; ++c) g[c] = __ldcs(gp[c] + g0 + 32 * k);
-            uint32_t gx[NG], gy[NG], gz[NG], gw[NG];
+            for (int h = 0; h < kH; ++h)
 #pragma unroll
-            for (int c = 0; c < NG; ++c) { gx[c] = g[c].x; gy[c] = g[c].y; gz[c] = g[c].z; gw[c] = g[c].w; }
-            w[k].x = sgd1(w[k].x, v[k].x, combine<NC>(gx, T), lr, mu, wd);
-            w[k].y = sgd1(w[k].y, v[k].y, combine<NC>(gy, T), lr, mu, wd);
-            w[k].z = sgd1(w[k].z, v[k].z, combine<NC>(gz, T), lr, mu, wd);
-            w[k].w = sgd1(w[k].w, v[k].w, combine<NC>(gw, T), lr, mu, wd);
+                for (int c = 0; c < NG; ++c) g[h][c] = __ldcs(gp[c] + g0 + 32 * (kb + h));
+#pragma unroll
+            for (int h = 0; h < kH; ++h) {
+                const int k = kb + h;
+                uint32_t gx[NG], gy[NG], gz[NG], gw[NG];
+#pragma unroll
+                for (int c = 0; c < NG; ++c) { gx[c] = g[h][c].x; gy[c] = g[h][c].y; gz[c] = g[h][c].z; gw[c] = g[h][c].w; }
+                w[k].x = sgd1(w[k].x, v[k].x, combine<NC>(gx, T), lr, mu, wd);
+                w[k].y = sgd1(w[k].y, v[k].y, combine<NC>(gy, T), lr, mu, wd);
+                w[k].z = sgd1(w[k].z, v[k].z, combine<NC>(gz, T), lr, mu, wd);
+                w[k].w = sgd1(w[k].w, v[k].w, combine<NC>(gw, T), lr, mu, wd);
+            }
         }
         // stores after every load: no load is ordered behind a possibly-aliasing store
 #pragma unroll
