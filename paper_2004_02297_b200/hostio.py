@@ -24,6 +24,7 @@ import torch
 
 SMALL = 1 << 20            # below this, plain torch copies
 CHUNK = 64 << 20           # staging chunk (bytes)
+THREADS = 16               # host copy threads per chunk (>= 4 MiB each)
 _init_lock = threading.Lock()   # lazy creation of the pool / staging buffers
 _use_lock = threading.Lock()    # one user of the staging buffers at a time
 _staging: dict = {}        # device index -> pinned uint8 tensor of CHUNK bytes
@@ -42,7 +43,7 @@ def _workers() -> ThreadPoolExecutor:
     if _pool is None:
         with _init_lock:
             if _pool is None:
-                _pool = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+                _pool = ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1)))
     return _pool
 
 
@@ -58,7 +59,7 @@ def _stage(device: torch.device) -> list:
 
 
 def _parallel_memmove(dst: int, src: int, nbytes: int) -> None:
-    n = max(1, min(16, nbytes >> 22))          # >= 4 MiB per thread
+    n = max(1, min(THREADS, nbytes >> 22))     # >= 4 MiB per thread
     step = -(-nbytes // n)
     futs = [_workers().submit(ctypes.memmove, dst + i * step, src + i * step, min(step, nbytes - i * step))
             for i in range(n) if i * step < nbytes]
