@@ -303,6 +303,8 @@ def main_ours(args):
     kernels_per_step = 2 + (0 if args.no_norm else 1)
     if world > 1 and getattr(sync, "transport", "") == "p2p":
         kernels_per_step += 1 + (0 if args.no_norm else 1)
+    elif world > 1:                               # nccl: one unpack per gathered chunk
+        kernels_per_step += sum(t is not None for t in sync._chunk_tables) - 1
     fused = not args.no_norm
     run_step = sync.launch if args.eager else sync.launch_graphed
 
