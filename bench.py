@@ -621,11 +621,9 @@ def run_reduce_compare(dev_masters, rs, dev, nc=8, reps=10):
 
     def unfused():
         level = [b.flat * float(b.sample_count) for b in buckets]
-        while len(level) > 1:
-            nxt = [level[i] + level[i + 1] for i in range(0, len(level) - 1, 2)]
-            if len(level) % 2:
-                nxt.append(level[-1])
-            level = nxt
+        while len(level) > 1:                     # the reference's pairwise association
+            carry = level[-1:] if len(level) % 2 else []
+            level = [a + b for a, b in zip(level[0::2], level[1::2])] + carry
         g = level[0].div_(total)
         for l, (wi, vi) in enumerate(zip(w, v)):
             gi = g[buckets[0].offsets[l]:buckets[0].offsets[l] + counts[l]]

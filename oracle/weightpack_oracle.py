@@ -240,10 +240,8 @@ def pairwise_sum(arrays):
         raise ValueError("pairwise_sum of no arrays")
     level = list(arrays)
     while len(level) > 1:
-        nxt = [level[i] + level[i + 1] for i in range(0, len(level) - 1, 2)]
-        if len(level) % 2:
-            nxt.append(level[-1])
-        level = nxt
+        carry = level[-1:] if len(level) % 2 else []
+        level = [a + b for a, b in zip(level[0::2], level[1::2])] + carry
     return level[0]
 
 
