@@ -35,3 +35,49 @@ def test_training_with_adt_awp(example):
     assert dev["final_bits"] == host["final_bits"]
     assert dev["final_loss"] == host["final_loss"] and dev["val_accuracy"] == host["val_accuracy"]
     assert dev["weight_bytes_vs_fp32"] == pytest.approx(host["weight_bytes_vs_fp32"])
+
+
+def _dp_rank(rank, world, port, q, argv):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank), ADT_EXAMPLE_BACKEND="gloo")
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "examples"))
+        import train_mlp_dp
+        q.put((rank, train_mlp_dp.main(argv)))
+    except Exception as e:  # surface child failures to the parent
+        import traceback
+        q.put((rank, {"error": repr(e), "tb": traceback.format_exc()}))
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_dp_training_over_ranks_matches_simulated_workers(example, transport):
+    """examples/train_mlp_dp.py with 2 ranks (sharing this GPU through gloo)
+    runs the same training as examples/train_mlp_adt.py with 2 simulated
+    workers: same widths chosen, same losses and accuracy (the sharded master
+    update is bit-exact; only the norms' partial-sum grouping differs), and
+    both ranks end with bit-identical replicas."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    argv = ["--steps", "60", "--interval", "5", "--transport", transport]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dp_rank, args=(r, 2, port, q, argv)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out in res:
+        assert "error" not in out, (rank, out.get("tb"))
+        assert out["replicas_identical"] and out["transport"] == transport
+    dp = res[0][1]
+    sim = example.main(["--steps", "60", "--workers", "2", "--interval", "5"])
+    assert dp["final_bits"] == sim["final_bits"] and max(dp["final_bits"]) > 8
+    assert dp["first_loss"] == sim["first_loss"]
+    assert dp["final_loss"] == pytest.approx(sim["final_loss"], rel=1e-6)
+    assert dp["val_accuracy"] == pytest.approx(sim["val_accuracy"], abs=1e-3)
+    assert dp["weight_bytes_vs_fp32"] == pytest.approx(sim["weight_bytes_vs_fp32"])
