@@ -55,6 +55,8 @@ def main(argv=None):
     ap.add_argument("--interval", type=int, default=50)
     ap.add_argument("--threshold", type=float, default=1e-3)
     ap.add_argument("--transport", default="auto", choices=("auto", "p2p", "nccl"))
+    ap.add_argument("--awp-on-device", action="store_true",
+                    help="AWP decision on every GPU (p2p transport): a step has no host round trip")
     ap.add_argument("--seed", type=int, default=7)
     args = ap.parse_args(argv)
     backend = os.environ.get("ADT_EXAMPLE_BACKEND", "nccl")
@@ -82,7 +84,7 @@ def _train(args, rank, world, dev):
     L = len(masters)
     sched = adt.PrecisionController(L, adt.PrecisionConfig(threshold=args.threshold, interval=args.interval,
                                                            step_bits=8, initial_bits=8))
-    sync = ShardedWeightSync(masters, sched, transport=args.transport)
+    sync = ShardedWeightSync(masters, sched, transport=args.transport, awp_on_device=args.awp_on_device)
     sync.step(batch=0)                                   # replicas of W0 at the initial widths
     reps = [r.view(s) for r, s in zip(sync.replicas, shapes)]
     bucket = GradBucket(shapes, dev)
@@ -97,8 +99,9 @@ def _train(args, rank, world, dev):
         counts = [len(p) for p in parts]
         bucket.sample_count = counts[rank]
         res = sync.update(bucket, counts, args.lr, 0.9, 5e-4, batch=b)
-        wire += sum(n * r for n, r in zip(sync.counts, res.round_tos))
-        raw += 4 * sum(sync.counts)
+        if not sync.awp_on_device:                       # widths the next batch's weights travel at
+            wire += sum(n * r for n, r in zip(sync.counts, res.round_tos))
+            raw += 4 * sum(sync.counts)
         # biases: every rank's bias gradients, combined in rank order (as the
         # single-process example sums its workers'), then a plain momentum step
         flat_gb = torch.cat([g.reshape(-1) for g in gb])
@@ -111,6 +114,10 @@ def _train(args, rank, world, dev):
             vel_b[i].mul_(0.9).add_(g)
             biases[i].sub_(args.lr * vel_b[i])
         losses.append(loss)
+    if sync.awp_on_device:                               # trace rows -> widths (refreshes sched)
+        trace = sync.drain_trace()
+        wire = sum(sync.counts[layer] * ((bits + 7) // 8) for _, layer, _, _, _, bits in trace)
+        raw = 4 * sum(sync.counts[layer] for _, layer, *_ in trace)
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     # every rank must hold bit-identical replicas and biases
@@ -129,6 +136,7 @@ def _train(args, rank, world, dev):
             h = torch.relu(h) if i + 1 < L else h
         acc = float((h.argmax(1) == ye).float().mean())
     out = {"steps": args.steps, "ranks": world, "transport": sync.transport,
+           "mode": "awp_on_device" if sync.awp_on_device else "awp",
            "first_loss": float(np.mean([float(e[0]) for e in every_loss])),
            "final_loss": float(np.mean([float(e[-1]) for e in every_loss])),
            "val_accuracy": acc, "final_bits": [sched.current_bits(i) for i in range(L)],

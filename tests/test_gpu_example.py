@@ -49,7 +49,7 @@ def _dp_rank(rank, world, port, q, argv):
         q.put((rank, {"error": repr(e), "tb": traceback.format_exc()}))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "p2p-device-awp"])
 def test_dp_training_over_ranks_matches_simulated_workers(example, transport):
     """examples/train_mlp_dp.py with 2 ranks (sharing this GPU through gloo)
     runs the same training as examples/train_mlp_adt.py with 2 simulated
@@ -62,7 +62,9 @@ def test_dp_training_over_ranks_matches_simulated_workers(example, transport):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    argv = ["--steps", "60", "--interval", "5", "--transport", transport]
+    argv = ["--steps", "60", "--interval", "5", "--transport", transport.split("-")[0]]
+    if transport.endswith("device-awp"):
+        argv.append("--awp-on-device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_dp_rank, args=(r, 2, port, q, argv)) for r in range(2)]
@@ -73,7 +75,7 @@ def test_dp_training_over_ranks_matches_simulated_workers(example, transport):
         p.join(timeout=60)
     for rank, out in res:
         assert "error" not in out, (rank, out.get("tb"))
-        assert out["replicas_identical"] and out["transport"] == transport
+        assert out["replicas_identical"] and out["transport"] == transport.split("-")[0]
     dp = res[0][1]
     sim = example.main(["--steps", "60", "--workers", "2", "--interval", "5"])
     assert dp["final_bits"] == sim["final_bits"] and max(dp["final_bits"]) > 8
