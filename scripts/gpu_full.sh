@@ -25,3 +25,4 @@ python scripts/step_overhead.py > $OUT/step_overhead.txt 2>&1
 timeout 600 python -m paper_2004_02297_b200 bench-codec --sizes 1000000,67108864 --workers 1,2,8 > $OUT/bench_codec.txt 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_awp_device.csv python scripts/awp_device_profile.py resnet50 > /dev/null 2>&1
 timeout 300 python examples/train_mlp_adt.py > $OUT/train_awp.json 2>&1; timeout 300 python examples/train_mlp_adt.py --awp-on-device > $OUT/train_awp_device.json 2>&1; timeout 300 python examples/train_mlp_adt.py --fp32 > $OUT/train_fp32.json 2>&1
+bash scripts/reduce_sweep.sh $OUT/sweep > $OUT/reduce_sweep.md 2>&1

@@ -31,3 +31,4 @@ tail -n 1 $O/bench_n2_gloo_p2p.log > profiles/r01_bench_n2_gloo_p2p.json
 python scripts/results_table.py $O > profiles/r01_results_table.md
 cp $O/step_overhead.txt profiles/r01_step_overhead.txt
 cat $O/train_fp32.json $O/train_awp.json $O/train_awp_device.json > profiles/r01_train_example.jsonl
+cp $O/reduce_sweep.md profiles/r01_reduce_sweep.md
