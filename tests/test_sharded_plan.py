@@ -64,13 +64,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, counts, rs, q):
+def _worker(rank, world, port, counts, rs, q, chunks=0):
+    """chunks = 0: one all_gather_into_tensor of the send buffers; chunks > 0:
+    the nccl transport's chunked gather (ChunkedGather, async collectives
+    queued at once, completed in order)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import c_oracle as C
+    from paper_2004_02297_b200.sharded import SPLIT_ALIGN, ChunkedGather
     rng = np.random.default_rng(1)
     layers = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
-    plan = ShardPlan.plan(counts, rs, world)
+    plan = ShardPlan.plan(counts, rs, world, SPLIT_ALIGN if chunks else 16)
     S = plan.send_bytes
     send = np.zeros(S, np.uint8)
     sums = np.zeros(plan.max_pieces, np.float64)
@@ -81,21 +85,29 @@ def _worker(rank, world, port, counts, rs, q):
         sums[k] = C.sumsq(seg)
     send[plan.payload_cap:plan.payload_cap + 8 * plan.max_pieces] = sums.view(np.uint8)
     recv = torch.zeros(S * world, dtype=torch.uint8)
-    dist.all_gather_into_tensor(recv, torch.from_numpy(send))
-    recv = recv.numpy()
+    if chunks:
+        ch = ChunkedGather.cut(plan, chunks)
+        src = torch.from_numpy(send)
+        works = [dist.all_gather_into_tensor(recv[ch.region[c]:ch.region[c + 1]], src[ch.bounds[c]:ch.bounds[c + 1]],
+                                             async_op=True) for c in range(len(ch.bounds) - 1)]
+        for w_ in works:
+            w_.wait()
+        tails = [t.view(np.float64) for t in ch.tails(recv, plan).numpy()]
+        recv = recv.numpy()
+        located = [(layer, lo, recv[off:off + (hi - lo) * r].tobytes())
+                   for segs in ch.segments for _, layer, lo, hi, r, off in segs]
+    else:
+        dist.all_gather_into_tensor(recv, torch.from_numpy(send))
+        recv = recv.numpy()
+        tails = [recv[qq * S + plan.payload_cap: qq * S + plan.payload_cap + 8 * plan.max_pieces].view(np.float64)
+                 for qq in range(world)]
+        located = [(pc.layer, pc.lo, recv[qq * S + pc.offset:qq * S + pc.offset + (pc.hi - pc.lo) * rs[pc.layer]]
+                    .tobytes()) for qq in range(world) for pc in plan.pieces[qq]]
     ok = True
     # reassemble every layer's payload from the gathered pieces
     for layer, (w, r) in enumerate(zip(layers, rs)):
-        parts = []
-        for qq in range(world):
-            for pc in plan.pieces[qq]:
-                if pc.layer == layer:
-                    base = qq * S + pc.offset
-                    parts.append((pc.lo, recv[base:base + (pc.hi - pc.lo) * r].tobytes()))
-        got = b"".join(p for _, p in sorted(parts))
+        got = b"".join(p for _, p in sorted((lo, p) for lyr, lo, p in located if lyr == layer))
         ok &= got == C.pack(w, r)
-    tails = [recv[qq * S + plan.payload_cap: qq * S + plan.payload_cap + 8 * plan.max_pieces].view(np.float64)
-             for qq in range(world)]
     norms = [math.sqrt(v) for v in plan.combine_sumsq(tails)]
     for w, n in zip(layers, norms):
         ref = math.sqrt(C.sumsq(w))
@@ -104,13 +116,14 @@ def _worker(rank, world, port, counts, rs, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_packed_allgather_reassembles_reference_payloads():
+@pytest.mark.parametrize("chunks", [0, 3])
+def test_gloo_world2_packed_allgather_reassembles_reference_payloads(chunks):
     counts = [20 * 25, 50 * 20 * 25, 3 * TILE + 17, 10 * 500, 9 * TILE]
     rs = [1, 2, 3, 4, 2]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, counts, rs, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, counts, rs, q, chunks)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
