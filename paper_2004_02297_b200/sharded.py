@@ -211,8 +211,9 @@ class ShardedWeightSync:
     `masters[l]` are this rank's FP32 master tensors (full layer shape; only
     this rank's shard ranges are read), `replicas[l]` receive every weight.
 
-    transport = "auto": "p2p" when all ranks' GPUs are peers on one node,
-        else "nccl" (peer_transport).
+    transport = "auto" (default): "p2p" when all ranks' GPUs are peers on one
+        node and every rank can map the others' memory, else "nccl"
+        (peer_transport, then a vote on the first peer mapping).
     transport = "nccl": pack -> ncclAllGather(uint8) of the packed send
         buffers -> unpack the gathered stream.
     transport = "p2p": every rank's send buffer is mapped into every other
@@ -225,7 +226,7 @@ class ShardedWeightSync:
     """
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None,
-                 transport: str = "nccl", awp_on_device: bool = False, trace_ring: int = 256,
+                 transport: str = "auto", awp_on_device: bool = False, trace_ring: int = 256,
                  nccl_chunks: int = 4):
         """awp_on_device (p2p transport): every rank runs the AWP decision on
         its GPU from the gathered per-piece sums (identical inputs, so
