@@ -215,7 +215,7 @@ def run_cpu_baseline(counts, rs, per_layer, reps):
     return {"value": byts / best / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"first min(n, {per_layer}) weights of each layer ({sum(w.size for w in sample)} weights), "
                       f"pack_parallel({threads} threads)+unpack+l2_norm, best of {reps}",
-            "seconds_per_pass": best}
+            "seconds_per_pass": best, "host_cpus": os.cpu_count()}
 
 
 def main_reference(args):
@@ -241,7 +241,8 @@ def main_reference(args):
         "config": {"workload": workload_name(args, bits), "sample_weights": sum(w.size for w in sample)},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"first min(n, {per_layer}) weights of each layer per step"},
+                         "sample": f"first min(n, {per_layer}) weights of each layer per step",
+                         "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
