@@ -92,6 +92,8 @@ def _rank_main(rank, world, port, q, transport="p2p"):
                     raise _lib.AdtError(-1, "peer mapping refused (test)")
                 engine.ipc_open = refuse
         counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
+        if transport.endswith("-tiny"):          # one tile in all: the other ranks own nothing
+            transport, counts = transport[:-5], [37]
         rng = np.random.default_rng(11)
         hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
         masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
@@ -130,7 +132,7 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         q.put((rank, False, [repr(e)], [], []))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl", "nccl1", "nccl7", "auto-ipcfail"])
+@pytest.mark.parametrize("transport", ["p2p", "nccl", "nccl1", "nccl7", "auto-ipcfail", "p2p-tiny", "nccl-tiny"])
 def test_sync_two_processes_one_gpu(transport):
     """transport="nccl" runs its all-gather code path over gloo here (CUDA
     tensors; NCCL itself refuses two ranks on one device) in 4 chunks ("nccl1",
