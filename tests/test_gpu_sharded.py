@@ -242,6 +242,8 @@ def _device_awp_main(rank, world, port, q, graphed):
         import paper_2004_02297_b200 as adt
         from paper_2004_02297_b200.sharded import ShardedWeightSync
         counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
+        if world == 3:                           # some rank owns no piece
+            counts = [37, 4100]
         L = len(counts)
         rng = np.random.default_rng(11)
         hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
@@ -283,7 +285,7 @@ def _device_awp_main(rank, world, port, q, graphed):
         q.put((rank, False, [traceback.format_exc()], []))
 
 
-@pytest.mark.parametrize("graphed,world", [(False, 2), (True, 2), (True, 8)])
+@pytest.mark.parametrize("graphed,world", [(False, 2), (True, 2), (True, 8), (True, 3)])
 def test_p2p_device_awp_processes_sharing_one_gpu(graphed, world):
     """ShardedWeightSync(p2p, awp_on_device): the decision on every rank's
     GPU from the gathered per-piece sums, escalated pieces re-packed by their
