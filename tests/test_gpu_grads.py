@@ -291,8 +291,6 @@ def _device_rank_main(rank, world, port, q):
         from paper_2004_02297_b200.grads import GradBucket
         from paper_2004_02297_b200.sharded import ShardedWeightSync
         counts = [20 * 25, 50 * 20 * 25, 3 * 4096 + 17, 10 * 500, 9 * 4096]
-        if transport.endswith("-tiny"):          # two tiles in all: some rank owns nothing
-            transport, counts = transport[:-5], [37, 4100]
         L = len(counts)
         hp = (0.05, 0.9, 5e-4)
         sc = [48, 80, 17][:world]
