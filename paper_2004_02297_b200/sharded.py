@@ -12,7 +12,8 @@ unpacks the whole stream into its full FP32 replica. Two transports:
   (adt_peer_barrier) each rank's unpack kernel reads its peers' payloads over
   NVLink directly (adt_unpack_multi) — the gather and the unpack are one pass;
 * nccl: `all_gather_into_tensor` (ncclAllGather, uint8) into a receive
-  buffer, then the unpack (the fallback when the GPUs are not peers).
+  buffer in chunks, each chunk unpacked as soon as it lands (ChunkedGather;
+  the fallback when the GPUs are not peers).
 
 Send buffer of rank p (S_max bytes, identical size on every rank):
     [piece payloads, 16-B aligned | pad | float64 sum of squares per piece]
@@ -215,7 +216,8 @@ class ShardedWeightSync:
         node and every rank can map the others' memory, else "nccl"
         (peer_transport, then a vote on the first peer mapping).
     transport = "nccl": pack -> ncclAllGather(uint8) of the packed send
-        buffers -> unpack the gathered stream.
+        buffers, `nccl_chunks` byte ranges queued at once -> unpack of each
+        range as it completes.
     transport = "p2p": every rank's send buffer is mapped into every other
         rank with CUDA IPC; after one stream-ordered barrier each rank unpacks
         straight out of its peers' send buffers over NVLink
