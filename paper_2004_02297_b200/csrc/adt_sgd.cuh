@@ -70,11 +70,15 @@ __device__ __forceinline__ uint32_t sgd1(uint32_t wb, uint32_t &vb, uint32_t gb,
 #ifndef ADT_SGD_HOIST2_MAX_NC
 #define ADT_SGD_HOIST2_MAX_NC 7     // two k-steps ahead up to this many (8: spills, no gain)
 #endif
+#ifndef ADT_SGD_HOIST_NC0
+#define ADT_SGD_HOIST_NC0 1         // pre-averaged gradient: k-steps of g loads ahead
+#endif
 __host__ __device__ constexpr int sgd_hoist(int nc) {
-    return (nc >= 1 && nc <= ADT_SGD_HOIST_MAX_NC) ? kVec : (nc >= 1 && nc <= ADT_SGD_HOIST2_MAX_NC) ? 2 : 1;
+    return nc == 0 ? ADT_SGD_HOIST_NC0
+                   : (nc <= ADT_SGD_HOIST_MAX_NC) ? kVec : (nc <= ADT_SGD_HOIST2_MAX_NC) ? 2 : 1;
 }
 #ifndef ADT_SGD_MIN_BLOCKS
-#define ADT_SGD_MIN_BLOCKS 4
+#define ADT_SGD_MIN_BLOCKS 3          // pre-averaged gradient: 3 CTAs/SM (213 us vs 217 us at 4 on AlexNet, r01_ab_reduce_prefetch.md)
 #endif
 #ifndef ADT_SGD_NC2_MIN_BLOCKS
 #define ADT_SGD_NC2_MIN_BLOCKS 2
