@@ -45,6 +45,18 @@ def layout_records(layout: PackedLayout, bias_bytes=None) -> list[WireRecord]:
     return out
 
 
+def return_gradients_bytes(parameter_count: int) -> WireRecord:
+    """transfer.py:177-197, 247-251 (TransferBoundary.return_gradients ->
+    send_to_host): one worker's gradients go back uncompressed — raw = wire =
+    4 bytes per parameter, recorded for all layers at once (layer "all" -> -1
+    here). On the B200 path these bytes are what the fused gradient reduce
+    reads from every rank's bucket (peer loads or the all-to-all)."""
+    if parameter_count < 0:
+        raise ValueError(f"parameter_count must be >= 0, got {parameter_count}")
+    nbytes = 4 * int(parameter_count)
+    return WireRecord(-1, nbytes, nbytes, 0, 0)
+
+
 def weight_stream_ratio(records) -> float:
     """raw / wire over the weight stream (transfer.py:119-132, TransferLedger.weight_stream_bytes/ratio)."""
     raw = sum(r.weight_raw_bytes for r in records)

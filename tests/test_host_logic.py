@@ -188,3 +188,8 @@ def test_wire_accounting_matches_reference_ledger_arithmetic():
     assert [r.weight_wire_bytes for r in recs] == [14 + 10_000, 14 + 10_000, 14 + 20_000]
     with pytest.raises(ValueError):
         transfer.weight_stream_ratio([])
+    # gradients return uncompressed (transfer.py:247-251): 4 bytes per parameter
+    g = transfer.return_gradients_bytes(1234)
+    assert (g.raw_bytes, g.wire_bytes, g.weight_raw_bytes, g.weight_wire_bytes) == (4936, 4936, 0, 0)
+    with pytest.raises(ValueError):
+        transfer.return_gradients_bytes(-1)
