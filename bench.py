@@ -433,6 +433,15 @@ def main_ours(args):
     fp32_gather = None
     if world > 1:
         fp32_gather = run_fp32_allgather(counts, world, dev) if backend == "nccl" else None
+    exchange = None
+    if world > 1:
+        # SURVEY §8e report: packed bytes each rank receives from its peers per
+        # step and the bus rate over the whole step (nccl-tests busbw convention)
+        payload = sum(n * r for n, r in zip(counts, rs))
+        per_rank = payload - sync.plan.rank_payload_bytes(rank)
+        exchange = {"packed_bytes_total": payload, "bytes_received_per_rank": per_rank,
+                    "busbw_GBps": payload * (world - 1) / world / (ms * 1e-3) / 1e9,
+                    "pack_ms": pk, "gather_unpack_ms": up, "sync_ms": ms}
     dp = None
     if world > 1 and not args.no_reduce:
         dp = run_dp_update(sync, counts, world, dev, backend)
@@ -456,7 +465,7 @@ def main_ours(args):
                        "transport": getattr(sync, "transport", "local")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
-            "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather,
+            "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather, "exchange": exchange,
             "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red, "dp_update": dp, "awp_step": awp,
         }
         print(json.dumps(line), flush=True)
