@@ -43,7 +43,7 @@ from .precision import (  # noqa: F401
     write_trace_csv,
 )
 from .sync import NonFiniteParameters, SyncResult, WeightSync  # noqa: F401
-from .grads import GradBucket, GradientSet  # noqa: F401
+from .grads import GradBucket, GradientSet, ShapeMismatch  # noqa: F401
 from .sharded import ShardedWeightSync, ShardPlan  # noqa: F401
 
 __version__ = "0.1.0"

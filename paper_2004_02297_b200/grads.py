@@ -39,6 +39,11 @@ def bucket_offsets(counts: Sequence[int]) -> tuple[tuple[int, ...], int]:
     return tuple(offs), pos
 
 
+
+class ShapeMismatch(ValueError):
+    """net.py:16-17 — gradients that do not fit the network (wrong layer
+    count or layer size, or no contributions at all)."""
+
 class GradBucket:
     """One worker's weight gradients in a flat CUDA float32 buffer.
 
@@ -63,10 +68,10 @@ class GradBucket:
     def load(self, grads: Sequence[torch.Tensor]) -> "GradBucket":
         """Copy per-layer gradient tensors in (stream-ordered)."""
         if len(grads) != len(self.views):
-            raise ValueError(f"{len(grads)} gradients for a {len(self.views)}-layer bucket")
+            raise ShapeMismatch(f"{len(grads)} gradients for a {len(self.views)}-layer bucket")
         for v, g in zip(self.views, grads):
             if g.numel() != v.numel():
-                raise ValueError(f"gradient has {g.numel()} entries, layer has {v.numel()}")
+                raise ShapeMismatch(f"gradient has {g.numel()} entries, layer has {v.numel()}")
             v.copy_(g.reshape(v.shape))
         return self
 

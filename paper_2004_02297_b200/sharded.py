@@ -40,7 +40,7 @@ from . import engine
 from ._lib import TILE_WEIGHTS
 from .layout import align_up
 from .precision import FixedPrecision, PrecisionController
-from .grads import GradBucket, bucket_offsets, shard_ranges
+from .grads import GradBucket, ShapeMismatch, bucket_offsets, shard_ranges
 from .sync import NonFiniteParameters, SyncResult
 
 
@@ -701,7 +701,7 @@ class ShardedWeightSync:
         if len(sample_counts) != self.world:
             raise ValueError("one sample count per rank")
         if list(bucket.counts) != list(self.counts):
-            raise ValueError("gradient bucket layer sizes differ from the masters")
+            raise ShapeMismatch("gradient bucket layer sizes differ from the masters")
         if self.velocities is None:
             self.velocities = [torch.zeros_like(m) for m in self.masters]
         self._owners_fixed = True

@@ -359,7 +359,8 @@ class WeightSync:
         The replicas then hold batch b+1's weights.
         """
         if len(grads) != len(self.masters):
-            raise ValueError("one gradient tensor per layer")
+            from .grads import ShapeMismatch
+            raise ShapeMismatch("one gradient tensor per layer")
         self._ensure_velocities()
         g = [t.detach().reshape(-1) for t in grads]
         if self.awp_on_device:
@@ -383,8 +384,10 @@ class WeightSync:
         with the reference's sample-count weighting and pairwise_sum tree,
         steps W and v, packs W' and fuses its norm; then the replicas are
         unpacked and AWP observes, exactly as update()."""
-        from .grads import GradBucket
-        if not 1 <= len(contributions) <= 16:
+        from .grads import GradBucket, ShapeMismatch
+        if not contributions:
+            raise ShapeMismatch("no gradient contributions")          # net.py:218-219
+        if len(contributions) > 16:
             raise ValueError("gather_and_update takes 1..16 gradient contributions")
         buckets = []
         for i, c in enumerate(contributions):
@@ -392,14 +395,14 @@ class WeightSync:
                 b = c
             else:
                 if len(c.weight_grads) != len(self.masters):
-                    raise ValueError(f"contribution has {len(c.weight_grads)} layers, network has {len(self.masters)}")
+                    raise ShapeMismatch(f"contribution has {len(c.weight_grads)} layers, network has {len(self.masters)}")
                 stage = self._grad_stage.get(i)
                 if stage is None:
                     stage = self._grad_stage[i] = GradBucket(self.counts, self.device)
                 b = stage.load(c.weight_grads)
                 b.sample_count = int(c.sample_count)
             if list(b.counts) != list(self.counts):
-                raise ValueError("gradient bucket layer sizes differ from the masters")
+                raise ShapeMismatch("gradient bucket layer sizes differ from the masters")
             buckets.append(b)
         self._ensure_velocities()
         key = self.capacity_layout if self.awp_on_device else self.layout

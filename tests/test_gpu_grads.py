@@ -154,6 +154,23 @@ def test_gather_and_update_nonfinite_raises(adt):
         sync.gather_and_update([GradientSet([g], [], 64), GradientSet([g], [], 64)], lr=1.0)
 
 
+def test_gather_and_update_shape_mismatch(adt):
+    """net.py:218-229: no contributions, or gradients that do not fit the
+    layers, raise ShapeMismatch (a ValueError) before any device work."""
+    from paper_2004_02297_b200.grads import GradBucket, GradientSet
+    sync = adt.WeightSync([torch.ones(100, device="cuda"), torch.ones(30, device="cuda")])
+    with pytest.raises(adt.ShapeMismatch):
+        sync.gather_and_update([], lr=0.1)
+    with pytest.raises(adt.ShapeMismatch):
+        sync.gather_and_update([GradientSet([torch.ones(100, device="cuda")], [], 4)], lr=0.1)
+    with pytest.raises(adt.ShapeMismatch):
+        sync.gather_and_update([GradientSet([torch.ones(100, device="cuda"), torch.ones(31, device="cuda")], [], 4)],
+                               lr=0.1)
+    with pytest.raises(adt.ShapeMismatch):
+        sync.gather_and_update([GradBucket([100, 31])], lr=0.1)
+    assert issubclass(adt.ShapeMismatch, ValueError)
+
+
 # ------------------------------------------------ two ranks sharing cuda:0
 def _free_port():
     s = socket.socket()
