@@ -116,3 +116,39 @@ def test_virtual_ranks_shard_pack_gather_unpack(adt, counts, world, seed):
     for h, s in zip(hosts, plan.combine_sumsq(tails)):
         ref = O.l2_norm(h) ** 2
         assert abs(s - ref) <= 1e-9 * max(ref, 1e-30)
+
+
+# ------------------------------------------- full BASELINE sizes, size-independent laws
+def _mask(r):
+    return torch.tensor(O.keep_mask(r) - (1 << 32) if O.keep_mask(r) >= 1 << 31 else O.keep_mask(r),
+                        dtype=torch.int32, device="cuda")
+
+
+@pytest.mark.parametrize("name,bits", [("alexnet", None), ("vgg16", 8), ("vgg16", 24), ("resnet50", 8),
+                                       ("1b", 16), ("1b", 24)])
+def test_full_size_sets_obey_the_laws(adt, name, bits):
+    """BASELINE.json's configs at full size, checked on the device (the
+    oracle is too slow there): for arbitrary 32-bit words the replicas equal
+    words & truncation_mask(r) (mask law), re-packing the replicas gives the
+    same bytes (idempotence), the payload is Σ n·r (size law); for N(0, 0.1²)
+    weights the fused norms match a float64 torch reduction to 1e-9."""
+    from paper_2004_02297_b200 import workloads
+    counts = workloads.counts_of(name)
+    rs = [(b + 7) // 8 for b in workloads.default_bits(name, bits)]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    words = [torch.randint(-(1 << 31), 1 << 31, (n,), dtype=torch.int32, device="cuda", generator=g) for n in counts]
+    packed, layout, _ = adt.pack_many([w.view(torch.float32) for w in words], rs)
+    assert sum(hi - lo for lo, hi in (layout.span(i) for i in range(len(counts)))) == sum(
+        n * r for n, r in zip(counts, rs))
+    reps = adt.unpack_many(packed, layout)
+    for w, rep, r in zip(words, reps, rs):
+        assert torch.equal(rep.view(torch.int32), w & _mask(r))
+    again, _, _ = adt.pack_many(reps, rs)
+    for i in range(len(counts)):                 # payload spans (the 16-B alignment pad is not data)
+        lo, hi = layout.span(i)
+        assert torch.equal(again[lo:hi], packed[lo:hi]), i
+    del words, reps, again, packed
+    vals = [torch.randn(n, device="cuda", generator=g) * 0.1 for n in counts]
+    _, _, ss = adt.pack_many(vals, rs, with_norms=True)
+    ref = torch.stack([v.double().square().sum() for v in vals])
+    assert torch.allclose(ss, ref, rtol=1e-9, atol=0.0)
