@@ -371,3 +371,48 @@ def test_sharded_update_p2p_device_awp_two_processes():
     for rank, ok, notes, _ in res:
         assert ok, (rank, notes)
     assert res[0][3] == res[1][3] and len(res[0][3]) > 0
+
+
+@pytest.mark.parametrize("nc", [1, 3, 8])
+def test_reduce_sgd_pack_full_alexnet_matches_per_op_torch(adt, nc):
+    """The fused gradient combine + SGD + pack at the full AlexNet set against
+    the same arithmetic as separate float32 torch ops (each op rounds once;
+    no alpha= forms, which may contract to FMA): masters, velocities and packed
+    payloads bit-identical — the full-size counterpart of the golden tests."""
+    from paper_2004_02297_b200 import engine, workloads
+    from paper_2004_02297_b200.grads import GradBucket
+    from paper_2004_02297_b200.layout import PackedLayout
+    counts = workloads.counts_of("alexnet")
+    rs = [(b + 7) // 8 for b in workloads.default_bits("alexnet")]
+    lr, mu, wd = 0.01, 0.9, 5e-4
+    g = torch.Generator(device="cuda").manual_seed(11)
+    w = [torch.randn(n, device="cuda", generator=g) * 0.1 for n in counts]
+    v = [torch.randn(n, device="cuda", generator=g) * 0.01 for n in counts]
+    w_ref, v_ref = [x.clone() for x in w], [x.clone() for x in v]
+    sc = [int(x) for x in torch.randint(1, 200, (nc,), generator=torch.Generator().manual_seed(nc))]
+    buckets = []
+    for _ in range(nc):
+        b = GradBucket(counts)
+        b.flat.normal_(generator=g).mul_(0.05)
+        buckets.append(b)
+    lay = PackedLayout.plan(counts, rs)
+    packed = torch.empty(lay.nbytes, dtype=torch.uint8, device="cuda")
+    table = engine.ReduceSgdTable(w, v, [buckets[0].byte_offset(l) for l in range(len(counts))], lay)
+    engine.reduce_sgd_pack(table, [b.flat.data_ptr() for b in buckets], sc, lr, mu, wd, packed)
+    total = torch.tensor(float(sum(sc)), dtype=torch.float32, device="cuda")
+    for l in range(len(counts)):
+        level = [b.views[l].reshape(-1) * torch.tensor(float(c), device="cuda") for b, c in zip(buckets, sc)]
+        while len(level) > 1:                     # net.py pairwise_sum association
+            carry = level[-1:] if len(level) % 2 else []
+            level = [a + b for a, b in zip(level[0::2], level[1::2])] + carry
+        gl = level[0] / total
+        gl = gl + wd * w_ref[l]
+        v_ref[l] = v_ref[l] * mu + gl
+        w_ref[l] = w_ref[l] - lr * v_ref[l]
+    ref_packed, ref_lay, _ = adt.pack_many(w_ref, rs)
+    for l in range(len(counts)):
+        assert torch.equal(w[l].view(torch.int32), w_ref[l].view(torch.int32)), l
+        assert torch.equal(v[l].view(torch.int32), v_ref[l].view(torch.int32)), l
+        lo, hi = lay.span(l)
+        rlo, rhi = ref_lay.span(l)
+        assert torch.equal(packed[lo:hi], ref_packed[rlo:rhi]), l
