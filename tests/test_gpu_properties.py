@@ -152,3 +152,48 @@ def test_full_size_sets_obey_the_laws(adt, name, bits):
     _, _, ss = adt.pack_many(vals, rs, with_norms=True)
     ref = torch.stack([v.double().square().sum() for v in vals])
     assert torch.allclose(ss, ref, rtol=1e-9, atol=0.0)
+
+
+@pytest.mark.parametrize("name,world", [("alexnet", 8), ("resnet50", 8), ("vgg16", 3)])
+def test_full_size_virtual_ranks_gather_unpack(adt, name, world):
+    """The sharded path at full size with every rank's send buffer on this
+    GPU: each virtual rank packs its ShardPlan pieces with the norm tail
+    fused, the rotated multi-source gather-unpack rebuilds every replica as
+    words & mask, and the rank-order combine of the tails gives the layer
+    norms (float64 torch reduction, 1e-9)."""
+    from paper_2004_02297_b200 import engine, workloads
+    from paper_2004_02297_b200.layout import PackedLayout
+    from paper_2004_02297_b200.sharded import ShardPlan
+    counts = workloads.counts_of(name)
+    rs = [(b + 7) // 8 for b in workloads.default_bits(name)]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    devs = [torch.randn(n, device="cuda", generator=g) * 0.1 for n in counts]
+    plan = ShardPlan.plan(counts, rs, world)
+    S = plan.send_bytes
+    bufs = [torch.zeros(S, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    tails = []
+    for q in range(world):
+        mine = plan.pieces[q]
+        tail = bufs[q][plan.payload_cap:plan.payload_cap + 8 * plan.max_pieces].view(torch.float64)
+        tails.append(tail)
+        if mine:
+            lay = PackedLayout(tuple(pc.hi - pc.lo for pc in mine), tuple(rs[pc.layer] for pc in mine),
+                               tuple(pc.offset for pc in mine), plan.payload_cap)
+            engine.pack(engine.SegmentTable([devs[pc.layer][pc.lo:pc.hi] for pc in mine], lay), bufs[q], tail)
+    outs = [torch.full_like(d, float("nan")) for d in devs]
+    views, cnt, rr, offs, srcs = [], [], [], [], []
+    for q in range(world):
+        for pc in plan.pieces[q]:
+            views.append(outs[pc.layer][pc.lo:pc.hi])
+            cnt.append(pc.hi - pc.lo)
+            rr.append(rs[pc.layer])
+            offs.append(pc.offset)
+            srcs.append(q)
+    start = sum(len(plan.pieces[q]) for q in range(world // 2))
+    engine.unpack_multi(engine.SegmentTable(views, PackedLayout(tuple(cnt), tuple(rr), tuple(offs), S), sources=srcs),
+                        [b.data_ptr() for b in bufs], start_seg=start)
+    for d, o, r in zip(devs, outs, rs):
+        assert torch.equal(o.view(torch.int32), d.view(torch.int32) & _mask(r))
+    sums = plan.combine_sumsq([t.cpu().tolist() for t in tails])
+    ref = torch.stack([d.double().square().sum() for d in devs]).cpu()
+    assert torch.allclose(torch.tensor(sums, dtype=torch.float64), ref, rtol=1e-9, atol=0.0)
