@@ -791,38 +791,48 @@ def run_e2e_sharded(args, sync, counts, rs, dev, backend):
 
 def run_e2e_weightsync(args, dev_masters, rs, dev):
     """WeightSync from pinned host FP32 masters: per step H2D of the masters,
-    pack (norm fused) + unpack on device, D2H of the L float64 sums."""
+    pack (norm fused) + unpack on device, D2H of the L float64 sums. The
+    masters live in one flat buffer (layers at 16-B aligned offsets, as a
+    flat parameter store keeps them), so the step's H2D is one copy rather
+    than one per layer (161 for ResNet-50)."""
     import torch
     import paper_2004_02297_b200 as adt
+    from paper_2004_02297_b200.grads import bucket_offsets
     from paper_2004_02297_b200.precision import FixedPrecision
-    host = [m.cpu().pin_memory() for m in dev_masters]
-    masters = [torch.empty_like(m) for m in dev_masters]
+    counts = [m.numel() for m in dev_masters]
+    offs, total = bucket_offsets(counts)
+    flat_host = torch.zeros(max(total, 4), dtype=torch.float32).pin_memory()
+    flat_dev = torch.empty_like(flat_host, device=dev)
+    for o, n, m in zip(offs, counts, dev_masters):
+        flat_host[o:o + n].copy_(m.reshape(-1).cpu())
+    masters = [flat_dev[o:o + n] for o, n in zip(offs, counts)]
 
     class Fixed(FixedPrecision):
         def round_tos(self):
             return list(rs)
 
     sync = adt.WeightSync(masters, Fixed(len(masters), 32))
-    h2d = sum(h.numel() * 4 for h in host)
+    h2d = flat_host.numel() * 4
     d2h = 8 * len(masters)
 
     def one():
-        for m, h in zip(masters, host):
-            m.copy_(h, non_blocking=True)
+        flat_dev.copy_(flat_host, non_blocking=True)
         sync.launch_graphed(fused_norm=True)   # the step's CUDA graph (as WeightSync.step)
         sync.read_norms()                      # D2H of the L float64 sums + host sync
 
     for _ in range(3):
         one()
     torch.cuda.synchronize()
+    steps = max(args.e2e_steps, 20)            # the host link is noisy: >= 20 steps
     t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
+    for _ in range(steps):
         one()
     torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / args.e2e_steps
+    dt = (time.perf_counter() - t0) / steps
     byts = sync.layout.roundtrip_bytes()
     return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": dt * 1e3, "note": "WeightSync from pinned host FP32 masters; wall clock"}
+            "ms_per_step": dt * 1e3, "steps": steps,
+            "note": "WeightSync from pinned host FP32 masters (one flat buffer, one H2D per step); wall clock"}
 
 
 if __name__ == "__main__":
