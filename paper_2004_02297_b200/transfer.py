@@ -103,12 +103,12 @@ def measured_profile(sync, bias_bytes=None) -> dict:
     host_packed = torch.empty(lay.nbytes, dtype=torch.uint8, pin_memory=True)
     host_packed.copy_(sync.packed[:lay.nbytes])
     dev_packed = torch.empty(lay.nbytes, dtype=torch.uint8, device=sync.device)
-    host_fp32 = [m.cpu().pin_memory() for m in sync.masters]
-    dev_fp32 = [torch.empty_like(m) for m in sync.masters]
+    # FP32 side as one contiguous pinned buffer, like the packed stream (one copy each)
+    host_fp32 = torch.cat([m.reshape(-1) for m in sync.masters]).cpu().pin_memory()
+    dev_fp32 = torch.empty_like(host_fp32, device=sync.device)
 
     def raw_h2d():
-        for d, h in zip(dev_fp32, host_fp32):
-            d.copy_(h, non_blocking=True)
+        dev_fp32.copy_(host_fp32, non_blocking=True)
 
     def packed_h2d():
         dev_packed.copy_(host_packed, non_blocking=True)
