@@ -282,6 +282,16 @@ def main_ours(args):
     g = torch.Generator(device=dev)
     g.manual_seed(0)
     masters = [torch.randn(n, generator=g, device=dev) * 0.1 for n in counts]
+    flat_masters = None
+    if world > 1:
+        # one flat master store (layers at 16-B aligned offsets, the gradient
+        # bucket layout): each rank's owned pieces are then one contiguous range
+        from paper_2004_02297_b200.grads import bucket_offsets
+        offs, total = bucket_offsets(counts)
+        flat_masters = torch.zeros(max(total, 4), device=dev)
+        for o, m in zip(offs, masters):
+            flat_masters[o:o + m.numel()].copy_(m)
+        masters = [flat_masters[o:o + n] for o, n in zip(offs, counts)]
     replicas = [torch.empty_like(m) for m in masters]
 
     class Fixed(FixedPrecision):
@@ -416,7 +426,7 @@ def main_ours(args):
         e2e = run_e2e_weightsync(args, masters, rs, dev)
         e2e_dropin = run_e2e(args, masters, rs, dev)
     elif not args.no_e2e and world > 1:
-        e2e = run_e2e_sharded(args, sync, counts, rs, dev, backend)
+        e2e = run_e2e_sharded(args, sync, counts, rs, dev, backend, flat_masters)
 
     h2d = None
     if not args.no_h2d and world == 1:
@@ -749,24 +759,24 @@ def run_e2e(args, dev_masters, rs, dev):
             "note": "drop-in per-layer pack_vectorized + unpack + l2_norm on host NumPy arrays; wall clock"}
 
 
-def run_e2e_sharded(args, sync, counts, rs, dev, backend):
+def run_e2e_sharded(args, sync, counts, rs, dev, backend, flat_masters):
     """N > 1 end to end through ShardedWeightSync: every step each rank copies
-    the FP32 master pieces it owns from pinned host memory (the paper's CPU
-    masters, sharded), runs the step (pack with the norm, exchange,
-    gather-unpack of every replica) and reads the per-layer norms back (the
-    AWP input). Wall time per step, max over ranks; value = the whole job's
-    algorithmic bytes per step / time, as the device-timed value."""
+    the FP32 master range it owns from pinned host memory (the paper's CPU
+    masters, sharded; one contiguous copy of its slice of the flat master
+    store), runs the step (pack with the norm, exchange, gather-unpack of
+    every replica) and reads the per-layer norms back (the AWP input). Wall
+    time per step, max over ranks; value = the whole job's algorithmic bytes
+    per step / time, as the device-timed value."""
     import torch
     import torch.distributed as dist
-    mine = sync.plan.pieces[sync.rank]
-    views = [sync.masters[pc.layer][pc.lo:pc.hi] for pc in mine]
-    host = [v.cpu().pin_memory() for v in views]
-    h2d = sum(h.numel() * 4 for h in host)
+    b0, b1 = sync.grad_ranges[sync.rank]       # this rank's pieces, contiguous in the flat store
+    dev_slice = flat_masters[b0:b1]
+    host = dev_slice.cpu().pin_memory()
+    h2d = host.numel() * 4
     world = sync.world
 
     def one():
-        for v, h in zip(views, host):
-            v.copy_(h, non_blocking=True)
+        dev_slice.copy_(host, non_blocking=True)
         sync.launch_graphed(True)
         sync._norms()                      # D2H of the gathered norm tails + host sync
 
