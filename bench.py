@@ -186,66 +186,146 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- reference (CPU)
-def cpu_reference_step(sample, rs, threads):
-    """One step of the reference CPU path on `sample` (list of float32 arrays):
-    pack_parallel + unpack + l2_norm per layer (weightpack codec.py:156-197,
-    precision.py:25-28, as restated in oracle/weightpack_oracle.py)."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+L2_BYTES_B200 = 126 << 20          # for the config text only; the flush decision reads the device
+
+
+def reference_package():
+    """The UNMODIFIED reference package `weightpack`, pip-installed into
+    baseline/_ref by __graft_entry__.build() (git-ignored, shipped to the GPU
+    box with the snapshot). None when it is absent (then the oracle port of the
+    same calls, oracle/weightpack_oracle.py, stands in and says so)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "weightpack")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import weightpack
+    return weightpack
+
+
+def reference_step(wp, layers, rs, workers=1):
+    """One step of the reference's own CPU path, the calls its training loop
+    makes per batch (training.py:209-213 pack every layer once with
+    codec.pack_vectorized, :214-225 unpack every block once per worker,
+    :246-250 l2_norm of every layer; codec.py:149-153, 183-197,
+    precision.py:25-28)."""
+    if wp is not None:
+        blocks = [wp.pack_vectorized(w, r) for w, r in zip(layers, rs)]
+        for _ in range(workers):
+            for b in blocks:
+                wp.unpack(b)
+        for w in layers:
+            wp.l2_norm(w)
+        return
     from oracle import weightpack_oracle as O
-    for w, r in zip(sample, rs):
-        p = O.pack_parallel(w, r, threads)
-        O.unpack(p, w.size, r)
+    payloads = [O.pack_vectorized(w, r) for w, r in zip(layers, rs)]
+    for _ in range(workers):
+        for p, w, r in zip(payloads, layers, rs):
+            O.unpack(p, w.size, r)
+    for w in layers:
         O.l2_norm(w)
 
 
-def cpu_sample(counts, per_layer):
+def host_weights(counts, limit=None):
+    """The bench inputs, generated on the host so both arms see identical bits:
+    N(0, 0.1²) float32 per layer from np.random.default_rng(0) (net.py:98).
+    limit: keep only the first `limit` weights of each layer (a bounded sample)."""
     import numpy as np
     rng = np.random.default_rng(0)
-    return [rng.standard_normal(min(n, per_layer), dtype=np.float32) * np.float32(0.1) for n in counts]
+    out = []
+    for n in counts:
+        w = rng.standard_normal(n, dtype=np.float32)
+        w *= np.float32(0.1)
+        out.append(w if limit is None or n <= limit else np.ascontiguousarray(w[:limit]))
+    return out
 
 
-def run_cpu_baseline(counts, rs, per_layer, min_reps=2, budget_s=10.0):
-    """The oracle port of the reference's path on this host, on a bounded
-    sample of the workload: passes are repeated until `budget_s` of CPU work
-    (at least `min_reps`); the best pass is reported."""
-    sample = cpu_sample(counts, per_layer)
-    threads = len(os.sched_getaffinity(0))
-    byts = 2 * sum((4 + r) * w.size for w, r in zip(sample, rs))
-    best, spent, reps = float("inf"), 0.0, 0
-    while reps < min_reps or spent < budget_s:
+FULL_REFERENCE_WEIGHTS = 1 << 28   # above this the reference CPU path runs on a per-layer sample
+
+
+def reference_sample(counts):
+    """(per-layer limit or None, text): the whole workload unless it is too big
+    for a CPU pass of a few seconds (the 1B set)."""
+    if sum(counts) <= FULL_REFERENCE_WEIGHTS:
+        return None, f"the whole workload ({sum(counts)} weights)"
+    lim = 1 << 22
+    return lim, f"first min(n, {lim}) weights of each layer ({sum(min(n, lim) for n in counts)} weights)"
+
+
+def reference_kind(wp):
+    return ("reference", "weightpack 0.1.0 from baseline/_ref: codec.pack_vectorized + codec.unpack + "
+            "precision.l2_norm per layer (training.py:209-254)") if wp is not None else \
+           ("port", "oracle/weightpack_oracle.py port of pack_vectorized + unpack + l2_norm "
+            "(baseline/_ref missing)")
+
+
+def reference_threads():
+    """Host threads the reference path may use: NumPy's codec ops are
+    single-threaded; OpenBLAS's ddot (l2_norm) uses up to the affinity count."""
+    return len(os.sched_getaffinity(0))
+
+
+def run_cpu_baseline(counts, rs, budget_s=10.0, min_reps=2):
+    """cpu_baseline of our arm: the same reference step the reference arm
+    times, on the same inputs, repeated until `budget_s` of CPU work (at least
+    `min_reps` passes); value = algorithmic bytes / mean pass time."""
+    wp = reference_package()
+    lim, sample = reference_sample(counts)
+    layers = host_weights(counts, lim)
+    byts = 2 * sum((4 + r) * w.size for w, r in zip(layers, rs))
+    times = []
+    while len(times) < min_reps or sum(times) < budget_s:
         t0 = time.perf_counter()
-        cpu_reference_step(sample, rs, threads)
-        dt = time.perf_counter() - t0
-        best, spent, reps = min(best, dt), spent + dt, reps + 1
-    return {"value": byts / best / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first min(n, {per_layer}) weights of each layer ({sum(w.size for w in sample)} weights), "
-                      f"pack_parallel({threads} threads)+unpack+l2_norm, best of {reps} passes ({spent:.1f} s)",
-            "seconds_per_pass": best, "host_cpus": os.cpu_count()}
+        reference_step(wp, layers, rs)
+        times.append(time.perf_counter() - t0)
+    kind, what = reference_kind(wp)
+    mean = sum(times) / len(times)
+    return {"value": byts / mean / 1e9, "unit": UNIT, "cores": reference_threads(), "kind": kind,
+            "sample": f"{sample}; {what}; mean of {len(times)} passes ({sum(times):.1f} s)",
+            "seconds_per_pass": mean, "host_cpus": os.cpu_count()}
+
+
+def bench_config(args, counts, bits, rs, world=1, transport=None):
+    """`config` of the JSON line — identical in both arms for the same flags."""
+    flush = args.l2 == "flush" or (args.l2 == "auto" and 4 * sum(counts) < 3 * L2_BYTES_B200 // 2)
+    return {"workload": workload_name(args, bits), "weights": sum(counts), "layers": len(counts),
+            "widths_bits": list(bits),
+            "packed_payload_bytes": sum(n * r for n, r in zip(counts, rs)),
+            "algorithmic_bytes_per_step": (1 + world) * sum((4 + r) * n for n, r in zip(counts, rs)),
+            "data_seed": 0,
+            "l2": ("GPU arm: L2 flushed before every timed step (read of a 2x L2 buffer outside the events)"
+                   if flush else "inputs larger than L2: FP32 masters > 1.5x the 126 MB L2 "
+                                 "(master + packed + replica several x L2); no flush"),
+            "parallelism": f"dp{world}" if world > 1 else "single"}
 
 
 def main_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))    # N workers: one pack, N unpacks (training.py:214-225)
     counts, bits, rs = workload(args)
-    per_layer = 1 << 18
-    sample = cpu_sample(counts, per_layer)
-    threads = len(os.sched_getaffinity(0))
-    byts = 2 * sum((4 + r) * w.size for w, r in zip(sample, rs))
+    wp = reference_package()
+    lim, sample = reference_sample(counts)
+    layers = host_weights(counts, lim)
+    byts = (1 + world) * sum((4 + r) * w.size for w, r in zip(layers, rs))
     for _ in range(args.warmup):
-        cpu_reference_step(sample, rs, threads)
+        reference_step(wp, layers, rs, world)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cpu_reference_step(sample, rs, threads)
+        reference_step(wp, layers, rs, world)
     dt = (time.perf_counter() - t0) / args.steps
     value = byts / dt / 1e9
+    kind, what = reference_kind(wp)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic N(0,0.1^2) float32, seed 0",
-        "config": {"workload": workload_name(args, bits), "sample_weights": sum(w.size for w in sample)},
+        "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic N(0,0.1^2) float32 from np.random.default_rng(0), host arrays",
+        "config": bench_config(args, counts, bits, rs, world=world),
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"first min(n, {per_layer}) weights of each layer per step",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": reference_threads(), "kind": kind,
+                         "sample": f"{sample}; {what}; each step one pass" + (f" with {world} worker unpacks" if world > 1 else ""),
                          "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -279,9 +359,9 @@ def main_ours(args):
 
     counts, bits, rs = workload(args)
     L = len(counts)
-    g = torch.Generator(device=dev)
-    g.manual_seed(0)
-    masters = [torch.randn(n, generator=g, device=dev) * 0.1 for n in counts]
+    host = host_weights(counts)                    # identical bits to the reference arm's inputs
+    masters = [torch.from_numpy(h).to(dev) for h in host]
+    del host
     flat_masters = None
     if world > 1:
         # one flat master store (layers at 16-B aligned offsets, the gradient
@@ -421,9 +501,10 @@ def main_ours(args):
                     "pack_GBps": pack_bytes / (pk * 1e-3) / 1e9, "unpack_GBps": unpack_bytes / (up * 1e-3) / 1e9}
 
     # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
-    e2e = e2e_dropin = None
+    e2e = e2e_dropin = e2e_fp32_h2d = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e_weightsync(args, masters, rs, dev)
+        e2e_fp32_h2d = run_e2e_weightsync(args, masters, rs, dev)
+        e2e = run_e2e_host_master(args, host_weights(counts), rs, dev)
         e2e_dropin = run_e2e(args, masters, rs, dev)
     elif not args.no_e2e and world > 1:
         e2e = run_e2e_sharded(args, sync, counts, rs, dev, backend, flat_masters)
@@ -458,22 +539,18 @@ def main_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_baseline(counts, rs, per_layer=1 << 24)
+        cpu = run_cpu_baseline(counts, rs)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic N(0,0.1^2) float32 generated on device, seed 0",
-            "config": {"workload": workload_name(args, bits), "weights": sum(counts), "layers": L,
-                       "packed_payload_bytes": sum(n * r for n, r in zip(counts, rs)),
-                       "algorithmic_bytes_per_step": total_bytes,
-                       "l2": (f"flushed before every timed step (read of a {2 * l2 >> 20} MB buffer outside the "
-                              "events; each step timed by its own events)") if flush else
-                             "FP32 masters > 1.5x L2 (working set master + packed + replica several x L2); no flush",
-                       "fused_norm": True, "parallelism": f"dp{world}" if world > 1 else "single",
-                       "transport": getattr(sync, "transport", "local")},
+            "dtype": "u8", "data": "synthetic N(0,0.1^2) float32 from np.random.default_rng(0), copied to the device",
+            "config": bench_config(args, counts, bits, rs, world=world),
+            "setup": {"fused_norm": not args.no_norm, "transport": getattr(sync, "transport", "local"),
+                      "l2_flushed": flush, "graphed": not args.eager},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dropin": e2e_dropin,
+            "e2e_device_pack": e2e_fp32_h2d,
             "gpu_launches": kernels_per_step * K, "clocks": clocks.summary(),
             "sync_ms_per_iter": ms, "host_to_device": h2d, "fp32_allgather": fp32_gather, "exchange": exchange,
             "fused_sgd_pack": sgd, "fused_reduce_sgd_pack": red, "dp_update": dp, "awp_step": awp,
@@ -798,6 +875,49 @@ def run_e2e_sharded(args, sync, counts, rs, dev, backend, flat_masters):
     return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(t[1].item()),
             "d2h_bytes_per_step": 8 * world * sync.plan.max_pieces * world, "ms_per_step": dt * 1e3,
             "note": "ShardedWeightSync from pinned host FP32 master shards; wall clock, max over ranks"}
+
+
+def run_e2e_host_master(args, host, rs, dev, steps=20):
+    """The paper's CPU-master setting end to end through the public API
+    (hostsync.HostWeightSync): per step the FP32 masters in
+    host memory are packed on the host cores with their norms fused
+    (adt_pack_host, AVX-512), the packed stream crosses PCIe in copies that
+    start while later units are still being packed, and the GPU unpacks it
+    into the replicas; the step ends when the replicas are complete (stream
+    sync). The norms (the AWP input) come out of the host pass: nothing is
+    read back from the device. Wall clock per step."""
+    import torch
+    import paper_2004_02297_b200 as adt
+    from paper_2004_02297_b200.hostsync import host_threads
+    from paper_2004_02297_b200.precision import FixedPrecision
+
+    class Fixed(FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    sync = adt.HostWeightSync(host, Fixed(len(host), 32), device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        sync.launch(fused_norm=True)
+        stream.synchronize()
+
+    for _ in range(3):
+        one()
+    steps = max(args.e2e_steps, steps)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    # the same host arrays as one raw FP32 pinned copy would move: the baseline
+    n = sum(h.size for h in host)
+    byts = 2 * sum((4 + r) * h.size for h, r in zip(host, rs))
+    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": sync.h2d_bytes, "d2h_bytes_per_step": 0,
+            "ms_per_step": dt * 1e3, "steps": steps, "host_threads": host_threads(),
+            "raw_fp32_bytes": 4 * n,
+            "note": "HostWeightSync: host FP32 masters -> adt_pack_host (all host cores, norms fused) -> packed "
+                    "H2D overlapped with the packing -> adt_unpack; wall clock; norms computed on the host, "
+                    "so no device->host read"}
 
 
 def run_e2e_weightsync(args, dev_masters, rs, dev):

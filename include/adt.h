@@ -14,7 +14,13 @@
  *   - every call is stream-ordered on `stream` (a cudaStream_t passed as void*;
  *     NULL = legacy default stream) and returns an int status: 0 = ADT_OK,
  *     negative = error (see adt_strerror); the library never aborts;
- *   - thread-safe: no mutable globals besides a per-device attribute cache.
+ *   - thread-safe: no mutable globals besides a per-device attribute cache
+ *     (and the host packer's worker pool, see adt_pack_host);
+ *   - peer-abort guard: entry points that read other ranks' memory take
+ *     `const uint32_t *abort` (device memory, or NULL = unguarded). It is the
+ *     `state + 1` word of adt_peer_barrier: when it is nonzero at kernel start
+ *     the kernel does no work, so after a barrier timeout no stale or
+ *     half-written peer bytes reach a replica, a master or the AWP state.
  *
  * Packed layout (codec.py:76-107): layer l's payload is
  * count_l * round_to_l bytes at byte `offset` of the packed buffer; weight i of
@@ -32,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 9
+#define ADT_ABI_VERSION 10
 
 /* status codes */
 #define ADT_OK 0
@@ -144,12 +150,12 @@ int adt_unpack_multi(const adt_segment *segs, int nseg, const uint8_t *const *so
  * owner's NVLink port in lockstep. Results do not depend on either option's
  * scheduling. */
 int adt_unpack_multi_ex(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
-                        const uint8_t *widths, int start_seg, void *stream);
+                        const uint8_t *widths, int start_seg, const uint32_t *abort, void *stream);
 
 /* dst[q*bytes .. (q+1)*bytes) = sources[q][offset .. offset+bytes) for q < nsrc
  * (small peer reads, e.g. every rank's norm tail). */
 int adt_copy_multi(uint8_t *dst, const uint8_t *const *sources, int nsrc, uint64_t offset, uint64_t bytes,
-                   void *stream);
+                   const uint32_t *abort, void *stream);
 
 /*
  * Stream-ordered barrier over peer memory (replaces the NCCL all-reduce of a
@@ -158,11 +164,14 @@ int adt_copy_multi(uint8_t *dst, const uint8_t *const *sources, int nsrc, uint64
  * training.py:214-225). flags[q] = rank q's array of nranks uint32 epochs,
  * mapped into this process (adt_ipc_open) — flags[rank] is local; all start
  * at 0. state = 2 local uint32: [0] this rank's epoch counter (start 0),
- * [1] 0, or the epoch whose wait timed out after max_polls polls (the kernel
- * then returns instead of hanging; callers check it on their next sync).
- * Every rank must issue the same sequence of barriers. Graph-capturable.
+ * [1] 0, or the epoch whose wait timed out after timeout_ns nanoseconds of
+ * device time (the kernel then returns instead of hanging). state + 1 is the
+ * abort word of the guarded entry points queued behind the barrier; once it
+ * is set, later barriers return at once. Callers poll it (e.g. a D2H copy
+ * after every step) and raise. Every rank must issue the same sequence of
+ * barriers. Graph-capturable.
  */
-int adt_peer_barrier(uint32_t *const *flags, int nranks, int rank, uint32_t *state, uint64_t max_polls,
+int adt_peer_barrier(uint32_t *const *flags, int nranks, int rank, uint32_t *state, uint64_t timeout_ns,
                      void *stream);
 
 /* CUDA IPC plumbing for adt_unpack_multi (thin wrappers over cudaIpc*):
@@ -211,7 +220,7 @@ int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum
 int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *const *grads,
                         const int64_t *sample_counts, int ncontrib, float lr, float momentum,
                         float weight_decay, uint8_t *packed, double *seg_sumsq, double *partials,
-                        void *stream);
+                        const uint32_t *abort, void *stream);
 
 /*
  * Device-resident AWP step (single-device WeightSync(awp_on_device=True)).
@@ -283,9 +292,10 @@ int adt_sgd_pack_dyn(const adt_sgd_segment *segs, int nseg, float lr, float mome
 int adt_reduce_sgd_pack_dyn(const adt_grad_segment *segs, int nseg, const float *const *grads,
                             const int64_t *sample_counts, int ncontrib, float lr, float momentum,
                             float weight_decay, uint8_t *packed, double *partials, const uint8_t *widths,
-                            void *stream);
+                            const uint32_t *abort, void *stream);
 /* One AWP observation of every layer from the finalized sums of squares. */
-int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg, void *stream);
+int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg,
+                    const uint32_t *abort, void *stream);
 /* Re-pack + re-unpack, at widths_new, of the layers listed in `escalated` (as written by
  * adt_awp_observe); masters[l] and replicas[l] share count / offset (capacity layout,
  * round_to 4). */
@@ -303,14 +313,50 @@ int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int n
  *   adt_awp_fixup_gather: re-unpack the escalated pieces of every rank from their (re-packed)
  *                         send buffers, at widths_new (per piece). */
 int adt_unpack_multi_dyn(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
-                         const uint8_t *widths, void *stream);
+                         const uint8_t *widths, const uint32_t *abort, void *stream);
 int adt_awp_combine(const double *tails, int npieces_total, const int32_t *piece_layer, int nlayers,
-                    double *seg_sumsq, void *stream);
+                    double *seg_sumsq, const uint32_t *abort, void *stream);
 int adt_awp_fixup_pieces(const adt_segment *masters, const adt_segment *replicas, int nseg, const int32_t *seg_layer,
-                         uint8_t *packed, const int32_t *escalated, const uint8_t *widths_new, void *stream);
+                         uint8_t *packed, const int32_t *escalated, const uint8_t *widths_new, const uint32_t *abort,
+                         void *stream);
 int adt_awp_fixup_gather(const adt_segment *replicas, int nseg, const int32_t *seg_layer,
                          const uint8_t *const *sources, int nsrc, const int32_t *escalated,
-                         const uint8_t *widths_new, void *stream);
+                         const uint8_t *widths_new, const uint32_t *abort, void *stream);
+
+/*
+ * Host (CPU) pack: the paper's Bitpack stage for CPU-resident master weights
+ * (PAPER.md:219-229, 259-268, 351-452). Same bytes as adt_pack / codec.pack
+ * (codec.py:116-180) and, with seg_sumsq != NULL, the float64 sum of squares
+ * of every layer (precision.py:25-28) fused into the same read. segs[l].weights
+ * are HOST pointers (4-B aligned), `packed` is host memory (pinned for DMA).
+ * Runs on `threads` host threads (<= 0: all of the process's CPU affinity) —
+ * a persistent worker pool owned by the library (created on first use;
+ * concurrent calls queue). Work is cut into fixed 64K-weight units, so bytes
+ * and sums never depend on the thread count. AVX-512 VBMI when the CPU has
+ * it (adt_host_simd() == 512), else a scalar loop. Synchronous.
+ */
+int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *seg_sumsq, int threads);
+
+/*
+ * The CPU-master transfer, pipelined: adt_pack_host of host_segs into the
+ * pinned staging buffer host_packed; while the host threads pack, the calling
+ * thread queues cudaMemcpyAsync (on `stream`) of every finished run of the
+ * packed stream (>= min_copy_bytes, 0 = 1 MiB) into dev_packed, so the PCIe
+ * DMA overlaps the packing; then adt_unpack of dev_segs (device replicas, the
+ * same counts / offsets / round_to, payloads in increasing offset order) from
+ * dev_packed. Only Σ n·r (+ pad) bytes cross the link instead of 4n.
+ * Returns once the host work is done and the copies + unpack are queued: the
+ * caller must not rewrite host_packed before `stream` has passed this point.
+ * seg_sumsq (host memory) receives the per-layer sums of squares.
+ */
+int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
+                       uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
+                       uint64_t min_copy_bytes, void *stream);
+
+/* Host threads adt_pack_host uses at most (the process's CPU affinity). */
+int adt_host_threads(int *n);
+/* 512 when the host packer runs its AVX-512 VBMI path, 0 for the scalar path. */
+int adt_host_simd(void);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

@@ -44,6 +44,7 @@ from .precision import (  # noqa: F401
 )
 from .sync import NonFiniteParameters, SyncResult, WeightSync  # noqa: F401
 from .grads import GradBucket, GradientSet, ShapeMismatch  # noqa: F401
-from .sharded import ShardedWeightSync, ShardPlan  # noqa: F401
+from .sharded import PeerTimeout, ShardedWeightSync, ShardPlan  # noqa: F401
+from .hostsync import HostWeightSync, pack_host  # noqa: F401
 
 __version__ = "0.1.0"

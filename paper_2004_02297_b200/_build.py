@@ -16,11 +16,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libadt.so")
-SOURCES = [os.path.join(PKG, "csrc", "adt_kernels.cu")]
+SOURCES = [os.path.join(PKG, "csrc", "adt_kernels.cu"), os.path.join(PKG, "csrc", "adt_host.cpp")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # No --use_fast_math: subnormals and NaN payloads travel through the byte path
 # untouched, and the float64 norm must not flush (SURVEY.md §7 hard part 6).
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-pthread", "-shared", "-lpthread",
               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 
 

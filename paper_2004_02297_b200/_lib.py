@@ -23,7 +23,7 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 9
+ABI_VERSION = 10
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
@@ -31,7 +31,8 @@ EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", 
            "adt_unpack", "adt_unpack_multi", "adt_unpack_multi_ex", "adt_copy_multi", "adt_peer_barrier", "adt_ipc_handle_bytes", "adt_ipc_get_handle",
            "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn", "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn",
            "adt_awp_observe", "adt_awp_fixup", "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces",
-           "adt_awp_fixup_gather", "adt_device_sm_count")
+           "adt_awp_fixup_gather", "adt_device_sm_count", "adt_pack_host", "adt_host_to_device", "adt_host_threads",
+           "adt_host_simd")
 
 
 class Segment(ctypes.Structure):
@@ -148,11 +149,12 @@ def load() -> ctypes.CDLL:
         lib.adt_unpack.restype = ctypes.c_int
         lib.adt_unpack.argtypes = [seg_p, ctypes.c_int, vp, vp]
         lib.adt_unpack_multi_ex.restype = ctypes.c_int
-        lib.adt_unpack_multi_ex.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp, ctypes.c_int, vp]
+        lib.adt_unpack_multi_ex.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp, ctypes.c_int, vp,
+                                            vp]
         lib.adt_unpack_multi.restype = ctypes.c_int
         lib.adt_unpack_multi.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp]
         lib.adt_copy_multi.restype = ctypes.c_int
-        lib.adt_copy_multi.argtypes = [vp, P(ctypes.c_void_p), ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp]
+        lib.adt_copy_multi.argtypes = [vp, P(ctypes.c_void_p), ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp, vp]
         lib.adt_peer_barrier.restype = ctypes.c_int
         lib.adt_peer_barrier.argtypes = [P(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, vp, ctypes.c_uint64, vp]
         lib.adt_ipc_handle_bytes.restype = ctypes.c_int
@@ -169,7 +171,7 @@ def load() -> ctypes.CDLL:
         lib.adt_reduce_sgd_pack.restype = ctypes.c_int
         lib.adt_reduce_sgd_pack.argtypes = [P(GradSegment), ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int64),
                                             ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
-                                            vp, vp, vp, vp]
+                                            vp, vp, vp, vp, vp]
         lib.adt_pack_dyn.restype = ctypes.c_int
         lib.adt_pack_dyn.argtypes = [seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack_dyn.restype = ctypes.c_int
@@ -180,24 +182,33 @@ def load() -> ctypes.CDLL:
         lib.adt_reduce_sgd_pack_dyn.restype = ctypes.c_int
         lib.adt_reduce_sgd_pack_dyn.argtypes = [P(GradSegment), ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int64),
                                                 ctypes.c_int, ctypes.c_float, ctypes.c_float, ctypes.c_float,
-                                                vp, vp, vp, vp]
+                                                vp, vp, vp, vp, vp]
         lib.adt_awp_observe.restype = ctypes.c_int
-        lib.adt_awp_observe.argtypes = [vp, P(AwpDevice), P(AwpConfig), vp]
+        lib.adt_awp_observe.argtypes = [vp, P(AwpDevice), P(AwpConfig), vp, vp]
         lib.adt_awp_fixup.restype = ctypes.c_int
         lib.adt_awp_fixup.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, vp, vp]
         lib.adt_unpack_multi_dyn.restype = ctypes.c_int
-        lib.adt_unpack_multi_dyn.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp, vp]
+        lib.adt_unpack_multi_dyn.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_void_p), ctypes.c_int, vp, vp, vp]
         lib.adt_awp_combine.restype = ctypes.c_int
-        lib.adt_awp_combine.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, vp, vp]
+        lib.adt_awp_combine.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, vp, vp, vp]
         lib.adt_awp_fixup_pieces.restype = ctypes.c_int
-        lib.adt_awp_fixup_pieces.argtypes = [seg_p, seg_p, ctypes.c_int, P(ctypes.c_int32), vp, vp, vp, vp]
+        lib.adt_awp_fixup_pieces.argtypes = [seg_p, seg_p, ctypes.c_int, P(ctypes.c_int32), vp, vp, vp, vp, vp]
         lib.adt_awp_fixup_gather.restype = ctypes.c_int
         lib.adt_awp_fixup_gather.argtypes = [seg_p, ctypes.c_int, P(ctypes.c_int32), P(ctypes.c_void_p), ctypes.c_int,
-                                             vp, vp, vp]
+                                             vp, vp, vp, vp]
         lib.adt_sumsq.restype = ctypes.c_int
         lib.adt_sumsq.argtypes = [seg_p, ctypes.c_int, vp, vp, vp]
         lib.adt_device_sm_count.restype = ctypes.c_int
         lib.adt_device_sm_count.argtypes = [P(ctypes.c_int)]
+        lib.adt_pack_host.restype = ctypes.c_int
+        lib.adt_pack_host.argtypes = [seg_p, ctypes.c_int, vp, vp, ctypes.c_int]
+        lib.adt_host_to_device.restype = ctypes.c_int
+        lib.adt_host_to_device.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, ctypes.c_uint64, vp, ctypes.c_int,
+                                           ctypes.c_uint64, vp]
+        lib.adt_host_threads.restype = ctypes.c_int
+        lib.adt_host_threads.argtypes = [P(ctypes.c_int)]
+        lib.adt_host_simd.restype = ctypes.c_int
+        lib.adt_host_simd.argtypes = []
         if lib.adt_abi_version() != ABI_VERSION:
             raise ImportError(f"libadt ABI {lib.adt_abi_version()} != expected {ABI_VERSION}; rebuild")
         _lib = lib

@@ -13,9 +13,10 @@
 constexpr int kAwpThreads = 256;
 __global__ void __launch_bounds__(kAwpThreads)
 adt_awp_observe_kernel(const double *__restrict__ seg_sumsq, const __grid_constant__ adt_awp_device D,
-                       const __grid_constant__ adt_awp_config C) {
+                       const __grid_constant__ adt_awp_config C, const uint32_t *abort) {
     __shared__ int64_t slot_batch[2];
     __shared__ int32_t n_esc;
+    if (aborted(abort)) return;        // inputs came from a failed exchange: the AWP state does not advance
     if (threadIdx.x == 0) {
         slot_batch[0] = D.counter[0] % D.ring_steps;
         slot_batch[1] = D.counter[1];
@@ -97,6 +98,7 @@ adt_awp_fixup_kernel(const __grid_constant__ FixupTable<MAXSEG> F) {
     const Table<MAXSEG> &T = F.T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t *ws = stage[warp];
+    if (aborted(T.abort)) return;
     const int32_t n_esc = F.escalated[0];                // usually 0: one load and out
     uint32_t vt = blockIdx.x;                            // virtual tile index over the escalated segments
     for (int32_t e = 0; e < n_esc; ++e) {
@@ -156,7 +158,8 @@ adt_awp_fixup_kernel(const __grid_constant__ FixupTable<MAXSEG> F) {
 // order as sharded.ShardPlan.combine_sumsq, so every rank gets the same bits.
 __global__ void __launch_bounds__(256)
 adt_awp_combine_kernel(const double *__restrict__ tails, int npieces_total, const int32_t *__restrict__ piece_layer,
-                       int nlayers, double *__restrict__ seg_sumsq) {
+                       int nlayers, double *__restrict__ seg_sumsq, const uint32_t *abort) {
+    if (aborted(abort)) return;
     for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlayers; l += gridDim.x * blockDim.x) {
         double acc = 0.0;
         for (int k = 0; k < npieces_total; ++k)

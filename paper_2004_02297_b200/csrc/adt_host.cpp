@@ -1,0 +1,400 @@
+// adt_host.cpp — the CPU half of the paper's CPU-master setting: Bitpack on the
+// host cores, only the packed bytes cross PCIe, Bitunpack on the GPU.
+//
+// Paper (Fig. 2): the FP32 master weights
+// live in host memory; before every host->GPU transfer the CPU keeps the top
+// RoundTo bytes of every weight (OpenMP + AVX2 in the paper), the packed
+// stream is copied to the GPU, and a CUDA kernel zero-fills the dropped bytes.
+// The byte semantics are the reference codec's (codec.py:116-197: weight i ->
+// payload bytes [i*r, (i+1)*r), most-significant byte first), and the layer's
+// l2 norm (precision.py:25-28) is fused into the same read of the masters.
+//
+// B200-host design (16-core Emerald Rapids VM, AVX-512 VBMI):
+//   * one pass over the masters: 64 words (256 B) per iteration — VPERMB /
+//     VPERMT2B gather the kept bytes of 64 words into r full 64-byte vectors,
+//     written with non-temporal stores when the destination is 64-B aligned
+//     (no read-for-ownership of the pinned staging lines); the float64 sum of
+//     squares rides along (VCVTPS2PD + VFMADD, four accumulators);
+//   * work units of 64K weights (fixed: results do not depend on the thread
+//     count), claimed in order from an atomic counter by a persistent worker
+//     pool plus the calling thread;
+//   * adt_host_to_device: the calling thread also issues cudaMemcpyAsync for
+//     every run of finished units (>= min batch), so the DMA of unit k overlaps
+//     the packing of unit k+16.., then queues the device unpack (adt_unpack).
+// A scalar path (bswap, r-byte copies) serves hosts without AVX-512 VBMI.
+
+#include <cuda_runtime.h>
+#include <immintrin.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include <sched.h>
+
+#include "adt.h"
+
+namespace {
+
+constexpr uint64_t kUnitWeights = 1u << 16;   // weights per work unit (multiple of 64)
+constexpr uint64_t kGroup = 64;               // weights per vector iteration
+
+// ------------------------------------------------------------ scalar path
+inline uint32_t bswap32(uint32_t w) { return __builtin_bswap32(w); }
+
+double pack_scalar(const uint32_t *src, uint64_t n, int r, uint8_t *dst) {
+    double acc = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t be = bswap32(src[i]);
+        memcpy(dst + i * r, &be, static_cast<size_t>(r));
+        float f;
+        memcpy(&f, src + i, 4);
+        acc += static_cast<double>(f) * static_cast<double>(f);
+    }
+    return acc;
+}
+
+// ------------------------------------------------------- AVX-512 VBMI path
+// Byte-gather indices, built once. For r = 2, 3: output vector k of a 64-word
+// group takes its bytes from the input vector pair (v[b], v[b+1]), b = 4k/r;
+// byte j of the packed stream is byte 3 - (j % r) of word j / r.
+struct PermTables {
+    alignas(64) uint8_t r4[64];        // VPERMB: byte-swap each word of one vector
+    alignas(64) uint8_t r2[2][64];     // VPERMT2B over (v[2k], v[2k+1])
+    alignas(64) uint8_t r3[3][64];     // VPERMT2B over (v[k], v[k+1]), k = 0..2
+    alignas(64) uint8_t r1lo[64];      // VPERMT2B over (v0, v1) -> bytes 0..31
+    alignas(64) uint8_t r1hi[64];      // VPERMT2B over (v2, v3) -> bytes 32..63
+    PermTables() {
+        for (int j = 0; j < 64; ++j) r4[j] = static_cast<uint8_t>((j / 4) * 4 + 3 - j % 4);
+        for (int k = 0; k < 2; ++k)
+            for (int j = 0; j < 64; ++j) {
+                const int g = 64 * k + j, w = g / 2, p = g % 2, base = 2 * k;
+                r2[k][j] = static_cast<uint8_t>((w / 16 - base) * 64 + (w % 16) * 4 + 3 - p);
+            }
+        for (int k = 0; k < 3; ++k)
+            for (int j = 0; j < 64; ++j) {
+                const int g = 64 * k + j, w = g / 3, p = g % 3, base = k;
+                r3[k][j] = static_cast<uint8_t>((w / 16 - base) * 64 + (w % 16) * 4 + 3 - p);
+            }
+        for (int j = 0; j < 64; ++j) {
+            const int w = j;                                   // one byte per word
+            r1lo[j] = static_cast<uint8_t>(j < 32 ? (w / 16) * 64 + (w % 16) * 4 + 3 : 0);
+            const int w2 = j - 32;                             // words 32..63 from (v2, v3)
+            r1hi[j] = static_cast<uint8_t>(j >= 32 ? (w2 / 16) * 64 + (w2 % 16) * 4 + 3 : 0);
+        }
+    }
+};
+const PermTables &perm() {
+    static const PermTables t;
+    return t;
+}
+
+#define ADT_AVX512 __attribute__((target("avx512f,avx512bw,avx512dq,avx512vbmi")))
+
+ADT_AVX512 inline __m512d sq_acc(__m512d acc, __m256 h) {
+    const __m512d d = _mm512_cvtps_pd(h);
+    return _mm512_fmadd_pd(d, d, acc);
+}
+
+template <bool NT>
+ADT_AVX512 inline void put(uint8_t *dst, __m512i v) {
+    if (NT) _mm512_stream_si512(reinterpret_cast<__m512i *>(dst), v);
+    else _mm512_storeu_si512(dst, v);
+}
+
+// Pack n words (n multiple of 64) into dst; returns the float64 sum of squares.
+template <int R, bool NT>
+ADT_AVX512 double pack_avx512(const uint32_t *src, uint64_t n, uint8_t *dst) {
+    const PermTables &T = perm();
+    __m512d a0 = _mm512_setzero_pd(), a1 = _mm512_setzero_pd(), a2 = _mm512_setzero_pd(), a3 = _mm512_setzero_pd();
+    const __m512i i4 = _mm512_load_si512(T.r4);
+    const __m512i i2a = _mm512_load_si512(T.r2[0]), i2b = _mm512_load_si512(T.r2[1]);
+    const __m512i i3a = _mm512_load_si512(T.r3[0]), i3b = _mm512_load_si512(T.r3[1]),
+                  i3c = _mm512_load_si512(T.r3[2]);
+    const __m512i i1l = _mm512_load_si512(T.r1lo), i1h = _mm512_load_si512(T.r1hi);
+    for (uint64_t i = 0; i < n; i += kGroup) {
+        const __m512i v0 = _mm512_loadu_si512(src + i), v1 = _mm512_loadu_si512(src + i + 16),
+                      v2 = _mm512_loadu_si512(src + i + 32), v3 = _mm512_loadu_si512(src + i + 48);
+        uint8_t *o = dst + i * R;
+        if (R == 4) {
+            put<NT>(o, _mm512_permutexvar_epi8(i4, v0));
+            put<NT>(o + 64, _mm512_permutexvar_epi8(i4, v1));
+            put<NT>(o + 128, _mm512_permutexvar_epi8(i4, v2));
+            put<NT>(o + 192, _mm512_permutexvar_epi8(i4, v3));
+        } else if (R == 3) {
+            put<NT>(o, _mm512_permutex2var_epi8(v0, i3a, v1));
+            put<NT>(o + 64, _mm512_permutex2var_epi8(v1, i3b, v2));
+            put<NT>(o + 128, _mm512_permutex2var_epi8(v2, i3c, v3));
+        } else if (R == 2) {
+            put<NT>(o, _mm512_permutex2var_epi8(v0, i2a, v1));
+            put<NT>(o + 64, _mm512_permutex2var_epi8(v2, i2b, v3));
+        } else {
+            const __m512i lo = _mm512_permutex2var_epi8(v0, i1l, v1);
+            const __m512i hi = _mm512_permutex2var_epi8(v2, i1h, v3);
+            put<NT>(o, _mm512_mask_blend_epi8(0xFFFFFFFF00000000ull, lo, hi));
+        }
+        a0 = sq_acc(a0, _mm512_castps512_ps256(_mm512_castsi512_ps(v0)));
+        a1 = sq_acc(a1, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v0), 1)));
+        a2 = sq_acc(a2, _mm512_castps512_ps256(_mm512_castsi512_ps(v1)));
+        a3 = sq_acc(a3, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v1), 1)));
+        a0 = sq_acc(a0, _mm512_castps512_ps256(_mm512_castsi512_ps(v2)));
+        a1 = sq_acc(a1, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v2), 1)));
+        a2 = sq_acc(a2, _mm512_castps512_ps256(_mm512_castsi512_ps(v3)));
+        a3 = sq_acc(a3, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v3), 1)));
+    }
+    if (NT) _mm_sfence();
+    return _mm512_reduce_add_pd(_mm512_add_pd(_mm512_add_pd(a0, a1), _mm512_add_pd(a2, a3)));
+}
+
+using PackFn = double (*)(const uint32_t *, uint64_t, uint8_t *);
+
+ADT_AVX512 PackFn pick_avx512(int r, bool nt) {
+    switch (r) {
+        case 1: return nt ? pack_avx512<1, true> : pack_avx512<1, false>;
+        case 2: return nt ? pack_avx512<2, true> : pack_avx512<2, false>;
+        case 3: return nt ? pack_avx512<3, true> : pack_avx512<3, false>;
+        default: return nt ? pack_avx512<4, true> : pack_avx512<4, false>;
+    }
+}
+
+bool have_vbmi() {
+    static const bool v = [] {
+        __builtin_cpu_init();
+        const char *e = getenv("ADT_HOST_SCALAR");          // A/B and test hook
+        return !(e != nullptr && e[0] == '1') && __builtin_cpu_supports("avx512vbmi") &&
+               __builtin_cpu_supports("avx512bw");
+    }();
+    return v;
+}
+
+bool use_nt() {
+    static const bool v = [] {
+        const char *e = getenv("ADT_HOST_NT");               // A/B: 0 = regular stores
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return v;
+}
+
+// One work unit: weights [lo, hi) of one layer. Returns its sum of squares.
+double pack_unit(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *packed) {
+    const uint32_t *src = static_cast<const uint32_t *>(s.weights) + lo;
+    uint8_t *dst = packed + s.offset + lo * static_cast<uint64_t>(s.round_to);
+    const uint64_t n = hi - lo, body = have_vbmi() ? n / kGroup * kGroup : 0;
+    double acc = 0.0;
+    if (body) {
+        const bool nt = use_nt() && (reinterpret_cast<uintptr_t>(dst) % 64 == 0);
+        acc = pick_avx512(s.round_to, nt)(src, body, dst);
+    }
+    if (body < n) acc += pack_scalar(src + body, n - body, s.round_to, dst + body * s.round_to);
+    return acc;
+}
+
+// ------------------------------------------------------------ worker pool
+// Persistent workers (affinity count - 1; the caller is the last worker).
+// One job at a time: concurrent callers queue on `submit_mu`.
+class Pool {
+  public:
+    static Pool &get() {
+        static Pool *p = new Pool();   // never destroyed: workers may outlive static destructors
+        return *p;
+    }
+    int workers() const { return static_cast<int>(threads_.size()); }
+
+    // Run job(worker_index) on min(nthreads - 1, workers) pool threads; the
+    // caller runs `caller()` concurrently and then waits for the pool threads.
+    void run(int nthreads, const std::function<void(int)> &job, const std::function<void()> &caller) {
+        std::lock_guard<std::mutex> serial(submit_mu_);
+        const int use = std::max(0, std::min(nthreads - 1, workers()));
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job_ = &job;
+            active_ = use;
+            want_ = use;
+            ++gen_;
+        }
+        cv_.notify_all();
+        caller();
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [&] { return active_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    Pool() {
+        cpu_set_t set;
+        int n = 1;
+        if (sched_getaffinity(0, sizeof(set), &set) == 0) n = CPU_COUNT(&set);
+        for (int i = 0; i + 1 < n; ++i) threads_.emplace_back([this, i] { loop(i); });
+        for (auto &t : threads_) t.detach();
+    }
+    void loop(int idx) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)> *job = nullptr;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (idx < want_) job = job_;
+            }
+            if (job == nullptr) continue;
+            (*job)(idx);
+            std::lock_guard<std::mutex> g(mu_);
+            if (--active_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> threads_;
+    std::mutex mu_, submit_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)> *job_ = nullptr;
+    uint64_t gen_ = 0;
+    int active_ = 0, want_ = 0;
+};
+
+struct Unit {
+    int seg;
+    uint64_t lo, hi;
+};
+
+int validate_host(const adt_segment *segs, int nseg, const uint8_t *packed) {
+    if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
+    bool any = false;
+    for (int i = 0; i < nseg; ++i) {
+        const adt_segment &g = segs[i];
+        if (g.round_to < 1 || g.round_to > 4) return ADT_ERR_ROUND_TO;
+        if (g.reserved != 0) return ADT_ERR_ARG;
+        if (g.count == 0) continue;
+        any = true;
+        if (g.weights == nullptr) return ADT_ERR_ARG;
+        if (reinterpret_cast<uintptr_t>(g.weights) % 4) return ADT_ERR_ALIGN;
+        if (g.count > (UINT64_MAX - g.offset) / 4) return ADT_ERR_ARG;
+    }
+    if (any && packed == nullptr) return ADT_ERR_ARG;
+    return ADT_OK;
+}
+
+std::vector<Unit> make_units(const adt_segment *segs, int nseg) {
+    std::vector<Unit> u;
+    for (int s = 0; s < nseg; ++s)
+        for (uint64_t lo = 0; lo < segs[s].count; lo += kUnitWeights)
+            u.push_back({s, lo, std::min(segs[s].count, lo + kUnitWeights)});
+    return u;
+}
+
+// Pack every unit on `threads` threads; `on_progress(ready_prefix)` is called
+// by the caller thread between its own units with the count of leading units
+// that are complete (for the DMA pipeline). Per-unit sums go to unit_ss.
+void pack_units(const adt_segment *segs, const std::vector<Unit> &units, uint8_t *packed, int threads,
+                std::vector<double> &unit_ss, const std::function<void(size_t)> &on_progress) {
+    const size_t nu = units.size();
+    std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[nu == 0 ? 1 : nu]);
+    for (size_t i = 0; i < nu; ++i) done[i].store(0, std::memory_order_relaxed);
+    std::atomic<size_t> next{0};
+    auto work_one = [&](size_t k) {
+        const Unit &u = units[k];
+        unit_ss[k] = pack_unit(segs[u.seg], u.lo, u.hi, packed);
+        done[k].store(1, std::memory_order_release);
+    };
+    const std::function<void(int)> job = [&](int) {
+        for (size_t k; (k = next.fetch_add(1, std::memory_order_relaxed)) < nu;) work_one(k);
+    };
+    size_t prefix = 0;
+    auto advance = [&] {
+        while (prefix < nu && done[prefix].load(std::memory_order_acquire)) ++prefix;
+        on_progress(prefix);
+    };
+    const std::function<void()> caller = [&] {
+        for (size_t k; (k = next.fetch_add(1, std::memory_order_relaxed)) < nu;) {
+            work_one(k);
+            advance();
+        }
+        while (prefix < nu) {                 // the pool finishes the last units
+            advance();
+            if (prefix < nu) _mm_pause();
+        }
+    };
+    Pool::get().run(threads, job, caller);
+    on_progress(nu);
+}
+
+void finish_sums(const std::vector<Unit> &units, const std::vector<double> &unit_ss, int nseg, double *seg_sumsq) {
+    if (seg_sumsq == nullptr) return;
+    for (int s = 0; s < nseg; ++s) seg_sumsq[s] = 0.0;
+    for (size_t k = 0; k < units.size(); ++k) seg_sumsq[units[k].seg] += unit_ss[k];   // fixed unit order
+}
+
+int resolve_threads(int threads) {
+    const int avail = Pool::get().workers() + 1;
+    return threads <= 0 ? avail : std::min(threads, avail);
+}
+
+}  // namespace
+
+extern "C" {
+
+int adt_host_threads(int *n) {
+    if (n == nullptr) return ADT_ERR_ARG;
+    *n = Pool::get().workers() + 1;
+    return ADT_OK;
+}
+
+int adt_host_simd(void) { return have_vbmi() ? 512 : 0; }
+
+int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *seg_sumsq, int threads) {
+    const int v = validate_host(segs, nseg, packed);
+    if (v != ADT_OK) return v;
+    const std::vector<Unit> units = make_units(segs, nseg);
+    std::vector<double> ss(units.size(), 0.0);
+    pack_units(segs, units, packed, resolve_threads(threads), ss, [](size_t) {});
+    finish_sums(units, ss, nseg, seg_sumsq);
+    return ADT_OK;
+}
+
+int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
+                       uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
+                       uint64_t min_copy_bytes, void *stream) {
+    int v = validate_host(host_segs, nseg, host_packed);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && (dev_segs == nullptr || dev_packed == nullptr)) return ADT_ERR_ARG;
+    uint64_t end_prev = 0;                    // payloads in increasing, non-overlapping order (the DMA
+    for (int i = 0; i < nseg; ++i) {          // ships the stream front to back as units complete)
+        const adt_segment &h = host_segs[i], &d = dev_segs[i];
+        if (h.count != d.count || h.offset != d.offset || h.round_to != d.round_to) return ADT_ERR_ARG;
+        if (h.count == 0) continue;
+        const uint64_t end = h.offset + h.count * static_cast<uint64_t>(h.round_to);
+        if (h.offset < end_prev || end > packed_bytes) return ADT_ERR_ARG;
+        end_prev = end;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const std::vector<Unit> units = make_units(host_segs, nseg);
+    std::vector<double> ss(units.size(), 0.0);
+    // byte range of the packed stream that is final once units [0, k) are done:
+    // [0, start of unit k), the trailing pad included with the last unit
+    auto ready_bytes = [&](size_t k) -> uint64_t {
+        if (k >= units.size()) return packed_bytes;
+        const adt_segment &s = host_segs[units[k].seg];
+        return s.offset + units[k].lo * static_cast<uint64_t>(s.round_to);
+    };
+    uint64_t sent = 0;
+    cudaError_t err = cudaSuccess;
+    const uint64_t batch = min_copy_bytes == 0 ? (1u << 20) : min_copy_bytes;
+    pack_units(host_segs, units, host_packed, resolve_threads(threads), ss, [&](size_t prefix) {
+        const uint64_t end = ready_bytes(prefix);
+        if (err != cudaSuccess || end <= sent) return;
+        if (end - sent < batch && prefix < units.size()) return;
+        err = cudaMemcpyAsync(dev_packed + sent, host_packed + sent, end - sent, cudaMemcpyHostToDevice, st);
+        sent = end;
+    });
+    finish_sums(units, ss, nseg, seg_sumsq);
+    if (err != cudaSuccess) return ADT_ERR_CUDA_BASE - static_cast<int>(err);
+    return adt_unpack(dev_segs, nseg, dev_packed, stream);
+}
+
+}  // extern "C"

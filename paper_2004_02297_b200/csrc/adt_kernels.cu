@@ -67,8 +67,17 @@ struct Table {
     // change decided on the device needs no new launch table. nullptr = round_to[].
     const uint8_t *dyn_r;
     uint32_t tile_rot;           // unpack: the tile walk starts rotated by this many tiles (< ntiles)
+    // Peer-abort guard (p2p transport): the peer barrier's timeout word. When
+    // it is nonzero at kernel start the kernel does no work, so a stalled or
+    // dead peer never lets stale / half-written peer bytes reach a replica or
+    // a master (the host raises at its next poll). nullptr = unguarded.
+    const uint32_t *abort;
 };
 constexpr int kHints = 1024;
+
+__device__ __forceinline__ bool aborted(const uint32_t *word) {
+    return word != nullptr && *reinterpret_cast<const volatile uint32_t *>(word) != 0u;
+}
 
 template <int MAXSEG>
 __device__ __forceinline__ int width_of(const Table<MAXSEG> &T, int s) {
@@ -553,6 +562,7 @@ __global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
 adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     uint32_t *ws = stage[threadIdx.x >> 5];
+    if (aborted(T.abort)) return;
     // Newest-first (ADT_UNPACK_REVERSE): CTAs are dispatched roughly in
     // blockIdx order, so walking the tiles backwards reads the payload the
     // pack pass wrote last — the part still resident in the 126 MB L2 —
@@ -702,10 +712,12 @@ int validate(const adt_segment *segs, int nseg, const void *packed, bool need_pa
 template <int MAXSEG>
 int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc,
                  uint8_t *pout, double *seg_sumsq, double *partials, uint32_t ntiles, bool finalize,
-                 cudaStream_t stream, const uint8_t *dyn_r = nullptr, int start_seg = -1) {
+                 cudaStream_t stream, const uint8_t *dyn_r = nullptr, int start_seg = -1,
+                 const uint32_t *abort = nullptr) {
     Table<MAXSEG> T;
     T.dyn_r = dyn_r;
     T.tile_rot = 0;
+    T.abort = abort;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = (srcs != nullptr && i < nsrc) ? srcs[i] : nullptr;
     T.packed_out = pout;
     T.seg_sumsq = seg_sumsq;
@@ -762,7 +774,7 @@ constexpr int kLargeSeg = 256;
 // (adt_norm_finalize) walks exactly the chunks the pack pass wrote.
 int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs, int nsrc, uint8_t *pout,
         double *seg_sumsq, double *partials, bool finalize, void *stream_v, const uint8_t *dyn_r = nullptr,
-        int start_seg = -1) {
+        int start_seg = -1, const uint32_t *abort = nullptr) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
     uint64_t partial_base = 0;
     int base = 0;
@@ -779,9 +791,9 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs
         double *pp = partials ? partials + partial_base : nullptr;
         const int st = cnt <= kSmallSeg
             ? launch_chunk<kSmallSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles),
-                                      finalize, stream, dyn_r ? dyn_r + base : nullptr, start_seg - base)
+                                      finalize, stream, dyn_r ? dyn_r + base : nullptr, start_seg - base, abort)
             : launch_chunk<kLargeSeg>(pass, segs + base, cnt, srcs, nsrc, pout, ss, pp, static_cast<uint32_t>(tiles),
-                                      finalize, stream, dyn_r ? dyn_r + base : nullptr, start_seg - base);
+                                      finalize, stream, dyn_r ? dyn_r + base : nullptr, start_seg - base, abort);
         if (st != ADT_OK) return st;
         partial_base += tiles * kWarpsPerTile;
         base += cnt;
@@ -797,6 +809,7 @@ struct SgdArgs {
     float total, lr, mu, wd;
     int nc;                                 // 0 = one pre-averaged gradient per segment
     const uint8_t *widths;                  // device-resident widths (global layer index) or nullptr
+    const uint32_t *abort;                  // peer-abort guard word or nullptr
 };
 
 template <int MAXSEG, int NC>
@@ -839,6 +852,7 @@ int launch_sgd_chunk(const adt_sgd_segment *segs, const adt_grad_segment *gsegs,
     SgdTable<MAXSEG> T;
     T.dyn_r = A.widths != nullptr ? A.widths + base : nullptr;
     T.tile_rot = 0;
+    T.abort = A.abort;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) {
         T.srcs[i] = A.srcs[i];
         T.scale[i] = A.scale[i];
@@ -971,21 +985,21 @@ int adt_unpack_multi(const adt_segment *segs, int nseg, const uint8_t *const *so
 }
 
 int adt_copy_multi(uint8_t *dst, const uint8_t *const *sources, int nsrc, uint64_t offset, uint64_t bytes,
-                   void *stream) {
+                   const uint32_t *abort, void *stream) {
     if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr || dst == nullptr) return ADT_ERR_ARG;
     SrcList S;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) S.p[i] = i < nsrc ? sources[i] : nullptr;
     for (int i = 0; i < nsrc; ++i)
         if (S.p[i] == nullptr) return ADT_ERR_ARG;
     if (bytes == 0) return ADT_OK;
-    adt_copy_multi_param_kernel<<<nsrc, 128, 0, static_cast<cudaStream_t>(stream)>>>(dst, S, offset, bytes);
+    adt_copy_multi_param_kernel<<<nsrc, 128, 0, static_cast<cudaStream_t>(stream)>>>(dst, S, offset, bytes, abort);
     return cuda_status(cudaGetLastError());
 }
 
-int adt_peer_barrier(uint32_t *const *flags, int nranks, int rank, uint32_t *state, uint64_t max_polls,
+int adt_peer_barrier(uint32_t *const *flags, int nranks, int rank, uint32_t *state, uint64_t timeout_ns,
                      void *stream) {
     if (flags == nullptr || state == nullptr || nranks < 1 || nranks > ADT_MAX_SOURCES || rank < 0 ||
-        rank >= nranks || max_polls == 0)
+        rank >= nranks || timeout_ns == 0)
         return ADT_ERR_ARG;
     FlagList F;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) F.p[i] = i < nranks ? flags[i] : nullptr;
@@ -993,7 +1007,7 @@ int adt_peer_barrier(uint32_t *const *flags, int nranks, int rank, uint32_t *sta
         if (F.p[i] == nullptr) return ADT_ERR_ARG;
         if (reinterpret_cast<uintptr_t>(F.p[i]) % 4) return ADT_ERR_ALIGN;
     }
-    adt_peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(F, nranks, rank, state, max_polls);
+    adt_peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(F, nranks, rank, state, timeout_ns);
     return cuda_status(cudaGetLastError());
 }
 
@@ -1076,7 +1090,8 @@ int sgd_pack_impl(const adt_sgd_segment *segs, int nseg, float lr, float momentu
 
 int reduce_sgd_pack_impl(const adt_grad_segment *segs, int nseg, const float *const *grads,
                          const int64_t *sample_counts, int ncontrib, float lr, float momentum, float weight_decay,
-                         uint8_t *packed, double *seg_sumsq, double *partials, const uint8_t *widths, void *stream) {
+                         uint8_t *packed, double *seg_sumsq, double *partials, const uint8_t *widths,
+                         const uint32_t *abort, void *stream) {
     if (nseg < 0 || (nseg > 0 && segs == nullptr)) return ADT_ERR_ARG;
     if (ncontrib < 1 || ncontrib > ADT_MAX_SOURCES || grads == nullptr || sample_counts == nullptr)
         return ADT_ERR_ARG;
@@ -1096,6 +1111,7 @@ int reduce_sgd_pack_impl(const adt_grad_segment *segs, int nseg, const float *co
     A.wd = weight_decay;
     A.nc = ncontrib;
     A.widths = widths;
+    A.abort = abort;
     bool any = false;
     for (int i = 0; i < nseg; ++i) {
         const adt_grad_segment &g = segs[i];
@@ -1125,9 +1141,9 @@ int adt_sgd_pack(const adt_sgd_segment *segs, int nseg, float lr, float momentum
 
 int adt_reduce_sgd_pack(const adt_grad_segment *segs, int nseg, const float *const *grads,
                         const int64_t *sample_counts, int ncontrib, float lr, float momentum, float weight_decay,
-                        uint8_t *packed, double *seg_sumsq, double *partials, void *stream) {
+                        uint8_t *packed, double *seg_sumsq, double *partials, const uint32_t *abort, void *stream) {
     return reduce_sgd_pack_impl(segs, nseg, grads, sample_counts, ncontrib, lr, momentum, weight_decay, packed,
-                                seg_sumsq, partials, nullptr, stream);
+                                seg_sumsq, partials, nullptr, abort, stream);
 }
 
 int adt_sgd_pack_dyn(const adt_sgd_segment *segs, int nseg, float lr, float momentum, float weight_decay,
@@ -1141,12 +1157,12 @@ int adt_sgd_pack_dyn(const adt_sgd_segment *segs, int nseg, float lr, float mome
 int adt_reduce_sgd_pack_dyn(const adt_grad_segment *segs, int nseg, const float *const *grads,
                             const int64_t *sample_counts, int ncontrib, float lr, float momentum,
                             float weight_decay, uint8_t *packed, double *partials, const uint8_t *widths,
-                            void *stream) {
+                            const uint32_t *abort, void *stream) {
     if (nseg > 0 && (segs == nullptr || widths == nullptr)) return ADT_ERR_ARG;
     for (int i = 0; i < nseg; ++i)
         if (segs[i].round_to != 4) return ADT_ERR_ARG;
     return reduce_sgd_pack_impl(segs, nseg, grads, sample_counts, ncontrib, lr, momentum, weight_decay, packed,
-                                nullptr, partials, widths, stream);
+                                nullptr, partials, widths, abort, stream);
 }
 
 int adt_pack_dyn(const adt_segment *segs, int nseg, uint8_t *packed, double *partials, const uint8_t *widths,
@@ -1170,7 +1186,8 @@ int adt_unpack_dyn(const adt_segment *segs, int nseg, const uint8_t *packed, con
     return run(Pass::Unpack, segs, nseg, srcs, 1, nullptr, nullptr, nullptr, false, stream, widths);
 }
 
-int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg, void *stream) {
+int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const adt_awp_config *cfg,
+                    const uint32_t *abort, void *stream) {
     if (seg_sumsq == nullptr || dev == nullptr || cfg == nullptr) return ADT_ERR_ARG;
     const adt_awp_device &D = *dev;
     if (D.nlayers < 1 || D.ngroups < 1 || D.ngroups > D.nlayers || D.ring_steps < 1 || D.reserved != 0) return ADT_ERR_ARG;
@@ -1178,7 +1195,7 @@ int adt_awp_observe(const double *seg_sumsq, const adt_awp_device *dev, const ad
         !D.counter)
         return ADT_ERR_ARG;
     if (cfg->interval < 1 || cfg->step_bits < 1 || cfg->max_bits < 1 || cfg->max_bits > 32) return ADT_ERR_ARG;
-    adt_awp_observe_kernel<<<1, kAwpThreads, 0, static_cast<cudaStream_t>(stream)>>>(seg_sumsq, D, *cfg);
+    adt_awp_observe_kernel<<<1, kAwpThreads, 0, static_cast<cudaStream_t>(stream)>>>(seg_sumsq, D, *cfg, abort);
     return cuda_status(cudaGetLastError());
 }
 
@@ -1190,9 +1207,10 @@ namespace {
 template <int MAXSEG>
 int launch_fixup_chunk(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
                        const uint8_t *const *sources, int nsrc, const int32_t *seg_layer, const int32_t *escalated,
-                       const uint8_t *widths_new, int base, cudaStream_t stream) {
+                       const uint8_t *widths_new, int base, cudaStream_t stream, const uint32_t *abort = nullptr) {
     FixupTable<MAXSEG> F;
     Table<MAXSEG> &T = F.T;
+    T.abort = abort;
     for (int i = 0; i < ADT_MAX_SOURCES; ++i) T.srcs[i] = (sources != nullptr && i < nsrc) ? sources[i] : nullptr;
     T.packed_out = packed;
     T.seg_sumsq = nullptr;
@@ -1250,7 +1268,8 @@ int adt_awp_fixup(const adt_segment *masters, const adt_segment *replicas, int n
 }
 
 int adt_awp_fixup_pieces(const adt_segment *masters, const adt_segment *replicas, int nseg, const int32_t *seg_layer,
-                         uint8_t *packed, const int32_t *escalated, const uint8_t *widths_new, void *stream) {
+                         uint8_t *packed, const int32_t *escalated, const uint8_t *widths_new, const uint32_t *abort,
+                         void *stream) {
     int v = validate(replicas, nseg, packed, true);
     if (v != ADT_OK) return v;
     if ((v = validate(masters, nseg, packed, true)) != ADT_OK) return v;
@@ -1264,9 +1283,9 @@ int adt_awp_fixup_pieces(const adt_segment *masters, const adt_segment *replicas
         const int cnt = min(kLargeSeg, nseg - base);
         const int st = cnt <= kSmallSeg
             ? launch_fixup_chunk<kSmallSeg>(masters + base, replicas + base, cnt, packed, nullptr, 0, seg_layer + base,
-                                            escalated, widths_new + base, base, s)
+                                            escalated, widths_new + base, base, s, abort)
             : launch_fixup_chunk<kLargeSeg>(masters + base, replicas + base, cnt, packed, nullptr, 0, seg_layer + base,
-                                            escalated, widths_new + base, base, s);
+                                            escalated, widths_new + base, base, s, abort);
         if (st != ADT_OK) return st;
     }
     return ADT_OK;
@@ -1274,7 +1293,7 @@ int adt_awp_fixup_pieces(const adt_segment *masters, const adt_segment *replicas
 
 int adt_awp_fixup_gather(const adt_segment *replicas, int nseg, const int32_t *seg_layer,
                          const uint8_t *const *sources, int nsrc, const int32_t *escalated,
-                         const uint8_t *widths_new, void *stream) {
+                         const uint8_t *widths_new, const uint32_t *abort, void *stream) {
     if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
     const int v = validate(replicas, nseg, sources[0], false, nsrc);
     if (v != ADT_OK) return v;
@@ -1287,16 +1306,16 @@ int adt_awp_fixup_gather(const adt_segment *replicas, int nseg, const int32_t *s
         const int cnt = min(kLargeSeg, nseg - base);
         const int st = cnt <= kSmallSeg
             ? launch_fixup_chunk<kSmallSeg>(nullptr, replicas + base, cnt, nullptr, sources, nsrc, seg_layer + base,
-                                            escalated, widths_new + base, base, s)
+                                            escalated, widths_new + base, base, s, abort)
             : launch_fixup_chunk<kLargeSeg>(nullptr, replicas + base, cnt, nullptr, sources, nsrc, seg_layer + base,
-                                            escalated, widths_new + base, base, s);
+                                            escalated, widths_new + base, base, s, abort);
         if (st != ADT_OK) return st;
     }
     return ADT_OK;
 }
 
 int adt_unpack_multi_ex(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
-                        const uint8_t *widths, int start_seg, void *stream) {
+                        const uint8_t *widths, int start_seg, const uint32_t *abort, void *stream) {
     if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
     for (int i = 0; i < nsrc; ++i)
         if (reinterpret_cast<uintptr_t>(sources[i]) % 16) return ADT_ERR_ALIGN;
@@ -1307,11 +1326,11 @@ int adt_unpack_multi_ex(const adt_segment *segs, int nseg, const uint8_t *const 
         if (widths != nullptr && segs[i].round_to != 4) return ADT_ERR_ARG;   // capacity layout
     }
     return run(Pass::Unpack, segs, nseg, sources, nsrc, nullptr, nullptr, nullptr, false, stream, widths,
-               start_seg < nseg ? start_seg : -1);
+               start_seg < nseg ? start_seg : -1, abort);
 }
 
 int adt_unpack_multi_dyn(const adt_segment *segs, int nseg, const uint8_t *const *sources, int nsrc,
-                         const uint8_t *widths, void *stream) {
+                         const uint8_t *widths, const uint32_t *abort, void *stream) {
     if (nsrc < 1 || nsrc > ADT_MAX_SOURCES || sources == nullptr) return ADT_ERR_ARG;
     for (int i = 0; i < nsrc; ++i)
         if (reinterpret_cast<uintptr_t>(sources[i]) % 16) return ADT_ERR_ALIGN;
@@ -1320,15 +1339,15 @@ int adt_unpack_multi_dyn(const adt_segment *segs, int nseg, const uint8_t *const
     if (nseg > 0 && widths == nullptr) return ADT_ERR_ARG;
     for (int i = 0; i < nseg; ++i)
         if (segs[i].round_to != 4 || (segs[i].count > 0 && sources[segs[i].reserved] == nullptr)) return ADT_ERR_ARG;
-    return run(Pass::Unpack, segs, nseg, sources, nsrc, nullptr, nullptr, nullptr, false, stream, widths);
+    return run(Pass::Unpack, segs, nseg, sources, nsrc, nullptr, nullptr, nullptr, false, stream, widths, -1, abort);
 }
 
 int adt_awp_combine(const double *tails, int npieces_total, const int32_t *piece_layer, int nlayers,
-                    double *seg_sumsq, void *stream) {
+                    double *seg_sumsq, const uint32_t *abort, void *stream) {
     if (tails == nullptr || piece_layer == nullptr || seg_sumsq == nullptr || npieces_total < 0 || nlayers < 1)
         return ADT_ERR_ARG;
     adt_awp_combine_kernel<<<(nlayers + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        tails, npieces_total, piece_layer, nlayers, seg_sumsq);
+        tails, npieces_total, piece_layer, nlayers, seg_sumsq, abort);
     return cuda_status(cudaGetLastError());
 }
 

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, sgd_min_blocks(NC))
 adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
     constexpr int NG = NC > 0 ? NC : 1;
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    if (aborted(T.abort)) return;      // a peer barrier timed out: never step with stale gradients
     const uint32_t tile = blockIdx.x;
     const int s = find_segment(T, tile);
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;

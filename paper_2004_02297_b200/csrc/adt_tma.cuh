@@ -225,6 +225,7 @@ template <int MAXSEG>
 __global__ void __launch_bounds__(kBlock, kCtasPerSm)
 adt_unpack_tma_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    if (aborted(T.abort)) return;
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {

@@ -127,10 +127,15 @@ class ReduceSgdTable:
             * _lib.PARTIALS_PER_TILE
 
 
+def _ptr(t) -> int | None:
+    """Device address of an optional guard word (a torch tensor view) or None."""
+    return t.data_ptr() if t is not None else None
+
+
 def reduce_sgd_pack(table: ReduceSgdTable, grads: Sequence[int], sample_counts: Sequence[int], lr: float,
                     momentum: float, weight_decay: float, packed: torch.Tensor,
                     sumsq: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
-                    partials: torch.Tensor | None = None) -> None:
+                    partials: torch.Tensor | None = None, abort: torch.Tensor | None = None) -> None:
     """adt_reduce_sgd_pack: the contributions at device addresses `grads`
     (local buffers or peer buckets mapped by ipc_open) are combined as
     net.gather_and_update does, the masters/velocities stepped in place, the
@@ -146,15 +151,16 @@ def reduce_sgd_pack(table: ReduceSgdTable, grads: Sequence[int], sample_counts: 
     _lib.check(_lib.load().adt_reduce_sgd_pack(
         table.array, table.nseg, _lib.pointer_array(grads), counts, len(grads), float(lr), float(momentum),
         float(weight_decay), packed.data_ptr(), sumsq.data_ptr() if sumsq is not None else None,
-        partials.data_ptr() if partials is not None else None, sh))
+        partials.data_ptr() if partials is not None else None, _ptr(abort), sh))
 
 
 class _Scratch:
-    """Per (device, stream) norm scratch: the float64 partials of one pass.
-    Entries live for the process: a buffer handed to a kernel on stream S must
-    not return to the caching allocator while S may still use it (it was
-    allocated on whatever stream was current), and there is one per stream in
-    use — a handful."""
+    """Per (device, stream) norm scratch: the float64 partials of one pass,
+    one buffer per stream in use (a handful). A buffer handed to a kernel on
+    stream S must not return to the caching allocator while S may still use
+    it (it was allocated on whatever stream was current): an outgrown buffer
+    is marked as used on S (record_stream) before it is dropped, so the
+    allocator reuses its memory only after S's queued work completes."""
 
     _lock = threading.Lock()
     _cache: dict = {}
@@ -166,12 +172,10 @@ class _Scratch:
             cur = cls._cache.get(key)
             if cur is None or cur.numel() < max(1, n):
                 if cur is not None:
-                    cls._retired.append(cur)           # possibly still in use on `stream`
+                    cur.record_stream(torch.cuda.ExternalStream(stream, device=device))
                 cur = torch.empty(max(1, n), dtype=torch.float64, device=device)
                 cls._cache[key] = cur
             return cur
-
-    _retired: list = []
 
 
 def _device_of(table: SegmentTable) -> torch.device:
@@ -221,36 +225,39 @@ def unpack(table: SegmentTable, packed: torch.Tensor, stream: torch.cuda.Stream 
 
 
 def unpack_multi(table: SegmentTable, sources: Sequence[int], stream: torch.cuda.Stream | None = None,
-                 start_seg: int = -1) -> None:
+                 start_seg: int = -1, abort: torch.Tensor | None = None) -> None:
     """adt_unpack_multi(_ex): layer l's payload read from sources[table source index]
     (raw device addresses: local buffers or peer buffers mapped by ipc_open);
-    start_seg >= 0 rotates the tile walk to start just before that segment."""
+    start_seg >= 0 rotates the tile walk to start just before that segment;
+    abort: the peer barrier's timeout word (the kernel does nothing once it is set)."""
     arr = _lib.pointer_array(sources)
-    if start_seg >= 0:
+    if start_seg >= 0 or abort is not None:
         _lib.check(_lib.load().adt_unpack_multi_ex(table.array, table.nseg, arr, len(sources), None, int(start_seg),
-                                                   stream_handle(stream)))
+                                                   _ptr(abort), stream_handle(stream)))
     else:
         _lib.check(_lib.load().adt_unpack_multi(table.array, table.nseg, arr, len(sources), stream_handle(stream)))
 
 
 def copy_multi(dst: torch.Tensor, sources: Sequence[int], offset: int, nbytes: int,
-               stream: torch.cuda.Stream | None = None) -> None:
+               stream: torch.cuda.Stream | None = None, abort: torch.Tensor | None = None) -> None:
     """dst[q*nbytes:(q+1)*nbytes] = bytes [offset, offset+nbytes) of sources[q]."""
     if dst.dtype != torch.uint8 or not dst.is_cuda or dst.numel() < nbytes * len(sources):
         raise ValueError("dst must be a CUDA uint8 tensor of len(sources)*nbytes")
     arr = _lib.pointer_array(sources)
-    _lib.check(_lib.load().adt_copy_multi(dst.data_ptr(), arr, len(sources), offset, nbytes, stream_handle(stream)))
+    _lib.check(_lib.load().adt_copy_multi(dst.data_ptr(), arr, len(sources), offset, nbytes, _ptr(abort),
+                                          stream_handle(stream)))
 
 
-def peer_barrier(flag_ptrs: Sequence[int], rank: int, state: torch.Tensor, max_polls: int = 1 << 24,
+def peer_barrier(flag_ptrs: Sequence[int], rank: int, state: torch.Tensor, timeout_s: float = 30.0,
                  stream: torch.cuda.Stream | None = None) -> None:
     """adt_peer_barrier: stream-ordered barrier over peer memory. flag_ptrs[q]
     = rank q's int32[nranks] epoch array mapped here; state = this rank's
-    int32[2] (epoch counter, timeout epoch)."""
+    int32[2] (epoch counter, timeout epoch = the abort word of the guarded
+    kernels behind it). The wait gives up after `timeout_s` of device time."""
     if state.dtype != torch.int32 or not state.is_cuda or state.numel() < 2:
         raise ValueError("state must be a CUDA int32 tensor of 2 entries")
     _lib.check(_lib.load().adt_peer_barrier(_lib.pointer_array(flag_ptrs), len(flag_ptrs), rank, state.data_ptr(),
-                                            int(max_polls), stream_handle(stream)))
+                                            max(1, int(timeout_s * 1e9)), stream_handle(stream)))
 
 
 def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
@@ -329,10 +336,11 @@ def unpack_dyn(table: SegmentTable, packed: torch.Tensor, widths: torch.Tensor,
                                           stream_handle(stream)))
 
 
-def awp_observe(sumsq: torch.Tensor, device_struct, config_struct, stream: torch.cuda.Stream | None = None) -> None:
+def awp_observe(sumsq: torch.Tensor, device_struct, config_struct, stream: torch.cuda.Stream | None = None,
+                abort: torch.Tensor | None = None) -> None:
     """adt_awp_observe: one device-side AWP observation of every layer."""
     _lib.check(_lib.load().adt_awp_observe(sumsq.data_ptr(), ctypes.byref(device_struct), ctypes.byref(config_struct),
-                                           stream_handle(stream)))
+                                           _ptr(abort), stream_handle(stream)))
 
 
 def awp_fixup(masters: SegmentTable, replicas: SegmentTable, packed: torch.Tensor, escalated: torch.Tensor,
@@ -353,7 +361,8 @@ def sgd_pack_dyn(table: SgdTable, lr: float, momentum: float, weight_decay: floa
 
 def reduce_sgd_pack_dyn(table: ReduceSgdTable, grads: Sequence[int], sample_counts: Sequence[int], lr: float,
                         momentum: float, weight_decay: float, packed: torch.Tensor, widths: torch.Tensor,
-                        partials: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None) -> None:
+                        partials: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
+                        abort: torch.Tensor | None = None) -> None:
     """adt_reduce_sgd_pack_dyn: gradient combine + update + pack at device-resident widths."""
     if len(grads) != len(sample_counts) or not 1 <= len(grads) <= _lib.MAX_SOURCES:
         raise ValueError(f"need 1..{_lib.MAX_SOURCES} contributions with one sample count each")
@@ -361,7 +370,7 @@ def reduce_sgd_pack_dyn(table: ReduceSgdTable, grads: Sequence[int], sample_coun
     _lib.check(_lib.load().adt_reduce_sgd_pack_dyn(
         table.array, table.nseg, _lib.pointer_array(grads), counts, len(grads), float(lr), float(momentum),
         float(weight_decay), packed.data_ptr(), partials.data_ptr() if partials is not None else None,
-        widths.data_ptr(), stream_handle(stream)))
+        widths.data_ptr(), _ptr(abort), stream_handle(stream)))
 
 
 def _int32_array(values) -> ctypes.Array:
@@ -372,33 +381,34 @@ def _int32_array(values) -> ctypes.Array:
 
 
 def unpack_multi_dyn(table: SegmentTable, sources: Sequence[int], widths: torch.Tensor,
-                     stream: torch.cuda.Stream | None = None, start_seg: int = -1) -> None:
+                     stream: torch.cuda.Stream | None = None, start_seg: int = -1,
+                     abort: torch.Tensor | None = None) -> None:
     """adt_unpack_multi_ex with device widths: gather-unpack with per-piece
     widths from device memory (and an optional rotated tile walk)."""
     _lib.check(_lib.load().adt_unpack_multi_ex(table.array, table.nseg, _lib.pointer_array(sources), len(sources),
-                                               widths.data_ptr(), int(start_seg), stream_handle(stream)))
+                                               widths.data_ptr(), int(start_seg), _ptr(abort), stream_handle(stream)))
 
 
 def awp_combine(tails: torch.Tensor, piece_layer: torch.Tensor, nlayers: int, sumsq: torch.Tensor,
-                stream: torch.cuda.Stream | None = None) -> None:
+                stream: torch.cuda.Stream | None = None, abort: torch.Tensor | None = None) -> None:
     """adt_awp_combine: per-layer sums from the gathered per-piece sums, rank-major order."""
     _lib.check(_lib.load().adt_awp_combine(tails.data_ptr(), piece_layer.numel(), piece_layer.data_ptr(), nlayers,
-                                           sumsq.data_ptr(), stream_handle(stream)))
+                                           sumsq.data_ptr(), _ptr(abort), stream_handle(stream)))
 
 
 def awp_fixup_pieces(masters: SegmentTable, replicas: SegmentTable, seg_layer: Sequence[int], packed: torch.Tensor,
                      escalated: torch.Tensor, widths_new: torch.Tensor,
-                     stream: torch.cuda.Stream | None = None) -> None:
+                     stream: torch.cuda.Stream | None = None, abort: torch.Tensor | None = None) -> None:
     """adt_awp_fixup_pieces: re-pack this rank's escalated pieces into its send buffer."""
     _lib.check(_lib.load().adt_awp_fixup_pieces(masters.array, replicas.array, masters.nseg, _int32_array(seg_layer),
                                                 packed.data_ptr(), escalated.data_ptr(), widths_new.data_ptr(),
-                                                stream_handle(stream)))
+                                                _ptr(abort), stream_handle(stream)))
 
 
 def awp_fixup_gather(replicas: SegmentTable, seg_layer: Sequence[int], sources: Sequence[int],
                      escalated: torch.Tensor, widths_new: torch.Tensor,
-                     stream: torch.cuda.Stream | None = None) -> None:
+                     stream: torch.cuda.Stream | None = None, abort: torch.Tensor | None = None) -> None:
     """adt_awp_fixup_gather: re-unpack every rank's escalated pieces from their send buffers."""
     _lib.check(_lib.load().adt_awp_fixup_gather(replicas.array, replicas.nseg, _int32_array(seg_layer),
                                                 _lib.pointer_array(sources), len(sources), escalated.data_ptr(),
-                                                widths_new.data_ptr(), stream_handle(stream)))
+                                                widths_new.data_ptr(), _ptr(abort), stream_handle(stream)))

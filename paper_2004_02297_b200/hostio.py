@@ -25,9 +25,8 @@ import torch
 SMALL = 1 << 20            # below this, plain torch copies
 CHUNK = 64 << 20           # staging chunk (bytes)
 THREADS = 16               # host copy threads per chunk (>= 4 MiB each)
-_init_lock = threading.Lock()   # lazy creation of the pool / staging buffers
-_use_lock = threading.Lock()    # one user of the staging buffers at a time
-_staging: dict = {}        # device index -> pinned uint8 tensor of CHUNK bytes
+_init_lock = threading.Lock()   # lazy creation of the pool; the free lists of staging sets
+_staging: dict = {}        # device index -> free staging sets (each: two pinned CHUNK buffers + events)
 _pool = None
 
 _PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
@@ -65,15 +64,28 @@ def _workers() -> ThreadPoolExecutor:
     return _pool
 
 
-def _stage(device: torch.device) -> list:
-    """Two pinned CHUNK-byte buffers per device (double buffering) and their events."""
-    idx = device.index if device.index is not None else torch.cuda.current_device()
-    with _init_lock:
-        st = _staging.get(idx)
-        if st is None:
-            st = _staging[idx] = [(torch.empty(CHUNK, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
-                                  for _ in range(2)]
-        return st
+class _Stage:
+    """A staging set (two pinned CHUNK-byte buffers + their events, double
+    buffering) checked out of the per-device free list for one copy: threads
+    copying at the same time each get their own set (a new one is created
+    when none is free), so host copies never serialise on a shared buffer."""
+
+    def __init__(self, device: torch.device):
+        self.idx = device.index if device.index is not None else torch.cuda.current_device()
+        self.bufs = None
+
+    def __enter__(self) -> list:
+        with _init_lock:
+            free = _staging.setdefault(self.idx, [])
+            self.bufs = free.pop() if free else None
+        if self.bufs is None:
+            self.bufs = [(torch.empty(CHUNK, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+                         for _ in range(2)]
+        return self.bufs
+
+    def __exit__(self, *exc):
+        with _init_lock:
+            _staging[self.idx].append(self.bufs)
 
 
 def _parallel_memmove(dst: int, src: int, nbytes: int) -> None:
@@ -95,9 +107,8 @@ def to_device(host: np.ndarray, device: torch.device | str = "cuda") -> torch.Te
     out = torch.empty(host.size, dtype=torch.from_numpy(host[:1]).dtype, device=dev)
     raw_out = out.view(torch.uint8)
     src = host.ctypes.data
-    bufs = _stage(out.device)
     stream = torch.cuda.current_stream(out.device)
-    with _use_lock:
+    with _Stage(out.device) as bufs:
         for k, pos in enumerate(range(0, host.nbytes, CHUNK)):
             n = min(CHUNK, host.nbytes - pos)
             buf, done = bufs[k & 1]
@@ -111,11 +122,10 @@ def to_device(host: np.ndarray, device: torch.device | str = "cuda") -> torch.Te
 
 def _from_device(dev_bytes: torch.Tensor, dst: int) -> None:
     """Chunk k+1's DMA into one pinned buffer overlaps the copy of chunk k out of the other."""
-    bufs = _stage(dev_bytes.device)
     stream = torch.cuda.current_stream(dev_bytes.device)
     total = dev_bytes.numel()
     chunks = list(range(0, total, CHUNK))
-    with _use_lock:
+    with _Stage(dev_bytes.device) as bufs:
         def issue(k):
             pos = chunks[k]
             buf, done = bufs[k & 1]

@@ -1,0 +1,183 @@
+"""CPU-master weight distribution: the paper's own setting.
+
+The FP32 master weights live in HOST memory (the optimizer updates them on the
+CPU); before every host->GPU transfer they are packed on the CPU (Bitpack,
+PAPER.md:259-268, 351-452: the top RoundTo bytes of every weight), only the
+packed stream crosses PCIe, and the GPU zero-fills the dropped bytes (Bitunpack,
+PAPER.md:454-493). The reference restates the byte semantics in
+codec.pack_vectorized / unpack (codec.py:149-197) and runs the caller order of
+training.py:207-254; this class is that caller order with the codec split
+across the two processors:
+
+    host:   adt_pack_host (all cores, AVX-512 VBMI, l2-norm fused into the read)
+            -> pinned staging buffer, cut into units of 64K weights
+    link:   cudaMemcpyAsync of every finished run of units while the rest is
+            still being packed (Σ n·r bytes instead of 4·Σ n)
+    device: adt_unpack of the whole stream into the FP32 replicas
+
+(one C call, adt_host_to_device). The norms come out of the host pass, so the
+AWP decision (precision.PrecisionController) needs no device->host read.
+Whether this beats copying FP32 depends on the host: the host pass streams
+(4 + r)·n bytes through host DRAM next to the DMA's r·n, against 4·n for a raw
+FP32 copy (bench.py `host_master`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib, engine
+from .layout import PackedLayout
+from .precision import FixedPrecision, PrecisionController
+from .sync import SyncResult, flat_views
+
+HOST_ALIGN = 64        # payload offsets: full 64-B lines for the packer's non-temporal stores
+
+
+def _host_view(m, i: int) -> np.ndarray:
+    """A host master as a flat float32 NumPy view of the caller's own memory
+    (the CPU optimizer updates it in place between steps), never a copy."""
+    if isinstance(m, torch.Tensor):
+        if m.is_cuda:
+            raise TypeError(f"master layer {i}: HostWeightSync takes host (CPU) masters; use WeightSync for "
+                            "device-resident masters")
+        m = m.detach().numpy()
+    if not isinstance(m, np.ndarray) or m.dtype != np.float32:
+        raise TypeError(f"master layer {i}: need a float32 NumPy array or CPU tensor")
+    if not m.flags.c_contiguous:
+        raise ValueError(f"master layer {i}: array is not C-contiguous (a flattened copy would be packed "
+                         "instead of it)")
+    return m.reshape(-1)
+
+
+class HostWeightSync:
+    """Host FP32 masters -> host pack -> packed H2D -> device unpack, per step.
+
+    masters: per-layer float32 host arrays (NumPy or CPU tensors; pinned or
+    not — only the staging buffer needs to be page-locked), read in place.
+    replicas: per-layer CUDA float32 tensors (allocated when omitted).
+    threads: host packer threads (0 = the process's whole CPU affinity).
+    """
+
+    def __init__(self, masters: Sequence, schedule=None, replicas: Sequence[torch.Tensor] | None = None,
+                 device: torch.device | str | None = None, threads: int = 0, min_copy_bytes: int = 1 << 20):
+        engine.require_cuda()
+        self.masters = [_host_view(m, i) for i, m in enumerate(masters)]
+        self.counts = [m.size for m in self.masters]
+        L = len(self.masters)
+        self.schedule = schedule if schedule is not None else FixedPrecision(L, 32)
+        if self.schedule.num_layers != L:
+            raise ValueError("schedule layer count differs from the number of master arrays")
+        self.adaptive = isinstance(self.schedule, PrecisionController)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if replicas is None:
+            replicas = [torch.empty(n, dtype=torch.float32, device=self.device) for n in self.counts]
+        self.replicas = flat_views(replicas, "replica")
+        if [r.numel() for r in self.replicas] != self.counts:
+            raise ValueError("replica sizes differ from the masters")
+        self.threads = int(threads)
+        self.min_copy_bytes = int(min_copy_bytes)
+        cap = PackedLayout.plan(self.counts, [4] * L, align=HOST_ALIGN).nbytes
+        # one pinned staging buffer and one device buffer with room for every
+        # width: a re-plan after an AWP escalation never reallocates
+        self.staging = torch.empty(max(64, cap + 64), dtype=torch.uint8, pin_memory=True)
+        base = (-self.staging.data_ptr()) % 64
+        self._stage_ptr = self.staging.data_ptr() + base        # 64-B aligned stream start
+        self.packed = torch.empty(max(64, cap), dtype=torch.uint8, device=self.device)
+        self.sumsq = np.zeros(max(1, L), dtype=np.float64)
+        self._dma_done = torch.cuda.Event()
+        self._dma_pending = False
+        self._plan(self.schedule.round_tos())
+
+    def _plan(self, round_tos) -> None:
+        self.layout = PackedLayout.plan(self.counts, round_tos, align=HOST_ALIGN)
+        self._host_segs = _lib.segment_array([(m.ctypes.data if n else 0, n, off, r) for m, n, off, r in
+                                              zip(self.masters, self.counts, self.layout.offsets,
+                                                  self.layout.round_tos)])
+        self.unpack_table = engine.SegmentTable(self.replicas, self.layout)
+
+    @property
+    def round_tos(self) -> list[int]:
+        return list(self.layout.round_tos)
+
+    @property
+    def h2d_bytes(self) -> int:
+        """Bytes one transfer moves over the link: the packed stream (payloads + < 64 B pad per layer)."""
+        return self.layout.nbytes
+
+    def launch(self, fused_norm: bool = True, stream: torch.cuda.Stream | None = None) -> None:
+        """One transfer: pack on the host (norms fused when `fused_norm`),
+        copy the packed stream as it is produced, unpack on the device. Returns
+        when the host side is done; the copies and the unpack are queued on
+        `stream` (default: the current stream)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self._dma_pending:
+            self._dma_done.synchronize()         # the staging buffer is free again
+        _lib.check(_lib.load().adt_host_to_device(
+            self._host_segs, self.unpack_table.array, len(self.counts), self._stage_ptr, self.packed.data_ptr(),
+            self.layout.nbytes, self.sumsq.ctypes.data if fused_norm else None, self.threads,
+            self.min_copy_bytes, int(s.cuda_stream)))
+        self._dma_done.record(s)
+        self._dma_pending = True
+
+    def norms(self) -> list[float]:
+        """precision.l2_norm of every master as of the last launch with the norm fused."""
+        return [math.sqrt(v) for v in self.sumsq[:len(self.counts)]]
+
+    def step(self, batch: int = 0, observe: bool | None = None) -> SyncResult:
+        """One batch (training.py:207-254 order, as sync.WeightSync.step): the
+        transfer of the masters at the widths in force, with their norms — the
+        observation of the post-update masters of batch - 1 — then the AWP
+        decision and, if a width escalated, the transfer again at the new widths."""
+        if observe is None:
+            observe = self.adaptive and batch > 0
+        used = self.round_tos
+        self.launch(fused_norm=observe)
+        res = SyncResult(round_tos=used)
+        if not observe:
+            return res
+        res.trace = self.schedule.observe_all(self.norms(), batch=batch - 1)
+        new = self.schedule.round_tos()
+        if new != used:
+            self._plan(new)
+            self.launch(fused_norm=False)
+            res.round_tos = new
+            res.repacked = True
+        return res
+
+    def observe_final(self, batch: int) -> list[tuple]:
+        """The observation after the last update (training.py:246-254): the
+        norms of the masters as they are now, from a host pass (no transfer)."""
+        segs = self._host_segs
+        scratch = np.empty(self.layout.nbytes + 64, dtype=np.uint8)
+        base = (-scratch.ctypes.data) % 64
+        _lib.check(_lib.load().adt_pack_host(segs, len(self.counts), scratch.ctypes.data + base,
+                                              self.sumsq.ctypes.data, self.threads))
+        return self.schedule.observe_all(self.norms(), batch=batch)
+
+
+def pack_host(masters: Sequence, round_tos: Sequence[int], threads: int = 0,
+              align: int = 16) -> tuple[np.ndarray, PackedLayout, np.ndarray]:
+    """adt_pack_host over host arrays: (packed stream as a uint8 array, its
+    layout, per-layer float64 sums of squares). Same bytes as the device pack."""
+    hosts = [_host_view(m, i) for i, m in enumerate(masters)]
+    lay = PackedLayout.plan([h.size for h in hosts], round_tos, align=align)
+    buf = np.empty(lay.nbytes + 64, dtype=np.uint8)
+    base = (-buf.ctypes.data) % 64
+    out = buf[base:base + lay.nbytes]
+    ss = np.zeros(max(1, len(hosts)), dtype=np.float64)
+    segs = _lib.segment_array([(h.ctypes.data if n else 0, n, off, r)
+                               for h, n, off, r in zip(hosts, lay.counts, lay.offsets, lay.round_tos)])
+    _lib.check(_lib.load().adt_pack_host(segs, len(hosts), out.ctypes.data, ss.ctypes.data, int(threads)))
+    return out, lay, ss[:len(hosts)]
+
+
+def host_threads() -> int:
+    n = ctypes.c_int(0)
+    _lib.check(_lib.load().adt_host_threads(ctypes.byref(n)))
+    return int(n.value)

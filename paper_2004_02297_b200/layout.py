@@ -28,21 +28,25 @@ class PackedLayout:
     nbytes: int  # buffer size including inter-layer pad
 
     @staticmethod
-    def plan(counts, round_tos, base: int = 0) -> "PackedLayout":
+    def plan(counts, round_tos, base: int = 0, align: int = ALIGN) -> "PackedLayout":
+        """align: payload offsets are multiples of this (16, or 64 for the host
+        packer's full-line non-temporal stores, hostsync.HostWeightSync)."""
+        if align < ALIGN or align % ALIGN:
+            raise ValueError(f"align must be a multiple of {ALIGN}")
         counts = tuple(int(c) for c in counts)
         round_tos = tuple(int(r) for r in round_tos)
         if len(counts) != len(round_tos):
             raise ValueError("counts and round_tos differ in length")
         offsets = []
-        pos = align_up(base)
+        pos = align_up(base, align)
         for n, r in zip(counts, round_tos):
             if n < 0:
                 raise ValueError(f"negative weight count {n}")
             if not 1 <= r <= 4:
                 raise ValueError(f"round_to must be an integer in [1, 4], got {r}")
             offsets.append(pos)
-            pos = align_up(pos + n * r)
-        return PackedLayout(counts, round_tos, tuple(offsets), pos - align_up(base))
+            pos = align_up(pos + n * r, align)
+        return PackedLayout(counts, round_tos, tuple(offsets), pos - align_up(base, align))
 
     @property
     def num_layers(self) -> int:

@@ -184,6 +184,13 @@ class ChunkedGather:
             :, plan.payload_cap - b:plan.payload_cap - b + 8 * plan.max_pieces]
 
 
+class PeerTimeout(RuntimeError):
+    """A device-side peer barrier gave up waiting for another rank (a stalled
+    or dead peer). The kernels queued behind it did no work (the abort guard),
+    so replicas, masters and the AWP state hold the last good step's values;
+    the exchange cannot continue — rebuild the ShardedWeightSync."""
+
+
 def peer_transport(dist, group=None) -> str:
     """"p2p" when every rank's GPU can map every other rank's memory (NVLink /
     NVSwitch peers on one node: the fused peer-read kernels apply), else
@@ -229,7 +236,7 @@ class ShardedWeightSync:
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None,
                  transport: str = "auto", awp_on_device: bool = False, trace_ring: int = 256,
-                 nccl_chunks: int = 4):
+                 nccl_chunks: int = 4, barrier_timeout_s: float = 30.0):
         """awp_on_device (p2p transport): every rank runs the AWP decision on
         its GPU from the gathered per-piece sums (identical inputs, so
         identical decisions), pieces keep capacity offsets in the send
@@ -239,7 +246,13 @@ class ShardedWeightSync:
 
         nccl_chunks (nccl transport): the packed send buffers are gathered in
         this many byte ranges (ChunkedGather), each unpacked as soon as it
-        lands, so the unpack overlaps the rest of the all-gather."""
+        lands, so the unpack overlaps the rest of the all-gather.
+
+        barrier_timeout_s (p2p transport): how long a device-side barrier waits
+        for the other ranks. On timeout every kernel behind it that reads peer
+        memory skips its work (abort guard) and the next call on this object
+        raises PeerTimeout: each call first waits for the previous step to
+        finish on the device, so the failure surfaces within one step."""
         import torch.distributed as dist
         engine.require_cuda()
         if transport not in ("nccl", "p2p", "auto"):
@@ -249,14 +262,20 @@ class ShardedWeightSync:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.transport = peer_transport(dist, group) if transport == "auto" else transport
-        self.masters = [m.detach().reshape(-1) for m in masters]
+        from .sync import flat_views
+        self.masters = flat_views(masters, "master")
         self.counts = [m.numel() for m in self.masters]
         self.schedule = schedule if schedule is not None else FixedPrecision(len(self.masters), 32)
         self.adaptive = isinstance(self.schedule, PrecisionController)
         self.device = self.masters[0].device
         if replicas is None:
             replicas = [torch.empty_like(m) for m in self.masters]
-        self.replicas = [r.reshape(-1) for r in replicas]
+        self.replicas = flat_views(replicas, "replica")
+        if barrier_timeout_s <= 0:
+            raise ValueError("barrier_timeout_s must be > 0")
+        self.barrier_timeout_s = float(barrier_timeout_s)
+        self._abort = None         # p2p: the barrier's timeout word (device), guard of every peer-reading kernel
+        self._poll_event = None
         self.send = self.recv = None
         self._slot = 0
         self._peer = None      # p2p: per slot, every rank's send-buffer address in this process
@@ -333,26 +352,30 @@ class ShardedWeightSync:
         if observe:
             engine.finalize(self.pack_table, self._partials, self._tail(send), main)
         self._barrier()
+        ab = self._abort
         if observe:
-            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
+            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces, abort=ab)
             self._side.wait_stream(main)
             m = self.plan.max_pieces
             engine.awp_combine(self.tails[:self.world * 8 * m].view(torch.float64), self._piece_layer,
-                               len(self.counts), self._sumsq_dev, self._side)
-            engine.awp_observe(self._sumsq_dev, d.struct, d.config, self._side)
-        engine.unpack_multi_dyn(self.unpack_table, self._peer[slot], self._pw_all, main, start_seg=self._unpack_start)
+                               len(self.counts), self._sumsq_dev, self._side, abort=ab)
+            engine.awp_observe(self._sumsq_dev, d.struct, d.config, self._side, abort=ab)
+        engine.unpack_multi_dyn(self.unpack_table, self._peer[slot], self._pw_all, main, start_seg=self._unpack_start,
+                                abort=ab)
         if observe:
             main.wait_stream(self._side)
             torch.index_select(d.widths_new, 0, self._idx_mine, out=self._pw_mine_new[:len(self._mine_layers)])
             torch.index_select(d.widths_new, 0, self._idx_all, out=self._pw_all_new[:len(self._all_layers)])
             engine.awp_fixup_pieces(self.pack_table, self._my_reps, self._mine_layers, send, d.escalated,
-                                    self._pw_mine_new, main)
+                                    self._pw_mine_new, main, abort=ab)
             self._barrier()
             engine.awp_fixup_gather(self.unpack_table, self._all_layers, self._peer[slot], d.escalated,
-                                    self._pw_all_new, main)
+                                    self._pw_all_new, main, abort=ab)
             d.widths.copy_(d.widths_new)
+        self._mirror_abort()
 
     def _step_device(self, batch: int, observe: bool, graphed: bool = True) -> SyncResult:
+        self._poll_abort()
         d = self._dawp
         if observe and not d.label_set:
             d.set_next_label(batch - 1)
@@ -370,6 +393,7 @@ class ShardedWeightSync:
             g.replay()
         else:
             self._device_step_kernels(slot, observe)
+        self._step_queued()
         if observe:
             d.pending += 1
             if d.pending >= d.ring_steps:
@@ -505,6 +529,10 @@ class ShardedWeightSync:
         returns False everywhere (no rank is left waiting in a collective)."""
         self._flags = torch.zeros(self.world, dtype=torch.int32, device=self.device)
         self._bstate = torch.zeros(2, dtype=torch.int32, device=self.device)
+        self._abort = self._bstate[1:2]
+        self._abort_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._poll_event = torch.cuda.Event()
+        self._poll_pending = False
         handle = engine.ipc_handle(self._flags)
         everyone = [None] * self.world
         self.dist.all_gather_object(everyone, handle, group=self.group)
@@ -535,18 +563,46 @@ class ShardedWeightSync:
         32-thread kernel: each rank stores its epoch into every peer's flag
         array over NVLink and waits for all of them in its own — no NCCL
         launch, no host round trip, capturable in a CUDA graph."""
-        engine.peer_barrier(self._flag_ptrs, self.rank, self._bstate)
+        engine.peer_barrier(self._flag_ptrs, self.rank, self._bstate, timeout_s=self.barrier_timeout_s)
+
+    def _mirror_abort(self) -> None:
+        """Queue the D2H copy of the abort word into pinned memory at the end of
+        a step (captured into the step's graph when capturing)."""
+        if self.transport == "p2p":
+            self._abort_host.copy_(self._abort, non_blocking=True)
+
+    def _step_queued(self) -> None:
+        if self.transport == "p2p":
+            self._poll_event.record()
+            self._poll_pending = True
+
+    def _poll_abort(self) -> None:
+        """Before queueing more work: wait for the previous step (so the host
+        is at most one step ahead of the device) and raise PeerTimeout if its
+        barrier gave up."""
+        if self.transport != "p2p":
+            return
+        if self._poll_pending:
+            self._poll_event.synchronize()
+            self._poll_pending = False
+            if int(self._abort_host[0]):
+                self._aborted = int(self._abort_host[0])
+        if getattr(self, "_aborted", 0):
+            raise PeerTimeout(f"rank {self.rank}: peer barrier epoch {self._aborted} timed out after "
+                              f"{self.barrier_timeout_s:g} s waiting for a peer; the step's peer reads were skipped")
 
     def check_barrier(self) -> None:
-        """Raise if a device barrier gave up waiting for a peer (its bounded
-        wait returns instead of hanging the GPU)."""
+        """Raise PeerTimeout if a device barrier gave up waiting for a peer (its
+        bounded wait returns instead of hanging the GPU). Synchronizes."""
         if self.transport == "p2p":
             bad = int(self._bstate[1].item())
             if bad:
-                raise RuntimeError(f"rank {self.rank}: peer barrier epoch {bad} timed out waiting for a peer")
+                self._aborted = bad
+                raise PeerTimeout(f"rank {self.rank}: peer barrier epoch {bad} timed out waiting for a peer")
 
     def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
         """pack shard (norm finalized into the send tail) -> exchange -> unpack."""
+        self._poll_abort()
         S = self.plan.send_bytes
         if self.transport == "nccl":
             send = self.send[0][:S]
@@ -556,6 +612,7 @@ class ShardedWeightSync:
         slot = self._slot
         self._slot ^= 1
         self._p2p_step(slot, fused_norm, mid_event)
+        self._step_queued()
 
     def _gather_unpack(self, send: torch.Tensor, mid_event=None) -> None:
         """nccl transport: all-gather the packed send buffers chunk by chunk
@@ -589,8 +646,10 @@ class ShardedWeightSync:
         if mid_event is not None:
             mid_event.record(torch.cuda.current_stream())
         if fused_norm:
-            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
-        engine.unpack_multi(self.unpack_table, self._peer[slot], start_seg=self._unpack_start)
+            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces,
+                              abort=self._abort)
+        engine.unpack_multi(self.unpack_table, self._peer[slot], start_seg=self._unpack_start, abort=self._abort)
+        self._mirror_abort()
 
     def launch_graphed(self, fused_norm: bool) -> None:
         """p2p: launch() replayed from CUDA graphs — every op of the step is a
@@ -601,6 +660,7 @@ class ShardedWeightSync:
         if self.transport != "p2p":
             self.launch(fused_norm)
             return
+        self._poll_abort()
         key = (fused_norm, self.plan)
         if getattr(self, "_graphs", None) is None or self._graphs[0] != key:
             graphs = []
@@ -613,6 +673,7 @@ class ShardedWeightSync:
         slot = self._slot
         self._slot ^= 1
         self._graphs[1][slot].replay()
+        self._step_queued()
 
     def _tail(self, send: torch.Tensor) -> torch.Tensor:
         base = self.plan.payload_cap
@@ -702,6 +763,7 @@ class ShardedWeightSync:
             raise ValueError("one sample count per rank")
         if list(bucket.counts) != list(self.counts):
             raise ShapeMismatch("gradient bucket layer sizes differ from the masters")
+        self._poll_abort()
         if self.velocities is None:
             self.velocities = [torch.zeros_like(m) for m in self.masters]
         self._owners_fixed = True
@@ -724,8 +786,9 @@ class ShardedWeightSync:
             def fused(send, widths, partials, stream):
                 self._barrier()                  # every rank's gradients are written
                 engine.reduce_sgd_pack_dyn(table, grads, sample_counts, lr, momentum, weight_decay, send, widths,
-                                           partials, stream)
+                                           partials, stream, abort=self._abort)
             self._device_step_kernels(slot, True, pack=fused)
+            self._step_queued()
             self._check_finite = True
             d.pending += 1
             if d.pending >= d.ring_steps:
@@ -740,13 +803,14 @@ class ShardedWeightSync:
             send = self.send[slot]
             self._barrier()                      # every rank's gradients are written
         engine.reduce_sgd_pack(self._reduce_table, grads, sample_counts, lr, momentum, weight_decay, send,
-                               self._tail(send))
+                               self._tail(send), abort=self._abort)
         if self.transport == "nccl":
             self._gather_unpack(send)
         else:
             self._barrier()                      # every shard is stepped and packed
-            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces)
-            engine.unpack_multi(self.unpack_table, self._peer[slot], start_seg=self._unpack_start)
+            engine.copy_multi(self.tails, self._peer[slot], self.plan.payload_cap, 8 * self.plan.max_pieces,
+                              abort=self._abort)
+            engine.unpack_multi(self.unpack_table, self._peer[slot], start_seg=self._unpack_start, abort=self._abort)
         used = self.round_tos
         res = SyncResult(round_tos=used)
         norms = self._norms()

@@ -32,7 +32,29 @@ from .precision import FixedPrecision, PrecisionController
 
 
 class NonFiniteParameters(FloatingPointError):
-    """net.py:20 — an update left a layer's weights outside the finite range."""
+    """net.py:20 — an update left a layer's weights outside the finite range.
+
+    Raised after the step that produced the non-finite weights has been
+    applied to every layer (one fused kernel steps all layers; the check reads
+    the fused norms afterwards), whereas the reference raises at the first bad
+    layer before updating the later ones (net.py:246-257): when it is raised
+    here, masters and velocities of every layer hold the post-step values."""
+
+
+def flat_views(tensors: Sequence[torch.Tensor], what: str) -> list[torch.Tensor]:
+    """1-D views of the caller's CUDA float32 tensors. A non-contiguous tensor
+    (e.g. a transposed weight) is refused: flattening it would copy, and the
+    in-place updates and unpacks would then land in the copy, not in the
+    caller's tensor."""
+    out = []
+    for i, t in enumerate(tensors):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+            raise TypeError(f"{what} layer {i}: need a CUDA float32 tensor")
+        if not t.is_contiguous():
+            raise ValueError(f"{what} layer {i}: tensor is not contiguous (its flattened copy would be written "
+                             "instead of it); pass .contiguous() storage")
+        out.append(t.detach().view(-1))
+    return out
 
 
 @dataclass
@@ -61,10 +83,7 @@ class WeightSync:
         each payload is still exactly the reference's n*r bytes."""
         engine.require_cuda()
         self.graphed = graphed
-        self.masters = [m.detach().reshape(-1) for m in masters]
-        for i, m in enumerate(self.masters):
-            if not m.is_cuda or m.dtype != torch.float32 or not m.is_contiguous():
-                raise TypeError(f"master layer {i}: need a contiguous CUDA float32 tensor")
+        self.masters = flat_views(masters, "master")
         self.counts = [m.numel() for m in self.masters]
         self.schedule = schedule if schedule is not None else FixedPrecision(len(self.masters), 32)
         if self.schedule.num_layers != len(self.masters):
@@ -73,7 +92,7 @@ class WeightSync:
         dev = self.masters[0].device if self.masters else torch.device("cuda")
         if replicas is None:
             replicas = [torch.empty_like(m) for m in self.masters]
-        self.replicas = [r.reshape(-1) for r in replicas]
+        self.replicas = flat_views(replicas, "replica")
         self.sumsq = torch.zeros(len(self.masters), dtype=torch.float64, device=dev)
         self._host_sumsq = torch.empty(len(self.masters), dtype=torch.float64, pin_memory=True)
         # The norm finalize (a tiny per-layer reduction of the pack's partials)
@@ -357,6 +376,12 @@ class WeightSync:
         the widths in force and fuses its norms; the norms are observed and,
         if a width escalated, W_{b+1} is re-packed (without updating again).
         The replicas then hold batch b+1's weights.
+
+        `grads` is the ALREADY AVERAGED gradient, applied as is. The
+        reference's gather_and_update (net.py:203-257) always forms
+        pairwise_sum(g_c * f32(n_c)) / f32(total), even for one contribution,
+        and g * n / n is not always bit-equal to g in float32: for bit parity
+        with the reference use gather_and_update([GradientSet(g, [], n)]).
         """
         if len(grads) != len(self.masters):
             from .grads import ShapeMismatch
@@ -470,6 +495,9 @@ class WeightSync:
             engine.sumsq(self._cap_pack, self.sumsq)
             d.set_next_label(batch)
             engine.awp_observe(self.sumsq, d.struct, d.config)
+            # an escalation decided by this last observation is in force from now
+            # on (round_tos, any later step): widths A <- B, as every step does
+            d.widths.copy_(d.widths_new)
             self._trace_log = rows          # kept for the next drain_trace(); return only this observation
             last = d.drain()
             return last

@@ -67,7 +67,7 @@ def trace_to_device(n=37748736):
     for _ in range(3):
         out = torch.empty(n, dtype=torch.float32, device="cuda")
         raw_out = out.view(torch.uint8)
-        bufs = hostio._stage(out.device)
+        bufs = hostio._Stage(out.device).__enter__()
         stream = torch.cuda.current_stream()
         t = [time.perf_counter()]
         log = []

@@ -97,19 +97,16 @@ def test_validation_happens_before_any_device_work(lib):
         return arr
     C = ctypes.c_int64
     cnt = (C * 17)(*([1] * 17))
-    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 0, 0.1, 0.9, 0.0, 16, None, None, None) \
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 0, 0.1, 0.9, 0.0, 16, None, None, None, None) \
         == lib.ADT_ERR_ARG
-    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48] * 17), cnt, 17, 0.1, 0.9, 0.0, 16, None, None,
-                                 None) == lib.ADT_ERR_ARG
-    assert h.adt_reduce_sgd_pack(red(5), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None) \
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48] * 17), cnt, 17, 0.1, 0.9, 0.0, 16, None, None, None, None) == lib.ADT_ERR_ARG
+    assert h.adt_reduce_sgd_pack(red(5), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None, None) \
         == lib.ADT_ERR_ROUND_TO
-    assert h.adt_reduce_sgd_pack(red(2, goff=8), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None,
-                                 None) == lib.ADT_ERR_ALIGN
-    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([40]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None) \
+    assert h.adt_reduce_sgd_pack(red(2, goff=8), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([40]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None, None) \
         == lib.ADT_ERR_ALIGN
-    assert h.adt_reduce_sgd_pack(red(2, wptr=8), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None,
-                                 None) == lib.ADT_ERR_ALIGN
-    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, 16, None, None) \
+    assert h.adt_reduce_sgd_pack(red(2, wptr=8), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, None, None, None, None) == lib.ADT_ERR_ALIGN
+    assert h.adt_reduce_sgd_pack(red(2), 1, lib.pointer_array([48]), cnt, 1, 0.1, 0.9, 0.0, 16, 16, None, None, None) \
         == lib.ADT_ERR_ARG
     # peer barrier: rank outside [0, nranks), too many ranks, misaligned flags, zero poll budget
     assert h.adt_peer_barrier(lib.pointer_array([16, 32]), 2, 2, 48, 10, None) == lib.ADT_ERR_ARG
@@ -123,6 +120,6 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_unpack_dyn(lib.segment_array([(16, 10, 0, 3)]), 1, 16, 32, None) == lib.ADT_ERR_ARG
     dev = lib.AwpDevice()
     cfg = lib.AwpConfig(-2e-3, 50, 8, 32, 0)
-    assert h.adt_awp_observe(16, ctypes.byref(dev), ctypes.byref(cfg), None) == lib.ADT_ERR_ARG   # empty device struct
+    assert h.adt_awp_observe(16, ctypes.byref(dev), ctypes.byref(cfg), None, None) == lib.ADT_ERR_ARG   # empty device struct
     m, r = lib.segment_array([(16, 10, 0, 4)]), lib.segment_array([(48, 10, 16, 4)])
     assert h.adt_awp_fixup(m, r, 1, 16, 64, 80, None) == lib.ADT_ERR_ARG                        # offsets differ

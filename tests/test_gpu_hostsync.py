@@ -1,0 +1,121 @@
+"""The CPU-master path end to end on a B200 (the paper's setting,
+PAPER.md:219-229): host FP32 masters -> adt_pack_host on the host cores ->
+packed stream over PCIe while the rest is packed -> adt_unpack on the GPU.
+Replicas must equal the reference's unpack(pack(W)) bit for bit, norms its
+l2_norm, and the AWP walk must take the reference run's decisions."""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import weightpack_oracle as O
+
+pytestmark = pytest.mark.gpu
+NORM_RTOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def adt():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2004_02297_b200 as adt
+    return adt
+
+
+def test_replicas_and_norms_mixed_widths(adt):
+    rng = np.random.default_rng(3)
+    counts = [20 * 25, 50 * 20 * 25, 4097, 0, 65536 * 3 + 11, 10 * 500, 3]
+    rs = [1, 2, 3, 4, 4, 1, 3]
+    hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+    hosts[4][:12] = np.array(O.SPECIAL_WORDS, np.uint32).view(np.float32)
+
+    class Fixed(adt.FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32))
+    for _ in range(3):                        # repeated transfers reuse the staging buffer
+        for r_ in sync.replicas:
+            r_.fill_(float("nan"))
+        sync.launch(fused_norm=True)
+        torch.cuda.synchronize()
+        for i, (h, r) in enumerate(zip(hosts, rs)):
+            want = h.view(np.uint32) & np.uint32(O.keep_mask(r))
+            assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), i
+    norms = sync.norms()
+    for i, h in enumerate(hosts):
+        if i == 4:
+            assert math.isnan(norms[i])       # NaN payloads in the specials: the reference's norm is NaN too
+            continue
+        ref = O.l2_norm(h)
+        assert abs(norms[i] - ref) <= NORM_RTOL * max(ref, 1e-30), i
+    assert sync.h2d_bytes < 4 * sum(counts)
+
+
+def test_large_set_in_many_copies(adt):
+    """A stream much larger than one copy batch: the DMA of early units overlaps
+    the packing of later ones; every byte must still land once, in order."""
+    rng = np.random.default_rng(8)
+    counts = [5_000_000, 3_000_001, 777_777]
+    rs = [3, 1, 2]
+    hosts = [rng.integers(0, 1 << 32, n, dtype=np.uint32).view(np.float32) for n in counts]
+
+    class Fixed(adt.FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32), min_copy_bytes=64 << 10)
+    sync.launch(fused_norm=False)
+    torch.cuda.synchronize()
+    for i, (h, r) in enumerate(zip(hosts, rs)):
+        want = h.view(np.uint32) & np.uint32(O.keep_mask(r))
+        assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), i
+    dev = sync.packed.cpu().numpy()
+    for i, (h, r) in enumerate(zip(hosts, rs)):
+        lo, hi = sync.layout.span(i)
+        assert dev[lo:hi].tobytes() == O.pack_vectorized(h, r)
+
+
+def test_lenet_awp_walk_host_masters(adt, golden_lenet):
+    """SURVEY §8d config 1 through the CPU-master path: the host arrays are the
+    masters (updated in place), norms come from the host pass, widths / trace
+    rows / payloads / replicas equal the reference run's."""
+    steps = int(golden_lenet["steps"])
+    walk = list(O.lenet_walk(steps, seed=7))
+    L = len(walk[0][1])
+    cfg = adt.PrecisionConfig(threshold=-2e-3, interval=int(golden_lenet["interval"]), step_bits=8, initial_bits=8)
+    masters = [w.copy() for w in walk[0][1]]
+    sync = adt.HostWeightSync(masters, adt.PrecisionController(L, cfg))
+    trace = []
+    for t in range(steps):
+        for m, w in zip(masters, walk[t][1]):
+            m[...] = w
+        res = sync.step(batch=t)
+        trace += res.trace
+        assert res.round_tos == list(golden_lenet["widths"][t]), t
+        torch.cuda.synchronize()
+        dev = sync.packed.cpu().numpy()
+        for i in range(L):
+            lo, hi = sync.layout.span(i)
+            assert hashlib.sha256(dev[lo:hi].tobytes()).digest() == golden_lenet["payload_sha"][t, i].tobytes()
+            rep = sync.replicas[i].cpu().numpy()
+            assert hashlib.sha256(rep.tobytes()).digest() == golden_lenet["unpacked_sha"][t, i].tobytes()
+    for m, w in zip(masters, walk[steps][1]):
+        m[...] = w
+    trace += sync.observe_final(batch=steps - 1)
+    assert len(trace) == steps * L
+    for k, (b, layer, norm, delta, counter, bits) in enumerate(trace):
+        t, i = divmod(k, L)
+        assert (b, layer) == (t, i)
+        assert bits == golden_lenet["bits"][t, i] and counter == golden_lenet["counter"][t, i], (t, i)
+        assert abs(norm - golden_lenet["norms"][t, i]) <= NORM_RTOL * golden_lenet["norms"][t, i]
+
+
+def test_rejects_device_and_strided_masters(adt):
+    with pytest.raises(TypeError):
+        adt.HostWeightSync([torch.zeros(8, device="cuda")])
+    with pytest.raises(ValueError):
+        adt.HostWeightSync([np.zeros((4, 6), np.float32).T])

@@ -174,9 +174,125 @@ def test_peer_barrier_two_virtual_ranks_and_timeout(adt):
         assert flags[r].tolist() == [5, 5]
     lone = torch.zeros(2, dtype=torch.int32, device="cuda")
     lone_flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
-    engine.peer_barrier([f.data_ptr() for f in lone_flags], 0, lone, max_polls=2000)
+    engine.peer_barrier([f.data_ptr() for f in lone_flags], 0, lone, timeout_s=0.05)
     torch.cuda.synchronize()
     assert lone.tolist() == [1, 1]             # epoch 1 published, and its wait timed out
+    # the timeout word guards every peer-reading kernel queued behind it: none does any work
+    from paper_2004_02297_b200.layout import PackedLayout
+    lay = PackedLayout.plan([5000], [2])
+    src = torch.randint(0, 255, (lay.nbytes,), dtype=torch.uint8, device="cuda")
+    out = torch.full((5000,), 7.0, device="cuda")
+    table = engine.SegmentTable([out], lay, sources=[0])
+    engine.unpack_multi(table, [src.data_ptr()], abort=lone[1:2])
+    dst = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    engine.copy_multi(dst, [src.data_ptr()], 0, 64, abort=lone[1:2])
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    engine.peer_barrier([f.data_ptr() for f in lone_flags], 0, lone, timeout_s=5.0)   # fails fast now
+    t1.record()
+    torch.cuda.synchronize()
+    assert torch.all(out == 7.0) and torch.all(dst == 0)
+    assert lone.tolist() == [2, 1] and t0.elapsed_time(t1) < 100.0
+    engine.unpack_multi(table, [src.data_ptr()], abort=states[0][1:2])   # a clear word: the kernel runs
+    torch.cuda.synchronize()
+    assert not torch.all(out == 7.0)
+
+
+def _stall_main(rank, world, port, q, stall, release, mode):
+    """Two ranks step together, then rank 1 stalls (stops calling; stays alive).
+    Rank 0 must raise PeerTimeout within one step, with replicas and masters
+    left exactly as the last good step wrote them: mode "step" (the failing
+    step returns, the next call raises) or "update" (the failing update raises
+    itself: it reads the norms back)."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2004_02297_b200.grads import GradBucket
+        from paper_2004_02297_b200.precision import FixedPrecision
+        from paper_2004_02297_b200.sharded import PeerTimeout, ShardedWeightSync
+        counts = [500, 3 * 4096 + 17, 25000]
+        rng = np.random.default_rng(5)
+        hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+        masters = [torch.from_numpy(h.copy()).cuda() for h in hosts]
+
+        class Mixed(FixedPrecision):
+            def round_tos(self):
+                return [1, 3, 2]
+
+        sync = ShardedWeightSync(masters, Mixed(len(counts), 32), transport="p2p", barrier_timeout_s=1.0)
+        bucket = GradBucket(counts, torch.device("cuda"))
+        bucket.flat.normal_(0.0, 0.01)
+        for b in range(3):
+            sync.step(batch=b)
+        sync.update(bucket, [64, 64], lr=0.1)     # maps the peers' gradient buckets (a collective)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 1:
+            stall.set()
+            release.wait(120)                 # alive (memory still mapped), but not stepping
+            q.put((rank, True, [], None))
+            return
+        stall.wait(60)
+        reps = [r.clone() for r in sync.replicas]
+        before = [m.clone() for m in masters]
+        notes, raised_at = [], None
+        if mode == "step":
+            for m in masters:
+                m.mul_(2.0)                   # a completed step would change every replica
+            before = [m.clone() for m in masters]
+            for call in range(4):
+                try:
+                    sync.step(batch=3 + call)
+                except PeerTimeout:
+                    raised_at = call
+                    break
+            if raised_at != 1:
+                notes.append(f"PeerTimeout at call {raised_at}, expected 1 (the call after the failed step)")
+        else:
+            try:
+                sync.update(bucket, [64, 64], lr=0.1)
+                notes.append("the update whose barrier timed out did not raise")
+            except PeerTimeout:
+                raised_at = 0
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(zip(reps, sync.replicas)):
+            if not torch.equal(a, b):
+                notes.append(f"replica {i} changed by the failed step")
+        if any(not torch.equal(a, b) for a, b in zip(before, masters)):
+            notes.append("masters stepped with stale gradients")
+        for fn in (lambda: sync.step(batch=9), lambda: sync.update(bucket, [64, 64], lr=0.1)):
+            try:
+                fn()
+                notes.append("a call after the timeout did not raise")
+            except PeerTimeout:
+                pass
+        release.set()
+        q.put((rank, not notes, notes, raised_at))
+    except Exception as e:  # surface child failures to the parent
+        release.set()
+        q.put((rank, False, [repr(e)], None))
+
+
+@pytest.mark.parametrize("mode", ["step", "update"])
+def test_p2p_stalled_peer_raises_within_one_step(mode):
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    stall, release = ctx.Event(), ctx.Event()
+    port = _free_port()
+    procs = [ctx.Process(target=_stall_main, args=(r, 2, port, q, stall, release, mode)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, notes, _ in res:
+        assert ok, (rank, notes)
 
 
 def _graphed_main(rank, world, port, q):
