@@ -500,6 +500,15 @@ def main_ours(args):
                     "pack_ms": pk, "unpack_ms": up,
                     "pack_GBps": pack_bytes / (pk * 1e-3) / 1e9, "unpack_GBps": unpack_bytes / (up * 1e-3) / 1e9}
 
+    if roofline is not None:
+        roofline["frac_spec"] = roofline["achieved"] / SPEC_HBM_GBPS
+        if roofline.get("traffic"):
+            dram = roofline["traffic"] / (dur * 1e-3) / 1e9
+            roofline["dram_GBps"] = dram
+            roofline["dram_frac"] = dram / hbm
+        if world == 1 and not args.quiet_extra:
+            roofline["cold"] = run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, not args.no_norm)
+
     # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
     e2e = e2e_dropin = e2e_fp32_h2d = None
     if not args.no_e2e and world == 1:
@@ -558,6 +567,65 @@ def main_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+SPEC_HBM_GBPS = 8000.0     # B200 HBM3e nominal (DGX figure; B200_PROFILING.md), for frac_spec
+
+
+def _graph_ms(fns, reps=10, rounds=5):
+    """Median over `rounds` replays of one CUDA graph holding `reps` copies of
+    the sequence `fns` -> device ms per copy (events only around the replay)."""
+    import torch
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            for f in fns:
+                f()
+    g.replay()
+    out = []
+    for _ in range(rounds):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        out.append(a.elapsed_time(b) / reps)
+    return sorted(out)[len(out) // 2]
+
+
+def run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, fused_norm=True):
+    """SURVEY §8d cold-L2 per-kernel figures: every launch preceded by a READ
+    of a 2xL2 buffer (L2 then holds only clean, unrelated lines, so each kernel
+    reads its inputs from DRAM and its dirty output is written back during the
+    next flush — counted against it). Kernel time = T[flush, kernel] - T[flush],
+    both from CUDA graphs of 10 copies (median of 5 replays)."""
+    import torch
+    from paper_2004_02297_b200 import engine
+    dev = sync.device
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    scratch = torch.ones(2 * l2 // 4, dtype=torch.float32, device=dev)
+    sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def flush():
+        torch.sum(scratch, dim=0, out=sink)
+
+    def pack():
+        engine.pack(sync.pack_table, sync.packed, None, torch.cuda.current_stream(),
+                    partials=sync._partials if fused_norm else None)
+
+    def unpack():
+        engine.unpack(sync.unpack_table, sync.packed, torch.cuda.current_stream())
+
+    f = _graph_ms([flush])
+    p = _graph_ms([flush, pack]) - f
+    u = _graph_ms([flush, unpack]) - f
+    pg, ug = pack_bytes / (p * 1e-3) / 1e9, unpack_bytes / (u * 1e-3) / 1e9
+    return {"pack_ms": p, "unpack_ms": u, "pack_GBps": pg, "unpack_GBps": ug, "pack_frac": pg / hbm,
+            "unpack_frac": ug / hbm, "frac": min(pg, ug) / hbm, "frac_spec": min(pg, ug) / SPEC_HBM_GBPS,
+            "flush_ms": f, "method": "T[2xL2 read flush + kernel] - T[flush], CUDA graphs of 10, median of 5"}
 
 
 def traffic_of(kernel, args):

@@ -344,7 +344,7 @@ int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *se
  * packed stream (>= min_copy_bytes, 0 = 1 MiB) into dev_packed, so the PCIe
  * DMA overlaps the packing; then adt_unpack of dev_segs (device replicas, the
  * same counts / offsets / round_to, payloads in increasing offset order) from
- * dev_packed. Only Σ n·r (+ pad) bytes cross the link instead of 4n.
+ * dev_packed — or no unpack when dev_segs is NULL (the caller queues it). Only Σ n·r (+ pad) bytes cross the link instead of 4n.
  * Returns once the host work is done and the copies + unpack are queued: the
  * caller must not rewrite host_packed before `stream` has passed this point.
  * seg_sumsq (host memory) receives the per-layer sums of squares.
@@ -357,6 +357,16 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
 int adt_host_threads(int *n);
 /* 512 when the host packer runs its AVX-512 VBMI path, 0 for the scalar path. */
 int adt_host_simd(void);
+
+/*
+ * Float64-input norm: *out = sum of x[i]^2 over n float64 words (device
+ * memory, 8-B aligned) — precision.l2_norm (precision.py:25-28) of an array
+ * that is not float32 (the reference converts any array-like to float64).
+ * Fixed grid and reduction order: bit-identical run to run. `partials` holds
+ * adt_sumsq_f64_partials(n) doubles of scratch.
+ */
+int adt_sumsq_f64_partials(uint64_t n, uint64_t *npartials);
+int adt_sumsq_f64(const double *x, uint64_t n, double *partials, double *out, void *stream);
 
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);

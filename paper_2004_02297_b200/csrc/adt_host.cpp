@@ -362,11 +362,14 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
                        uint64_t min_copy_bytes, void *stream) {
     int v = validate_host(host_segs, nseg, host_packed);
     if (v != ADT_OK) return v;
-    if (nseg > 0 && (dev_segs == nullptr || dev_packed == nullptr)) return ADT_ERR_ARG;
+    if (nseg > 0 && dev_packed == nullptr) return ADT_ERR_ARG;
     uint64_t end_prev = 0;                    // payloads in increasing, non-overlapping order (the DMA
     for (int i = 0; i < nseg; ++i) {          // ships the stream front to back as units complete)
-        const adt_segment &h = host_segs[i], &d = dev_segs[i];
-        if (h.count != d.count || h.offset != d.offset || h.round_to != d.round_to) return ADT_ERR_ARG;
+        const adt_segment &h = host_segs[i];
+        if (dev_segs != nullptr) {
+            const adt_segment &d = dev_segs[i];
+            if (h.count != d.count || h.offset != d.offset || h.round_to != d.round_to) return ADT_ERR_ARG;
+        }
         if (h.count == 0) continue;
         const uint64_t end = h.offset + h.count * static_cast<uint64_t>(h.round_to);
         if (h.offset < end_prev || end > packed_bytes) return ADT_ERR_ARG;
@@ -394,7 +397,7 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
     });
     finish_sums(units, ss, nseg, seg_sumsq);
     if (err != cudaSuccess) return ADT_ERR_CUDA_BASE - static_cast<int>(err);
-    return adt_unpack(dev_segs, nseg, dev_packed, stream);
+    return dev_segs == nullptr ? ADT_OK : adt_unpack(dev_segs, nseg, dev_packed, stream);
 }
 
 }  // extern "C"

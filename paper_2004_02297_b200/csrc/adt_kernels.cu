@@ -603,6 +603,7 @@ namespace {
 
 #include "adt_peer.cuh"
 #include "adt_awp.cuh"
+#include "adt_f64.cuh"
 
 // ----------------------------------------------------------------- host side
 enum class Pass { Pack, PackNorm, Norm, Unpack, Finalize };
@@ -1348,6 +1349,29 @@ int adt_awp_combine(const double *tails, int npieces_total, const int32_t *piece
         return ADT_ERR_ARG;
     adt_awp_combine_kernel<<<(nlayers + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         tails, npieces_total, piece_layer, nlayers, seg_sumsq, abort);
+    return cuda_status(cudaGetLastError());
+}
+
+int adt_sumsq_f64_partials(uint64_t n, uint64_t *npartials) {
+    if (npartials == nullptr) return ADT_ERR_ARG;
+    *npartials = static_cast<uint64_t>(f64_ctas(n));
+    return ADT_OK;
+}
+
+int adt_sumsq_f64(const double *x, uint64_t n, double *partials, double *out, void *stream) {
+    if (out == nullptr || partials == nullptr || (n > 0 && x == nullptr)) return ADT_ERR_ARG;
+    if (reinterpret_cast<uintptr_t>(x) % 8) return ADT_ERR_ALIGN;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int ctas = f64_ctas(n);
+    if (n > 0) {
+        adt_sumsq_f64_kernel<<<ctas, kF64Threads, 0, s>>>(x, n, partials);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_status(e);
+        adt_sumsq_f64_finalize<<<1, 32, 0, s>>>(partials, ctas, out);
+    } else {
+        cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+        if (e != cudaSuccess) return cuda_status(e);
+    }
     return cuda_status(cudaGetLastError());
 }
 

@@ -313,6 +313,21 @@ def sumsq(table: SegmentTable, out: torch.Tensor, stream: torch.cuda.Stream | No
     _lib.check(_lib.load().adt_sumsq(table.array, table.nseg, out.data_ptr(), parts.data_ptr(), sh))
 
 
+def sumsq_f64(x: torch.Tensor, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_sumsq_f64: out[0] = float64 sum of squares of the float64 CUDA tensor x."""
+    if x.dtype != torch.float64 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("x must be a contiguous CUDA float64 tensor")
+    if out.dtype != torch.float64 or not out.is_cuda or out.numel() < 1:
+        raise ValueError("out must be a CUDA float64 tensor")
+    lib = _lib.load()
+    np_ = ctypes.c_uint64(0)
+    _lib.check(lib.adt_sumsq_f64_partials(x.numel(), ctypes.byref(np_)))
+    sh = stream_handle(stream)
+    parts = _Scratch.get(x.device, sh, int(np_.value))
+    _lib.check(lib.adt_sumsq_f64(x.data_ptr() if x.numel() else None, x.numel(), parts.data_ptr(), out.data_ptr(),
+                                 sh))
+
+
 def sm_count() -> int:
     v = ctypes.c_int(0)
     _lib.check(_lib.load().adt_device_sm_count(ctypes.byref(v)))

@@ -110,18 +110,26 @@ class HostWeightSync:
         """Bytes one transfer moves over the link: the packed stream (payloads + < 64 B pad per layer)."""
         return self.layout.nbytes
 
-    def launch(self, fused_norm: bool = True, stream: torch.cuda.Stream | None = None) -> None:
+    def launch(self, fused_norm: bool = True, stream: torch.cuda.Stream | None = None, events=None) -> None:
         """One transfer: pack on the host (norms fused when `fused_norm`),
         copy the packed stream as it is produced, unpack on the device. Returns
         when the host side is done; the copies and the unpack are queued on
-        `stream` (default: the current stream)."""
+        `stream` (default: the current stream). events = (e0, e1, e2): timing
+        events recorded before the copies, between the copies and the unpack,
+        and after the unpack (transfer.LedgerRecorder)."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         if self._dma_pending:
             self._dma_done.synchronize()         # the staging buffer is free again
+        if events is not None:
+            events[0].record(s)
         _lib.check(_lib.load().adt_host_to_device(
-            self._host_segs, self.unpack_table.array, len(self.counts), self._stage_ptr, self.packed.data_ptr(),
-            self.layout.nbytes, self.sumsq.ctypes.data if fused_norm else None, self.threads,
-            self.min_copy_bytes, int(s.cuda_stream)))
+            self._host_segs, self.unpack_table.array if events is None else None, len(self.counts), self._stage_ptr,
+            self.packed.data_ptr(), self.layout.nbytes, self.sumsq.ctypes.data if fused_norm else None,
+            self.threads, self.min_copy_bytes, int(s.cuda_stream)))
+        if events is not None:
+            events[1].record(s)
+            engine.unpack(self.unpack_table, self.packed, s)
+            events[2].record(s)
         self._dma_done.record(s)
         self._dma_pending = True
 
@@ -129,7 +137,7 @@ class HostWeightSync:
         """precision.l2_norm of every master as of the last launch with the norm fused."""
         return [math.sqrt(v) for v in self.sumsq[:len(self.counts)]]
 
-    def step(self, batch: int = 0, observe: bool | None = None) -> SyncResult:
+    def step(self, batch: int = 0, observe: bool | None = None, events=None) -> SyncResult:
         """One batch (training.py:207-254 order, as sync.WeightSync.step): the
         transfer of the masters at the widths in force, with their norms — the
         observation of the post-update masters of batch - 1 — then the AWP
@@ -137,7 +145,7 @@ class HostWeightSync:
         if observe is None:
             observe = self.adaptive and batch > 0
         used = self.round_tos
-        self.launch(fused_norm=observe)
+        self.launch(fused_norm=observe, events=events)
         res = SyncResult(round_tos=used)
         if not observe:
             return res

@@ -342,17 +342,26 @@ class WeightSync:
         self._side.synchronize()
         return [math.sqrt(v) for v in self._host_sumsq.tolist()]
 
-    def step(self, batch: int = 0, observe: bool | None = None) -> SyncResult:
-        """One batch of weight distribution (see module doc for the ordering)."""
+    def step(self, batch: int = 0, observe: bool | None = None, events=None) -> SyncResult:
+        """One batch of weight distribution (see module doc for the ordering).
+        events = (e0, e1, e2): CUDA timing events recorded before the pack,
+        between pack and unpack, and after the unpack (transfer.LedgerRecorder)."""
         if observe is None:
             observe = self.adaptive and batch > 0
         if self.awp_on_device:
+            if events is not None:
+                raise ValueError("per-phase events need the host-planned step (awp_on_device=False)")
             return self._step_device(batch, observe)
         used = self.round_tos
+        main = torch.cuda.current_stream()
+        if events is not None:
+            events[0].record(main)
         if self.graphed:
-            self.launch_graphed(fused_norm=observe)
+            self.launch_graphed(fused_norm=observe, mid_event=events[1] if events is not None else None)
         else:
-            self.launch(fused_norm=observe)
+            self.launch(fused_norm=observe, mid_event=events[1] if events is not None else None)
+        if events is not None:
+            events[2].record(main)
         res = SyncResult(round_tos=used)
         if not observe:
             return res

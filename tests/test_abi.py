@@ -31,7 +31,8 @@ def test_header_declares_the_expected_surface():
          "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn",
          "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn", "adt_awp_observe", "adt_awp_fixup",
          "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces", "adt_awp_fixup_gather",
-         "adt_device_sm_count"])
+         "adt_device_sm_count", "adt_pack_host", "adt_host_to_device", "adt_host_threads", "adt_host_simd",
+         "adt_sumsq_f64_partials", "adt_sumsq_f64"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -123,3 +124,26 @@ def test_validation_happens_before_any_device_work(lib):
     assert h.adt_awp_observe(16, ctypes.byref(dev), ctypes.byref(cfg), None, None) == lib.ADT_ERR_ARG   # empty device struct
     m, r = lib.segment_array([(16, 10, 0, 4)]), lib.segment_array([(48, 10, 16, 4)])
     assert h.adt_awp_fixup(m, r, 1, 16, 64, 80, None) == lib.ADT_ERR_ARG                        # offsets differ
+
+
+def test_host_entry_points_validate_arguments(lib):
+    """adt_pack_host / adt_host_to_device / adt_sumsq_f64 refuse bad input
+    before doing any work (host pointers, no device needed)."""
+    h = lib.load()
+    bad_r = lib.segment_array([(16, 10, 0, 5)])
+    assert h.adt_pack_host(bad_r, 1, 16, None, 0) == lib.ADT_ERR_ROUND_TO
+    assert h.adt_pack_host(lib.segment_array([(18, 10, 0, 2)]), 1, 16, None, 0) == lib.ADT_ERR_ALIGN
+    assert h.adt_pack_host(lib.segment_array([(16, 10, 0, 2)]), 1, None, None, 0) == lib.ADT_ERR_ARG
+    assert h.adt_pack_host(None, -1, None, None, 0) == lib.ADT_ERR_ARG
+    segs = lib.segment_array([(16, 10, 0, 2), (32, 10, 0, 2)])          # overlapping payloads
+    assert h.adt_host_to_device(segs, segs, 2, 64, 64, 1 << 20, None, 0, 0, None) == lib.ADT_ERR_ARG
+    one = lib.segment_array([(16, 10, 0, 2)])
+    other = lib.segment_array([(16, 10, 0, 3)])                          # device side disagrees
+    assert h.adt_host_to_device(one, other, 1, 64, 64, 1 << 20, None, 0, 0, None) == lib.ADT_ERR_ARG
+    assert h.adt_host_to_device(one, one, 1, 64, 64, 8, None, 0, 0, None) == lib.ADT_ERR_ARG   # stream too short
+    assert h.adt_sumsq_f64(None, 10, 16, 16, None) == lib.ADT_ERR_ARG
+    assert h.adt_sumsq_f64(12, 10, 16, 16, None) == lib.ADT_ERR_ALIGN
+    n = ctypes.c_uint64(0)
+    assert h.adt_sumsq_f64_partials(10 ** 9, ctypes.byref(n)) == lib.ADT_OK and 1 <= n.value <= 1184
+    t = ctypes.c_int(0)
+    assert h.adt_host_threads(ctypes.byref(t)) == lib.ADT_OK and t.value == len(os.sched_getaffinity(0))

@@ -580,3 +580,27 @@ def test_trace_csv_byte_identical_across_reruns(adt):
 
     a, b, c = run(False), run(False), run(True)
     assert a == b == c and len(a.splitlines()) == 1 + 39 * L
+
+
+def test_l2_norm_any_array_like_float64(adt):
+    """precision.py:25-28 takes ANY array-like (np.asarray(float64)): float64,
+    float16 and integer inputs go through the float64-input kernel and match
+    the reference's float64 norm to 1e-12; float32 stays on the exact path."""
+    rng = np.random.default_rng(12)
+    x64 = rng.standard_normal(10 ** 6)
+    ref = O.l2_norm(x64)
+    assert abs(adt.l2_norm(x64) - ref) <= 1e-12 * ref
+    assert abs(adt.l2_norm(torch.from_numpy(x64).cuda()) - ref) <= 1e-12 * ref
+    assert abs(adt.l2_norm(x64.tolist()[:1000]) - O.l2_norm(x64[:1000])) <= 1e-12 * O.l2_norm(x64[:1000])
+    ints = rng.integers(-1000, 1000, 12345)
+    assert abs(adt.l2_norm(ints) - O.l2_norm(ints)) <= 1e-12 * O.l2_norm(ints)
+    h = rng.standard_normal(5000).astype(np.float16)
+    assert abs(adt.l2_norm(h) - O.l2_norm(h)) <= 1e-12 * O.l2_norm(h)
+    assert adt.l2_norm(np.zeros(0)) == 0.0 and adt.l2_norm([3.0, 4.0]) == 5.0
+    assert math.isnan(adt.l2_norm(np.array([1.0, np.nan])))
+    big = rng.standard_normal(3 * 10 ** 7)               # many CTAs: fixed order, bit-identical reruns
+    a, b = adt.l2_norm(big), adt.l2_norm(big)
+    assert a == b and abs(a - O.l2_norm(big)) <= 1e-12 * a
+    many = adt.l2_norm_many([x64, x64.astype(np.float32), ints])
+    assert many[0] == adt.l2_norm(x64) and many[2] == adt.l2_norm(ints)
+    assert abs(many[1] - O.l2_norm(x64.astype(np.float32))) <= 1e-12 * many[1]
