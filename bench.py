@@ -394,8 +394,10 @@ def main_ours(args):
         plan = sync.plan
         pack_bytes = sum((pc.hi - pc.lo) * (4 + plan.round_tos[pc.layer]) for pc in plan.pieces[rank])
         unpack_bytes = sum((4 + r) * n for n, r in zip(counts, rs))
-    # ours per step: pack, unpack, norm finalize; p2p adds the peer barrier and the norm-tail gather
-    kernels_per_step = 2 + (0 if args.no_norm else 1)
+    # ours per step: pack, unpack, norm finalize (small sets: the one adt_roundtrip launch);
+    # p2p adds the peer barrier and the norm-tail gather
+    small = world == 1 and getattr(sync, "_small", False)
+    kernels_per_step = 1 if small else 2 + (0 if args.no_norm else 1)
     if world > 1 and getattr(sync, "transport", "") == "p2p":
         kernels_per_step += 1 + (0 if args.no_norm else 1)
     elif world > 1:                               # nccl: one unpack per gathered chunk
@@ -435,6 +437,10 @@ def main_ours(args):
             torch.cuda.synchronize()
             return ev
 
+        if world == 1 and not args.quiet_extra:       # capture the split graphs outside the timed passes
+            sync.launch_graphed(fused, mid_event=torch.cuda.Event(enable_timing=True))
+            run_step(fused)
+            torch.cuda.synchronize()
         with ClockSampler(local) as clocks:
             step_ms = [a.elapsed_time(c) for a, _, c in flushed(False)]
         flushed_split = None
@@ -489,7 +495,14 @@ def main_ours(args):
         up = sum(up_list) / len(up_list)
     hbm, peak_kind = peaks()
     roofline = None
-    if pk is not None:
+    if small:
+        # the step IS one kernel (adt_roundtrip): its duration is the step's
+        dom, dur, byts = "adt_roundtrip_kernel", ms, total_bytes
+        roofline = {"bound": "hbm", "achieved": byts / (dur * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": byts / (dur * 1e-3) / 1e9 / hbm, "traffic": traffic_of(dom, args), "kernel": dom,
+                    "peak_source": f"{peak_kind} hbm_gbs (burst copy)", "step_kernels": 1,
+                    "split_two_kernel_path": {"pack_ms": pk, "unpack_ms": up} if pk is not None else None}
+    elif pk is not None:
         if world == 1:
             dom, dur, byts = ("adt_unpack_kernel", up, unpack_bytes) if up >= pk else ("adt_pack_kernel", pk, pack_bytes)
         else:
@@ -506,7 +519,7 @@ def main_ours(args):
             dram = roofline["traffic"] / (dur * 1e-3) / 1e9
             roofline["dram_GBps"] = dram
             roofline["dram_frac"] = dram / hbm
-        if world == 1 and not args.quiet_extra:
+        if world == 1 and not args.quiet_extra and not small:
             roofline["cold"] = run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, not args.no_norm)
 
     # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
@@ -597,35 +610,49 @@ def _graph_ms(fns, reps=10, rounds=5):
 
 
 def run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, fused_norm=True):
-    """SURVEY §8d cold-L2 per-kernel figures: every launch preceded by a READ
-    of a 2xL2 buffer (L2 then holds only clean, unrelated lines, so each kernel
-    reads its inputs from DRAM and its dirty output is written back during the
-    next flush — counted against it). Kernel time = T[flush, kernel] - T[flush],
-    both from CUDA graphs of 10 copies (median of 5 replays)."""
+    """SURVEY §8d cold-L2 per-kernel figures, by rotation: K independent
+    copies of the step's buffers (masters, packed stream, replicas; K = 4, or
+    2 when a copy is over 1 GB) and one CUDA graph of `reps` x K launches that
+    cycles through them — pack(0), pack(1), ..., pack(K-1), pack(0), ... Every
+    launch reads inputs last touched K-1 launches (>= 3 x its own traffic, well
+    over the 126 MB L2) earlier, i.e. from DRAM, and the write-backs of the
+    previous launches' outputs land inside the timed region: steady-state
+    streaming, nothing left in L2 for free. Same for the unpack. Median of 5
+    replays; per-launch ms = replay time / (reps x K)."""
     import torch
     from paper_2004_02297_b200 import engine
     dev = sync.device
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    scratch = torch.ones(2 * l2 // 4, dtype=torch.float32, device=dev)
-    sink = torch.empty((), dtype=torch.float32, device=dev)
+    lay = sync.layout
+    foot = 4 * sum(lay.counts) * 2 + lay.nbytes
+    K = 4 if foot < (1 << 30) else 2
+    sets = []
+    for k in range(K):
+        masters = [m.clone() for m in sync.masters]
+        reps = [torch.empty_like(m) for m in sync.masters]
+        packed = torch.empty_like(sync.packed)
+        parts = torch.empty_like(sync._partials)
+        sets.append((engine.SegmentTable(masters, lay), engine.SegmentTable(reps, lay), packed, parts))
+    stream = torch.cuda.current_stream()
+    for ptab, utab, packed, parts in sets:           # every packed copy holds a real stream
+        engine.pack(ptab, packed, None, stream, partials=parts)
+    reps_per = max(2, 8 // K)
 
-    def flush():
-        torch.sum(scratch, dim=0, out=sink)
+    def packs():
+        for ptab, _, packed, parts in sets:
+            engine.pack(ptab, packed, None, stream, partials=parts if fused_norm else None)
 
-    def pack():
-        engine.pack(sync.pack_table, sync.packed, None, torch.cuda.current_stream(),
-                    partials=sync._partials if fused_norm else None)
+    def unpacks():
+        for _, utab, packed, _ in sets:
+            engine.unpack(utab, packed, stream)
 
-    def unpack():
-        engine.unpack(sync.unpack_table, sync.packed, torch.cuda.current_stream())
-
-    f = _graph_ms([flush])
-    p = _graph_ms([flush, pack]) - f
-    u = _graph_ms([flush, unpack]) - f
+    p = _graph_ms([packs], reps=reps_per) / K
+    u = _graph_ms([unpacks], reps=reps_per) / K
     pg, ug = pack_bytes / (p * 1e-3) / 1e9, unpack_bytes / (u * 1e-3) / 1e9
+    del sets
+    torch.cuda.empty_cache()
     return {"pack_ms": p, "unpack_ms": u, "pack_GBps": pg, "unpack_GBps": ug, "pack_frac": pg / hbm,
             "unpack_frac": ug / hbm, "frac": min(pg, ug) / hbm, "frac_spec": min(pg, ug) / SPEC_HBM_GBPS,
-            "flush_ms": f, "method": "T[2xL2 read flush + kernel] - T[flush], CUDA graphs of 10, median of 5"}
+            "method": f"rotation over {K} buffer sets, CUDA graph of {reps_per * K} launches, median of 5 replays"}
 
 
 def traffic_of(kernel, args):
@@ -963,12 +990,22 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
         def round_tos(self):
             return list(rs)
 
+    import numpy as np
     sync = adt.HostWeightSync(host, Fixed(len(host), 32), device=dev)
     stream = torch.cuda.current_stream(dev)
+    # the step's result lives on the GPU (the replicas): each step reads back the
+    # last 4 words of the last replica (16 B D2H, which also completes the step)
+    # and checks them against the host masters truncated to their width
+    tail_dev = sync.replicas[-1][-4:]
+    tail_host = torch.empty(4, dtype=torch.float32, pin_memory=True)
+    want = (host[-1][-4:].view(np.uint32) & np.uint32((0xFFFFFFFF << (8 * (4 - rs[-1]))) & 0xFFFFFFFF))
 
     def one():
         sync.launch(fused_norm=True)
+        tail_host.copy_(tail_dev, non_blocking=True)
         stream.synchronize()
+        if not np.array_equal(tail_host.numpy().view(np.uint32), want):
+            raise AssertionError("host-master e2e: the replica read back differs from the packed masters")
 
     for _ in range(3):
         one()
@@ -980,12 +1017,12 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
     # the same host arrays as one raw FP32 pinned copy would move: the baseline
     n = sum(h.size for h in host)
     byts = 2 * sum((4 + r) * h.size for h, r in zip(host, rs))
-    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": sync.h2d_bytes, "d2h_bytes_per_step": 0,
+    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": sync.h2d_bytes, "d2h_bytes_per_step": 16,
             "ms_per_step": dt * 1e3, "steps": steps, "host_threads": host_threads(),
             "raw_fp32_bytes": 4 * n,
             "note": "HostWeightSync: host FP32 masters -> adt_pack_host (all host cores, norms fused) -> packed "
-                    "H2D overlapped with the packing -> adt_unpack; wall clock; norms computed on the host, "
-                    "so no device->host read"}
+                    "H2D overlapped with the packing -> adt_unpack -> 16 B read-back check; wall clock; the "
+                    "norms come from the host pass"}
 
 
 def run_e2e_weightsync(args, dev_masters, rs, dev):

@@ -368,6 +368,21 @@ int adt_host_simd(void);
 int adt_sumsq_f64_partials(uint64_t n, uint64_t *npartials);
 int adt_sumsq_f64(const double *x, uint64_t n, double *partials, double *out, void *stream);
 
+/*
+ * One-launch step for small sets (latency-bound: LeNet is 106 tiles): pack
+ * masters -> packed with the fused norm, grid barrier, unpack packed ->
+ * replicas (each CTA unpacks a tile another CTA packed), per-layer sums of
+ * squares -> seg_sumsq (same fixed order as adt_norm_finalize). Same results as
+ * adt_pack(+finalize) followed by adt_unpack. Requires nseg <= 16 and at most
+ * adt_roundtrip_max_tiles() tiles (one CTA per SM, launched cooperatively, so
+ * the grid barrier never waits on an unscheduled CTA); ADT_ERR_ARG otherwise.
+ * barrier: 2 uint32 of device memory, zero-initialised once, owned by the
+ * caller and not shared by concurrent launches. partials: adt_partials_count.
+ */
+int adt_roundtrip(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
+                  double *seg_sumsq, double *partials, uint32_t *barrier, void *stream);
+int adt_roundtrip_max_tiles(int *tiles);
+
 /* Number of SMs of the current device (cached). */
 int adt_device_sm_count(int *sm_count);
 

@@ -32,7 +32,7 @@ EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", 
            "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn", "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn",
            "adt_awp_observe", "adt_awp_fixup", "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces",
            "adt_awp_fixup_gather", "adt_device_sm_count", "adt_pack_host", "adt_host_to_device", "adt_host_threads",
-           "adt_host_simd", "adt_sumsq_f64_partials", "adt_sumsq_f64")
+           "adt_host_simd", "adt_sumsq_f64_partials", "adt_sumsq_f64", "adt_roundtrip", "adt_roundtrip_max_tiles")
 
 
 class Segment(ctypes.Structure):
@@ -211,6 +211,10 @@ def load() -> ctypes.CDLL:
         lib.adt_host_simd.argtypes = []
         lib.adt_sumsq_f64_partials.restype = ctypes.c_int
         lib.adt_sumsq_f64_partials.argtypes = [ctypes.c_uint64, P(ctypes.c_uint64)]
+        lib.adt_roundtrip.restype = ctypes.c_int
+        lib.adt_roundtrip.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, vp, vp, vp]
+        lib.adt_roundtrip_max_tiles.restype = ctypes.c_int
+        lib.adt_roundtrip_max_tiles.argtypes = [P(ctypes.c_int)]
         lib.adt_sumsq_f64.restype = ctypes.c_int
         lib.adt_sumsq_f64.argtypes = [vp, ctypes.c_uint64, vp, vp, vp]
         if lib.adt_abi_version() != ABI_VERSION:

@@ -333,6 +333,7 @@ __device__ __forceinline__ void st_packed(V *a, V x) {
     else *a = x;
 }
 
+template <bool BULK = (ADT_PACK_BULK_STORE != 0)>
 __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec], uint32_t m, int r, int warp,
                                              int lane, uint32_t g0, uint32_t *ws) {
     if (!ADT_PACK_STAGE_ALL && m == kTile && r != 3) {
@@ -377,6 +378,12 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
     }
     const uint32_t span = kWarpGroups * 4 * r;            // the warp's packed bytes
     const uint32_t lo = warp * span, nbytes = m * r;
+    if (!BULK) {                                          // plain generic-proxy stores (adt_roundtrip)
+        __syncwarp();
+        if (lo < nbytes) warp_store_bytes(ws, dst + lo, min(span, nbytes - lo), lane);
+        __syncwarp();
+        return;
+    }
 #if ADT_PACK_BULK_STORE
     // The warp's 16-B-multiple part leaves shared memory as ONE bulk async copy
     // (cp.async.bulk shared->global, SASS UBLKCP) issued by lane 0; the ragged
@@ -423,7 +430,7 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
 #define ADT_PERSISTENT 0
 #endif
 
-template <int MAXSEG, bool NORM, bool WRITE>
+template <int MAXSEG, bool NORM, bool WRITE, bool BULK = (ADT_PACK_BULK_STORE != 0)>
 __device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
@@ -452,7 +459,7 @@ __device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile,
         }
     }
 
-    if (WRITE) store_packed(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
+    if (WRITE) store_packed<BULK>(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
 
     if (NORM) warp_partial(T.partials, tile, sumsq16(v));
 }
@@ -592,6 +599,69 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     }
 }
 
+
+// ---------------------------------------------- small sets: one launch per step
+// Sets of at most one tile per SM (LeNet: 106 tiles) are latency-bound: three
+// dependent launches (pack, finalize, unpack) cost more than their bytes. One
+// cooperative launch does the whole step: every CTA packs one tile (norm
+// partials fused, plain stores), a grid barrier, then every CTA unpacks the
+// tile packed by CTA ntiles-1-b (reading another CTA's bytes back from global
+// memory: the same round trip as the two-kernel step), and CTA l < nseg sums
+// layer l's partials in the fixed (tile, warp) order of adt_norm_finalize.
+template <int MAXSEG>
+struct RoundTable {
+    Table<MAXSEG> P;          // masters -> packed stream (P.weights = masters, P.packed_out, partials, seg_sumsq)
+    Table<MAXSEG> U;          // packed stream -> replicas (U.weights = replicas, U.srcs[0] = packed)
+    uint32_t *barrier;        // [2]: arrivals, generation (zero-initialised, caller-owned)
+};
+
+__device__ __forceinline__ void grid_barrier(uint32_t *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t *gen = bar + 1;
+        const uint32_t g = *gen;
+        __threadfence();                                   // this CTA's packed bytes and partials
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);                        // release the generation
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int MAXSEG>
+__global__ void __launch_bounds__(kThreads)
+adt_roundtrip_kernel(const __grid_constant__ RoundTable<MAXSEG> R, uint32_t ntiles) {
+    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    __shared__ double red[kWarpsPerTile];
+    uint32_t *ws = stage[threadIdx.x >> 5];
+    const uint32_t tile = blockIdx.x;
+    pack_tile<MAXSEG, true, true, false>(R.P, tile, find_segment(R.P, tile), ws);
+    grid_barrier(R.barrier);
+    const uint32_t ut = ntiles - 1 - tile;
+    unpack_tile<MAXSEG>(R.U, ut, find_segment(R.U, ut), ws);
+    if (static_cast<int>(blockIdx.x) < R.P.nseg && R.P.seg_sumsq != nullptr) {
+        const int s = blockIdx.x;
+        const uint32_t lo = R.P.tile_begin[s] * kWarpsPerTile;
+        const uint32_t n = (R.P.tile_begin[s + 1] - R.P.tile_begin[s]) * kWarpsPerTile;
+        double a = 0.0;
+        for (uint32_t i = threadIdx.x; i < n; i += kThreads) a += R.P.partials[lo + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarpsPerTile; ++w) t += red[w];
+            R.P.seg_sumsq[s] = t;
+        }
+    }
+}
 
 #include "adt_sgd.cuh"
 
@@ -1373,6 +1443,72 @@ int adt_sumsq_f64(const double *x, uint64_t n, double *partials, double *out, vo
         if (e != cudaSuccess) return cuda_status(e);
     }
     return cuda_status(cudaGetLastError());
+}
+
+}  // extern "C"
+
+namespace {
+// Fill a Table<16> from segments (adt_roundtrip): tile map, hints, widths.
+uint32_t fill_small_table(Table<kSmallSeg> &T, const adt_segment *segs, int nseg) {
+    memset(&T, 0, sizeof(T));
+    T.nseg = nseg;
+    uint32_t acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+        T.tile_begin[i] = acc;
+        acc += static_cast<uint32_t>((segs[i].count + kTile - 1) / kTile);
+        T.count[i] = segs[i].count;
+        T.offset[i] = segs[i].offset;
+        T.weights[i] = reinterpret_cast<uintptr_t>(segs[i].weights);
+        T.round_to[i] = static_cast<uint8_t>(segs[i].round_to);
+    }
+    T.tile_begin[nseg] = acc;
+    fill_hints(T, nseg, acc);
+    return acc;
+}
+}  // namespace
+
+extern "C" {
+
+int adt_roundtrip_max_tiles(int *tiles) {
+    if (tiles == nullptr) return ADT_ERR_ARG;
+    int sms = 0;
+    const int st = sm_count_cached(&sms);
+    if (st != ADT_OK) return st;
+    *tiles = sms;                                  // one resident CTA per SM: co-residency by construction
+    return ADT_OK;
+}
+
+int adt_roundtrip(const adt_segment *masters, const adt_segment *replicas, int nseg, uint8_t *packed,
+                  double *seg_sumsq, double *partials, uint32_t *barrier, void *stream) {
+    int v = validate(masters, nseg, packed, true);
+    if (v != ADT_OK) return v;
+    if ((v = validate(replicas, nseg, packed, true)) != ADT_OK) return v;
+    if (nseg < 1 || nseg > kSmallSeg || partials == nullptr || barrier == nullptr) return ADT_ERR_ARG;
+    for (int i = 0; i < nseg; ++i)
+        if (masters[i].count != replicas[i].count || masters[i].offset != replicas[i].offset ||
+            masters[i].round_to != replicas[i].round_to)
+            return ADT_ERR_ARG;
+    RoundTable<kSmallSeg> R;
+    const uint32_t ntiles = fill_small_table(R.P, masters, nseg);
+    fill_small_table(R.U, replicas, nseg);
+    int cap = 0;
+    if ((v = adt_roundtrip_max_tiles(&cap)) != ADT_OK) return v;
+    if (ntiles == 0 || ntiles > static_cast<uint32_t>(cap)) return ADT_ERR_ARG;
+    R.P.packed_out = packed;
+    R.P.partials = partials;
+    R.P.seg_sumsq = seg_sumsq;
+    R.U.srcs[0] = packed;
+    R.barrier = barrier;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (the grid barrier)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_status(cudaLaunchKernelEx(&cfg, adt_roundtrip_kernel<kSmallSeg>, R, ntiles));
 }
 
 int adt_device_sm_count(int *sm_count) {

@@ -328,6 +328,23 @@ def sumsq_f64(x: torch.Tensor, out: torch.Tensor, stream: torch.cuda.Stream | No
                                  sh))
 
 
+def roundtrip_max_tiles() -> int:
+    v = ctypes.c_int(0)
+    _lib.check(_lib.load().adt_roundtrip_max_tiles(ctypes.byref(v)))
+    return int(v.value)
+
+
+def roundtrip(masters: SegmentTable, replicas: SegmentTable, packed: torch.Tensor, sumsq: torch.Tensor | None,
+              partials: torch.Tensor, barrier: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """adt_roundtrip: the whole single-GPU step of a small set in one launch
+    (pack with fused norms -> grid barrier -> unpack -> per-layer sums)."""
+    if barrier.dtype != torch.int32 or not barrier.is_cuda or barrier.numel() < 2:
+        raise ValueError("barrier must be a CUDA int32 tensor of 2 zeros")
+    _lib.check(_lib.load().adt_roundtrip(masters.array, replicas.array, masters.nseg, packed.data_ptr(),
+                                         sumsq.data_ptr() if sumsq is not None else None, partials.data_ptr(),
+                                         barrier.data_ptr(), stream_handle(stream)))
+
+
 def sm_count() -> int:
     v = ctypes.c_int(0)
     _lib.check(_lib.load().adt_device_sm_count(ctypes.byref(v)))

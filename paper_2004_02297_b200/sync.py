@@ -69,7 +69,7 @@ class WeightSync:
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None,
                  replicas: Sequence[torch.Tensor] | None = None, graphed: bool = True,
-                 awp_on_device: bool = False, trace_ring: int = 256):
+                 awp_on_device: bool = False, trace_ring: int = 256, fuse_small: bool = True):
         """graphed: step() replays its kernels from a CUDA graph captured once
         per packed layout (one graph launch instead of three ctypes launches
         and the stream bookkeeping per step).
@@ -80,9 +80,17 @@ class WeightSync:
         and the trace rows come back in batches through drain_trace() (at the
         latest every `trace_ring` observations, automatically). Layers keep
         fixed capacity offsets in the packed buffer (room for 4 bytes/weight);
-        each payload is still exactly the reference's n*r bytes."""
+        each payload is still exactly the reference's n*r bytes.
+
+        fuse_small: sets of at most one 4096-weight tile per SM and <= 16
+        layers (LeNet) run the whole step as ONE cooperative launch
+        (adt_roundtrip: pack + norms, grid barrier, unpack) instead of three
+        dependent launches — the same bytes, norms and replicas."""
         engine.require_cuda()
         self.graphed = graphed
+        self.fuse_small = bool(fuse_small)
+        self._small = False
+        self._rt_barrier = None
         self.masters = flat_views(masters, "master")
         self.counts = [m.numel() for m in self.masters]
         self.schedule = schedule if schedule is not None else FixedPrecision(len(self.masters), 32)
@@ -101,7 +109,7 @@ class WeightSync:
         self._fin_done = torch.cuda.Event()
         self._fin_pending = False
         self._partials = None
-        self._graphs = None      # (key, pack graph, finalize+unpack graph)
+        self._graphs = None      # {(fused_norm, split): graphs} for the current layout
         self.velocities = None   # momentum buffers, created by the first update()
         self._grad_stage = {}    # gather_and_update: staging buckets for per-layer gradient lists
         self._reduce_table = None
@@ -215,6 +223,11 @@ class WeightSync:
         self.unpack_table = engine.SegmentTable(self.replicas, self.layout)
         if self._partials is None or self._partials.numel() < self.pack_table.npartials:
             self._partials = torch.empty(max(1, self.pack_table.npartials), dtype=torch.float64, device=self.device)
+        ntiles = self.pack_table.npartials // 8
+        self._small = (self.fuse_small and 0 < ntiles <= engine.roundtrip_max_tiles()
+                       and 1 <= len(self.counts) <= 16)
+        if self._small and self._rt_barrier is None:
+            self._rt_barrier = torch.zeros(2, dtype=torch.int32, device=self.device)
 
     @property
     def round_tos(self) -> list[int]:
@@ -224,9 +237,18 @@ class WeightSync:
 
     def launch(self, fused_norm: bool, mid_event: torch.cuda.Event | None = None) -> None:
         """The device work of one step on the current stream, no host sync:
-        pack (+ norm partials), [side stream: finalize -> self.sumsq], unpack."""
+        pack (+ norm partials), [side stream: finalize -> self.sumsq], unpack
+        (small sets without a requested pack/unpack split: one adt_roundtrip)."""
         self._host_widths_only()
         main = torch.cuda.current_stream()
+        if self._small and mid_event is None:
+            if self._fin_pending:
+                main.wait_event(self._fin_done)
+            engine.roundtrip(self.pack_table, self.unpack_table, self.packed, self.sumsq if fused_norm else None,
+                             self._partials, self._rt_barrier, main)
+            self._fin_done.record(main)
+            self._fin_pending = True
+            return
         if fused_norm:
             if self._fin_pending:
                 main.wait_event(self._fin_done)  # previous finalize done reading the partials
@@ -254,10 +276,12 @@ class WeightSync:
         cost (ctypes + stream bookkeeping): LeNet 39.6 -> 18.7 us per step."""
         self._host_widths_only()
         split = mid_event is not None
-        key = (fused_norm, split, self.layout)
-        if self._graphs is None or self._graphs[0] != key:
-            self._graphs = (key, self._capture(fused_norm, split))
-        graphs = self._graphs[1]
+        key = (fused_norm, split)
+        if self._graphs is None:
+            self._graphs = {}                # per (fused_norm, split); dropped by every re-plan
+        graphs = self._graphs.get(key)
+        if graphs is None:
+            graphs = self._graphs[key] = self._capture(fused_norm, split)
         graphs[0].replay()
         if split:
             mid_event.record(torch.cuda.current_stream())
@@ -323,8 +347,13 @@ class WeightSync:
         if not split:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                pack()
-                rest()
+                if self._small:                  # the one-launch step (adt_roundtrip)
+                    engine.roundtrip(self.pack_table, self.unpack_table, self.packed,
+                                     self.sumsq if fused_norm else None, self._partials, self._rt_barrier,
+                                     torch.cuda.current_stream())
+                else:
+                    pack()
+                    rest()
             return (g,)
         g_pack, g_rest = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_pack):

@@ -604,3 +604,40 @@ def test_l2_norm_any_array_like_float64(adt):
     many = adt.l2_norm_many([x64, x64.astype(np.float32), ints])
     assert many[0] == adt.l2_norm(x64) and many[2] == adt.l2_norm(ints)
     assert abs(many[1] - O.l2_norm(x64.astype(np.float32))) <= 1e-12 * many[1]
+
+
+def test_one_launch_small_step_matches_three_launch_step(adt):
+    """adt_roundtrip (pack + norms, grid barrier, unpack, per-layer sums in one
+    cooperative launch) gives the same packed bytes, replicas and bit-identical
+    norms as pack -> finalize -> unpack, across many graph replays (the grid
+    barrier is reused launch after launch), up to the one-tile-per-SM limit."""
+    from paper_2004_02297_b200 import engine
+    rng = np.random.default_rng(21)
+    limit = engine.roundtrip_max_tiles()
+    for counts, rs in (([20 * 25, 50 * 20 * 25, 500 * 800, 10 * 500], [1, 2, 3, 4]),
+                       ([4096 * (limit - 2), 5000, 3], [3, 1, 2]),
+                       ([4096 * limit + 1], [2])):          # one tile over the limit: the 3-launch step
+        hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+        outs = []
+        for fuse in (True, False):
+            class Fixed(adt.FixedPrecision):
+                def round_tos(self):
+                    return list(rs)
+            sync = adt.WeightSync([torch.from_numpy(h.copy()).cuda() for h in hosts], Fixed(len(counts), 32),
+                                  fuse_small=fuse)
+            for _ in range(300):
+                sync.launch_graphed(fused_norm=True)
+            norms = sync.read_norms()
+            torch.cuda.synchronize()
+            outs.append((sync._small, sync.packed[:sync.layout.nbytes].cpu().numpy(),
+                         [r.cpu().numpy().view(np.uint32) for r in sync.replicas], norms, sync.layout))
+        (small, pk_a, rep_a, n_a, lay), (_, pk_b, rep_b, n_b, _) = outs
+        assert small == (sum((n + 4095) // 4096 for n in counts) <= limit)
+        for i, (h, r) in enumerate(zip(hosts, rs)):
+            lo, hi = lay.span(i)
+            assert pk_a[lo:hi].tobytes() == pk_b[lo:hi].tobytes() == O.pack_vectorized(h, r)
+            assert np.array_equal(rep_a[i], h.view(np.uint32) & np.uint32(O.keep_mask(r)))
+            assert np.array_equal(rep_a[i], rep_b[i])
+        assert n_a == n_b                                       # same fixed summation order
+        for h, n in zip(hosts, n_a):
+            assert abs(n - O.l2_norm(h)) <= 1e-6 * O.l2_norm(h)
