@@ -347,10 +347,17 @@ def main_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # communicator lines for the driver's rank check (NCCL's INIT log) and one
+        # line per rank of our own, whichever transport carries the weights
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        print(f"[bench] rank {rank} of world {dist.get_world_size()} (local rank {local}, {backend}) on "
+              f"{torch.cuda.get_device_name(dev)} pci {torch.cuda.get_device_properties(dev).pci_bus_id}",
+              file=sys.stderr, flush=True)
 
     import paper_2004_02297_b200 as adt
     from paper_2004_02297_b200 import engine
@@ -549,12 +556,18 @@ def main_ours(args):
     exchange = None
     if world > 1:
         # SURVEY §8e report: packed bytes each rank receives from its peers per
-        # step and the bus rate over the whole step (nccl-tests busbw convention)
+        # step and the bus rate over the whole step (nccl-tests busbw convention),
+        # and the same step at 32 bits over the same transport: the target is
+        # sync(P, widths) / sync_fp32(P) = Σ n·r / 4 Σ n
         payload = sum(n * r for n, r in zip(counts, rs))
         per_rank = payload - sync.plan.rank_payload_bytes(rank)
+        fp32_ms = run_fp32_sync(sync, masters, replicas, K, dev, backend, args)
         exchange = {"packed_bytes_total": payload, "bytes_received_per_rank": per_rank,
                     "busbw_GBps": payload * (world - 1) / world / (ms * 1e-3) / 1e9,
-                    "pack_ms": pk, "gather_unpack_ms": up, "sync_ms": ms}
+                    "pack_ms": pk, "gather_unpack_ms": up, "sync_ms": ms,
+                    "fp32_sync_ms": fp32_ms, "transport": sync.transport,
+                    "target_ratio": payload / (4 * sum(counts)),
+                    "achieved_ratio": (ms / fp32_ms) if fp32_ms else None}
     dp = None
     if world > 1 and not args.no_reduce:
         dp = run_dp_update(sync, counts, world, dev, backend)
@@ -632,18 +645,17 @@ def run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, fused_norm=True):
         packed = torch.empty_like(sync.packed)
         parts = torch.empty_like(sync._partials)
         sets.append((engine.SegmentTable(masters, lay), engine.SegmentTable(reps, lay), packed, parts))
-    stream = torch.cuda.current_stream()
     for ptab, utab, packed, parts in sets:           # every packed copy holds a real stream
-        engine.pack(ptab, packed, None, stream, partials=parts)
+        engine.pack(ptab, packed, None, torch.cuda.current_stream(), partials=parts)
     reps_per = max(2, 8 // K)
 
-    def packs():
+    def packs():                                     # current stream: the capture stream inside _graph_ms
         for ptab, _, packed, parts in sets:
-            engine.pack(ptab, packed, None, stream, partials=parts if fused_norm else None)
+            engine.pack(ptab, packed, None, torch.cuda.current_stream(), partials=parts if fused_norm else None)
 
     def unpacks():
         for _, utab, packed, _ in sets:
-            engine.unpack(utab, packed, stream)
+            engine.unpack(utab, packed, torch.cuda.current_stream())
 
     p = _graph_ms([packs], reps=reps_per) / K
     u = _graph_ms([unpacks], reps=reps_per) / K
@@ -881,6 +893,34 @@ def run_dp_update(sync, counts, world, dev, backend, reps=10):
     return {"ms": a, "fp32_ddp_ms": b, "speedup": b / a, "transport": sync.transport,
             "note": "ShardedWeightSync.update (fused reduce+SGD+pack, packed gather, unpack, AWP observe) vs "
                     "FP32 all_reduce + torch momentum step; device ms per step, max over ranks"}
+
+
+def run_fp32_sync(sync, masters, replicas, K, dev, backend, args):
+    """The N > 1 baseline on the SAME transport: ShardedWeightSync at 32 bits
+    (r = 4: the packed stream is the FP32 words, byte-swapped) — the raw
+    FP32 weight exchange through the same pack / barrier / gather-unpack
+    kernels. Device ms per step (K steps between two events), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2004_02297_b200.precision import FixedPrecision
+    from paper_2004_02297_b200.sharded import ShardedWeightSync
+    full = ShardedWeightSync(masters, FixedPrecision(len(masters), 32), replicas, transport=sync.transport)
+    for _ in range(args.warmup):
+        full.launch_graphed(True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        full.launch_graphed(True)
+    b.record()
+    b.synchronize()
+    if hasattr(full, "check_barrier"):
+        full.check_barrier()
+    t = torch.tensor([a.elapsed_time(b) / K], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del full
+    return float(t.item())
 
 
 def run_fp32_allgather(counts, world, dev, reps=20):

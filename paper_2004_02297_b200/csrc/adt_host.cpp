@@ -109,10 +109,33 @@ ADT_AVX512 inline void put(uint8_t *dst, __m512i v) {
     else _mm512_storeu_si512(dst, v);
 }
 
+// Software prefetch of the masters ahead of the loads. The fused norm
+// (VCVTPS2PD + FMA) lengthens each iteration, so the out-of-order window holds
+// fewer loads in flight and one core's stream falls to a fraction of what the
+// host DRAM delivers; prefetching into L2 several KB ahead restores the memory
+// parallelism (ADT_HOST_PF = distance in bytes, 0 = off; ADT_HOST_PF_HINT =
+// 0 for L1, 1 for L2 — scripts/host_pack_probe.py sweeps them).
+int prefetch_bytes() {
+    static const int v = [] {
+        const char *e = getenv("ADT_HOST_PF");
+        return e != nullptr ? atoi(e) : 8192;
+    }();
+    return v;
+}
+bool prefetch_l2() {
+    static const bool v = [] {
+        const char *e = getenv("ADT_HOST_PF_HINT");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return v;
+}
+
 // Pack n words (n multiple of 64) into dst; returns the float64 sum of squares.
 template <int R, bool NT>
 ADT_AVX512 double pack_avx512(const uint32_t *src, uint64_t n, uint8_t *dst) {
     const PermTables &T = perm();
+    const int pf = prefetch_bytes();
+    const bool l2 = prefetch_l2();
     __m512d a0 = _mm512_setzero_pd(), a1 = _mm512_setzero_pd(), a2 = _mm512_setzero_pd(), a3 = _mm512_setzero_pd();
     const __m512i i4 = _mm512_load_si512(T.r4);
     const __m512i i2a = _mm512_load_si512(T.r2[0]), i2b = _mm512_load_si512(T.r2[1]);
@@ -120,6 +143,20 @@ ADT_AVX512 double pack_avx512(const uint32_t *src, uint64_t n, uint8_t *dst) {
                   i3c = _mm512_load_si512(T.r3[2]);
     const __m512i i1l = _mm512_load_si512(T.r1lo), i1h = _mm512_load_si512(T.r1hi);
     for (uint64_t i = 0; i < n; i += kGroup) {
+        if (pf > 0) {                 // may run past the unit's end: prefetches never fault
+            const char *p = reinterpret_cast<const char *>(src + i) + pf;
+            if (l2) {
+                _mm_prefetch(p, _MM_HINT_T1);
+                _mm_prefetch(p + 64, _MM_HINT_T1);
+                _mm_prefetch(p + 128, _MM_HINT_T1);
+                _mm_prefetch(p + 192, _MM_HINT_T1);
+            } else {
+                _mm_prefetch(p, _MM_HINT_T0);
+                _mm_prefetch(p + 64, _MM_HINT_T0);
+                _mm_prefetch(p + 128, _MM_HINT_T0);
+                _mm_prefetch(p + 192, _MM_HINT_T0);
+            }
+        }
         const __m512i v0 = _mm512_loadu_si512(src + i), v1 = _mm512_loadu_si512(src + i + 16),
                       v2 = _mm512_loadu_si512(src + i + 32), v3 = _mm512_loadu_si512(src + i + 48);
         uint8_t *o = dst + i * R;

@@ -637,7 +637,7 @@ template <int MAXSEG>
 __global__ void __launch_bounds__(kThreads)
 adt_roundtrip_kernel(const __grid_constant__ RoundTable<MAXSEG> R, uint32_t ntiles) {
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
-    __shared__ double red[kWarpsPerTile];
+    __shared__ double red[kFinThreads / 32];
     uint32_t *ws = stage[threadIdx.x >> 5];
     const uint32_t tile = blockIdx.x;
     pack_tile<MAXSEG, true, true, false>(R.P, tile, find_segment(R.P, tile), ws);
@@ -645,19 +645,27 @@ adt_roundtrip_kernel(const __grid_constant__ RoundTable<MAXSEG> R, uint32_t ntil
     const uint32_t ut = ntiles - 1 - tile;
     unpack_tile<MAXSEG>(R.U, ut, find_segment(R.U, ut), ws);
     if (static_cast<int>(blockIdx.x) < R.P.nseg && R.P.seg_sumsq != nullptr) {
+        // adt_norm_finalize_kernel's exact order (kFinThreads virtual threads,
+        // each summing p[v], p[v + kFinThreads], ...; the same shuffle tree per
+        // virtual warp; warp sums added in order) so both step forms agree bit for bit
+        constexpr int kVirt = kFinThreads / kThreads;
         const int s = blockIdx.x;
         const uint32_t lo = R.P.tile_begin[s] * kWarpsPerTile;
         const uint32_t n = (R.P.tile_begin[s + 1] - R.P.tile_begin[s]) * kWarpsPerTile;
-        double a = 0.0;
-        for (uint32_t i = threadIdx.x; i < n; i += kThreads) a += R.P.partials[lo + i];
+        const double *p = R.P.partials + lo;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        for (int k = 0; k < kVirt; ++k) {
+            double a = 0.0;
+            for (uint32_t i = threadIdx.x + k * kThreads; i < n; i += kFinThreads) a += p[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xFFFFFFFFu, a, o);
+            if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) + k * kWarpsPerTile] = a;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             double t = 0.0;
 #pragma unroll
-            for (int w = 0; w < kWarpsPerTile; ++w) t += red[w];
+            for (int w = 0; w < kFinThreads / 32; ++w) t += red[w];
             R.P.seg_sumsq[s] = t;
         }
     }
@@ -1503,11 +1511,15 @@ int adt_roundtrip(const adt_segment *masters, const adt_segment *replicas, int n
     cfg.gridDim = dim3(ntiles);
     cfg.blockDim = dim3(kThreads);
     cfg.stream = static_cast<cudaStream_t>(stream);
+    static const bool coop = [] {                  // A/B hook: ADT_RT_COOP=0 launches it as a plain grid
+        const char *e = getenv("ADT_RT_COOP");
+        return !(e != nullptr && e[0] == '0');
+    }();
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (the grid barrier)
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 1 : 0;
     return cuda_status(cudaLaunchKernelEx(&cfg, adt_roundtrip_kernel<kSmallSeg>, R, ntiles));
 }
 

@@ -69,7 +69,7 @@ class WeightSync:
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None,
                  replicas: Sequence[torch.Tensor] | None = None, graphed: bool = True,
-                 awp_on_device: bool = False, trace_ring: int = 256, fuse_small: bool = True):
+                 awp_on_device: bool = False, trace_ring: int = 256, fuse_small: bool = False):
         """graphed: step() replays its kernels from a CUDA graph captured once
         per packed layout (one graph launch instead of three ctypes launches
         and the stream bookkeeping per step).
@@ -85,7 +85,9 @@ class WeightSync:
         fuse_small: sets of at most one 4096-weight tile per SM and <= 16
         layers (LeNet) run the whole step as ONE cooperative launch
         (adt_roundtrip: pack + norms, grid barrier, unpack) instead of three
-        dependent launches — the same bytes, norms and replicas."""
+        dependent launches — the same bytes, norms and replicas. Off by
+        default: measured slower on a B200 (LeNet 12.3 vs 6.2 us per step back
+        to back, profiles/r02_ab_small_step.md)."""
         engine.require_cuda()
         self.graphed = graphed
         self.fuse_small = bool(fuse_small)

@@ -32,11 +32,12 @@ def best(fn, reps=5):
 
 def main():
     print(f"host threads {hostsync.host_threads()} simd {hostsync._lib.load().adt_host_simd()} "
-          f"NT {os.environ.get('ADT_HOST_NT', '1')}")
+          f"NT {os.environ.get('ADT_HOST_NT', '1')} prefetch {os.environ.get('ADT_HOST_PF', '8192')} B "
+          f"hint {'L2' if os.environ.get('ADT_HOST_PF_HINT', '1') != '0' else 'L1'}")
     rng = np.random.default_rng(0)
     w = rng.standard_normal(1 << 26, dtype=np.float32)          # 256 MiB
     for r in (1, 2, 3, 4):
-        for th in (1, 4, 8, 16):
+        for th in ((1, 16) if os.environ.get("PROBE_QUICK") else (1, 4, 8, 16)):
             dt = best(lambda: hostsync.pack_host([w], [r], threads=th, align=64))
             print(f"pack_host r={r} threads={th:2d}: {dt * 1e3:7.2f} ms  read {w.nbytes / dt / 1e9:6.1f} GB/s  "
                   f"(read+write {w.size * (4 + r) / dt / 1e9:6.1f} GB/s)")
