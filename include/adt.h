@@ -353,6 +353,21 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
                        uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
                        uint64_t min_copy_bytes, void *stream);
 
+/*
+ * adt_host_to_device through a small pinned RING instead of a staging buffer
+ * as large as the stream: the stream is cut into chunks (runs of 64K-weight
+ * units) of at most slot_bytes (>= 256 KiB + 64); chunk c is packed into slot
+ * c % (ring_bytes / slot_bytes) once the copy of the slot's previous chunk has
+ * completed, and the calling thread queues each chunk's copy (in order) as
+ * soon as it is packed. The ring stays cache-resident, so the copies read the
+ * packed bytes from the host's last-level cache rather than DRAM, and only the
+ * masters stream through host memory. Same bytes, sums and unpack as
+ * adt_host_to_device; needs more slots than host threads.
+ */
+int adt_host_to_device_ring(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *ring,
+                            uint64_t ring_bytes, uint64_t slot_bytes, uint8_t *dev_packed, uint64_t packed_bytes,
+                            double *seg_sumsq, int threads, void *stream);
+
 /* Host threads adt_pack_host uses at most (the process's CPU affinity). */
 int adt_host_threads(int *n);
 /* 512 when the host packer runs its AVX-512 VBMI path, 0 for the scalar path. */

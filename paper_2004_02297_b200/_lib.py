@@ -32,7 +32,8 @@ EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", 
            "adt_ipc_open", "adt_ipc_close", "adt_sumsq", "adt_sgd_pack", "adt_reduce_sgd_pack", "adt_pack_dyn", "adt_unpack_dyn", "adt_sgd_pack_dyn", "adt_reduce_sgd_pack_dyn",
            "adt_awp_observe", "adt_awp_fixup", "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces",
            "adt_awp_fixup_gather", "adt_device_sm_count", "adt_pack_host", "adt_host_to_device", "adt_host_threads",
-           "adt_host_simd", "adt_sumsq_f64_partials", "adt_sumsq_f64", "adt_roundtrip", "adt_roundtrip_max_tiles")
+           "adt_host_simd", "adt_sumsq_f64_partials", "adt_sumsq_f64", "adt_roundtrip", "adt_roundtrip_max_tiles",
+           "adt_host_to_device_ring")
 
 
 class Segment(ctypes.Structure):
@@ -205,6 +206,9 @@ def load() -> ctypes.CDLL:
         lib.adt_host_to_device.restype = ctypes.c_int
         lib.adt_host_to_device.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, ctypes.c_uint64, vp, ctypes.c_int,
                                            ctypes.c_uint64, vp]
+        lib.adt_host_to_device_ring.restype = ctypes.c_int
+        lib.adt_host_to_device_ring.argtypes = [seg_p, seg_p, ctypes.c_int, vp, ctypes.c_uint64, ctypes.c_uint64, vp,
+                                                ctypes.c_uint64, vp, ctypes.c_int, vp]
         lib.adt_host_threads.restype = ctypes.c_int
         lib.adt_host_threads.argtypes = [P(ctypes.c_int)]
         lib.adt_host_simd.restype = ctypes.c_int

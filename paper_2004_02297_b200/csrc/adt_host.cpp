@@ -122,10 +122,10 @@ int prefetch_bytes() {
     }();
     return v;
 }
-bool prefetch_l2() {
-    static const bool v = [] {
+int prefetch_hint() {                 // 0 = L1 (T0), 1 = L2 (T1, default), 2 = non-temporal (NTA)
+    static const int v = [] {
         const char *e = getenv("ADT_HOST_PF_HINT");
-        return !(e != nullptr && e[0] == '0');
+        return e != nullptr ? atoi(e) : 1;
     }();
     return v;
 }
@@ -135,7 +135,7 @@ template <int R, bool NT>
 ADT_AVX512 double pack_avx512(const uint32_t *src, uint64_t n, uint8_t *dst) {
     const PermTables &T = perm();
     const int pf = prefetch_bytes();
-    const bool l2 = prefetch_l2();
+    const int hint = prefetch_hint();
     __m512d a0 = _mm512_setzero_pd(), a1 = _mm512_setzero_pd(), a2 = _mm512_setzero_pd(), a3 = _mm512_setzero_pd();
     const __m512i i4 = _mm512_load_si512(T.r4);
     const __m512i i2a = _mm512_load_si512(T.r2[0]), i2b = _mm512_load_si512(T.r2[1]);
@@ -145,11 +145,16 @@ ADT_AVX512 double pack_avx512(const uint32_t *src, uint64_t n, uint8_t *dst) {
     for (uint64_t i = 0; i < n; i += kGroup) {
         if (pf > 0) {                 // may run past the unit's end: prefetches never fault
             const char *p = reinterpret_cast<const char *>(src + i) + pf;
-            if (l2) {
+            if (hint == 1) {
                 _mm_prefetch(p, _MM_HINT_T1);
                 _mm_prefetch(p + 64, _MM_HINT_T1);
                 _mm_prefetch(p + 128, _MM_HINT_T1);
                 _mm_prefetch(p + 192, _MM_HINT_T1);
+            } else if (hint == 2) {
+                _mm_prefetch(p, _MM_HINT_NTA);
+                _mm_prefetch(p + 64, _MM_HINT_NTA);
+                _mm_prefetch(p + 128, _MM_HINT_NTA);
+                _mm_prefetch(p + 192, _MM_HINT_NTA);
             } else {
                 _mm_prefetch(p, _MM_HINT_T0);
                 _mm_prefetch(p + 64, _MM_HINT_T0);
@@ -219,18 +224,22 @@ bool use_nt() {
     return v;
 }
 
-// One work unit: weights [lo, hi) of one layer. Returns its sum of squares.
-double pack_unit(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *packed) {
+// One work unit: weights [lo, hi) of one layer, packed to `dst` (where weight
+// lo's bytes go). Returns its sum of squares. nt: non-temporal stores allowed.
+double pack_unit_to(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *dst, bool nt) {
     const uint32_t *src = static_cast<const uint32_t *>(s.weights) + lo;
-    uint8_t *dst = packed + s.offset + lo * static_cast<uint64_t>(s.round_to);
     const uint64_t n = hi - lo, body = have_vbmi() ? n / kGroup * kGroup : 0;
     double acc = 0.0;
     if (body) {
-        const bool nt = use_nt() && (reinterpret_cast<uintptr_t>(dst) % 64 == 0);
+        nt = nt && use_nt() && (reinterpret_cast<uintptr_t>(dst) % 64 == 0);
         acc = pick_avx512(s.round_to, nt)(src, body, dst);
     }
     if (body < n) acc += pack_scalar(src + body, n - body, s.round_to, dst + body * s.round_to);
     return acc;
+}
+
+double pack_unit(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *packed) {
+    return pack_unit_to(s, lo, hi, packed + s.offset + lo * static_cast<uint64_t>(s.round_to), true);
 }
 
 // ------------------------------------------------------------ worker pool
@@ -432,6 +441,101 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
         err = cudaMemcpyAsync(dev_packed + sent, host_packed + sent, end - sent, cudaMemcpyHostToDevice, st);
         sent = end;
     });
+    finish_sums(units, ss, nseg, seg_sumsq);
+    if (err != cudaSuccess) return ADT_ERR_CUDA_BASE - static_cast<int>(err);
+    return dev_segs == nullptr ? ADT_OK : adt_unpack(dev_segs, nseg, dev_packed, stream);
+}
+
+int adt_host_to_device_ring(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *ring,
+                            uint64_t ring_bytes, uint64_t slot_bytes, uint8_t *dev_packed, uint64_t packed_bytes,
+                            double *seg_sumsq, int threads, void *stream) {
+    int v = validate_host(host_segs, nseg, ring);
+    if (v != ADT_OK) return v;
+    if (nseg > 0 && dev_packed == nullptr) return ADT_ERR_ARG;
+    if (ring == nullptr || reinterpret_cast<uintptr_t>(ring) % 64 || slot_bytes % 64 ||
+        slot_bytes < kUnitWeights * 4 + 64 || ring_bytes < 2 * slot_bytes)   // a slot holds any one unit + pad
+        return ADT_ERR_ARG;
+    uint64_t end_prev = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const adt_segment &h = host_segs[i];
+        if (dev_segs != nullptr) {
+            const adt_segment &d = dev_segs[i];
+            if (h.count != d.count || h.offset != d.offset || h.round_to != d.round_to) return ADT_ERR_ARG;
+        }
+        if (h.count == 0) continue;
+        const uint64_t end = h.offset + h.count * static_cast<uint64_t>(h.round_to);
+        if (h.offset < end_prev || end > packed_bytes) return ADT_ERR_ARG;
+        end_prev = end;
+    }
+    const std::vector<Unit> units = make_units(host_segs, nseg);
+    std::vector<double> ss(units.size(), 0.0);
+    auto start_of = [&](size_t k) -> uint64_t {
+        if (k >= units.size()) return packed_bytes;
+        const adt_segment &s = host_segs[units[k].seg];
+        return s.offset + units[k].lo * static_cast<uint64_t>(s.round_to);
+    };
+    // chunks: runs of consecutive units whose stream span [a, b) (b = the next
+    // chunk's start: inter-layer pad included) fits one ring slot
+    struct Chunk { uint64_t a, b; size_t u0, u1; };
+    std::vector<Chunk> chunks;
+    for (size_t k = 0; k < units.size();) {
+        const uint64_t a = start_of(k);
+        size_t e = k + 1;
+        while (e < units.size() && start_of(e + 1) - a <= slot_bytes) ++e;
+        chunks.push_back({a, start_of(e), k, e});
+        k = e;
+    }
+    const size_t nc = chunks.size();
+    const int nslots = static_cast<int>(std::min<uint64_t>(ring_bytes / slot_bytes, 1024));
+    const int nthreads = resolve_threads(threads);
+    if (nslots <= nthreads) return ADT_ERR_ARG;      // every in-flight chunk needs its own slot
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<cudaEvent_t> ev(nslots, nullptr);
+    for (auto &e : ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr;
+    std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[nc == 0 ? 1 : nc]);
+    std::unique_ptr<std::atomic<int64_t>[]> issued(new std::atomic<int64_t>[nslots]);
+    for (size_t i = 0; i < nc; ++i) done[i].store(0, std::memory_order_relaxed);
+    for (int i = 0; i < nslots; ++i) issued[i].store(-1, std::memory_order_relaxed);
+    std::atomic<size_t> next{0};
+    std::atomic<int> failed{0};
+    const bool nt = getenv("ADT_RING_NT") != nullptr && getenv("ADT_RING_NT")[0] == '1';
+    // packers: chunk c -> slot c % nslots, after the copy of chunk c - nslots has left it
+    const std::function<void(int)> job = [&](int) {
+        for (size_t c; (c = next.fetch_add(1, std::memory_order_relaxed)) < nc;) {
+            const int slot = static_cast<int>(c % nslots);
+            if (c >= static_cast<size_t>(nslots)) {
+                const int64_t prev = static_cast<int64_t>(c) - nslots;
+                while (issued[slot].load(std::memory_order_acquire) < prev && !failed.load()) _mm_pause();
+                if (ev[slot] != nullptr) cudaEventSynchronize(ev[slot]);
+            }
+            uint8_t *base = ring + static_cast<uint64_t>(slot) * slot_bytes;
+            const Chunk &ch = chunks[c];
+            for (size_t k = ch.u0; k < ch.u1; ++k) {
+                const Unit &u = units[k];
+                ss[k] = pack_unit_to(host_segs[u.seg], u.lo, u.hi, base + (start_of(k) - ch.a), nt);
+            }
+            done[c].store(1, std::memory_order_release);
+        }
+    };
+    cudaError_t err = cudaSuccess;
+    // the caller: issues each chunk's copy (in order) as soon as it is packed
+    const std::function<void()> caller = [&] {
+        for (size_t c = 0; c < nc; ++c) {
+            while (!done[c].load(std::memory_order_acquire)) _mm_pause();
+            const int slot = static_cast<int>(c % nslots);
+            if (err == cudaSuccess)
+                err = cudaMemcpyAsync(dev_packed + chunks[c].a, ring + static_cast<uint64_t>(slot) * slot_bytes,
+                                      chunks[c].b - chunks[c].a, cudaMemcpyHostToDevice, st);
+            if (err == cudaSuccess && ev[slot] != nullptr) err = cudaEventRecord(ev[slot], st);
+            if (err != cudaSuccess) failed.store(1);
+            issued[slot].store(static_cast<int64_t>(c), std::memory_order_release);
+        }
+    };
+    // the caller only issues copies: nthreads - 1 pool threads pack (plus one extra when available)
+    Pool::get().run(nthreads + 1, job, caller);
+    for (auto &e : ev)
+        if (e != nullptr) cudaEventDestroy(e);
     finish_sums(units, ss, nseg, seg_sumsq);
     if (err != cudaSuccess) return ADT_ERR_CUDA_BASE - static_cast<int>(err);
     return dev_segs == nullptr ? ADT_OK : adt_unpack(dev_segs, nseg, dev_packed, stream);

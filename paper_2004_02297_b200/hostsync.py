@@ -9,13 +9,14 @@ codec.pack_vectorized / unpack (codec.py:149-197) and runs the caller order of
 training.py:207-254; this class is that caller order with the codec split
 across the two processors:
 
-    host:   adt_pack_host (all cores, AVX-512 VBMI, l2-norm fused into the read)
-            -> pinned staging buffer, cut into units of 64K weights
+    host:   adt_pack_host (all cores, AVX-512 VBMI, l2-norm fused into the
+            read) -> pinned staging buffer, cut into units of 64K weights
     link:   cudaMemcpyAsync of every finished run of units while the rest is
             still being packed (Σ n·r bytes instead of 4·Σ n)
     device: adt_unpack of the whole stream into the FP32 replicas
 
-(one C call, adt_host_to_device). The norms come out of the host pass, so the
+(one C call, adt_host_to_device; or adt_host_to_device_ring through a small
+pinned ring when ring_bytes > 0). The norms come out of the host pass, so the
 AWP decision (precision.PrecisionController) needs no device->host read.
 Whether this beats copying FP32 depends on the host: the host pass streams
 (4 + r)·n bytes through host DRAM next to the DMA's r·n, against 4·n for a raw
@@ -65,7 +66,8 @@ class HostWeightSync:
     """
 
     def __init__(self, masters: Sequence, schedule=None, replicas: Sequence[torch.Tensor] | None = None,
-                 device: torch.device | str | None = None, threads: int = 0, min_copy_bytes: int = 1 << 20):
+                 device: torch.device | str | None = None, threads: int = 0, min_copy_bytes: int = 1 << 20,
+                 ring_bytes: int = 0, slot_bytes: int = 384 << 10):
         engine.require_cuda()
         self.masters = [_host_view(m, i) for i, m in enumerate(masters)]
         self.counts = [m.size for m in self.masters]
@@ -83,9 +85,15 @@ class HostWeightSync:
         self.threads = int(threads)
         self.min_copy_bytes = int(min_copy_bytes)
         cap = PackedLayout.plan(self.counts, [4] * L, align=HOST_ALIGN).nbytes
-        # one pinned staging buffer and one device buffer with room for every
-        # width: a re-plan after an AWP escalation never reallocates
-        self.staging = torch.empty(max(64, cap + 64), dtype=torch.uint8, pin_memory=True)
+        # ring_bytes = 0 (default): one pinned staging buffer as large as the
+        # stream (adt_host_to_device). > 0: a small pinned ring of slot_bytes
+        # slots (adt_host_to_device_ring) — measured 1.2-1.9x SLOWER on the B200
+        # boxes (per-chunk copy + event overheads outweigh the DRAM traffic it
+        # saves; profiles/r02_hostmaster.md), kept as an option. The device
+        # buffer has room for every width: a re-plan never reallocates.
+        self.ring_bytes, self.slot_bytes = int(ring_bytes), int(slot_bytes)
+        stage = self.ring_bytes if self.ring_bytes else cap
+        self.staging = torch.empty(max(64, stage + 64), dtype=torch.uint8, pin_memory=True)
         base = (-self.staging.data_ptr()) % 64
         self._stage_ptr = self.staging.data_ptr() + base        # 64-B aligned stream start
         self.packed = torch.empty(max(64, cap), dtype=torch.uint8, device=self.device)
@@ -122,10 +130,17 @@ class HostWeightSync:
             self._dma_done.synchronize()         # the staging buffer is free again
         if events is not None:
             events[0].record(s)
-        _lib.check(_lib.load().adt_host_to_device(
-            self._host_segs, self.unpack_table.array if events is None else None, len(self.counts), self._stage_ptr,
-            self.packed.data_ptr(), self.layout.nbytes, self.sumsq.ctypes.data if fused_norm else None,
-            self.threads, self.min_copy_bytes, int(s.cuda_stream)))
+        dev_segs = self.unpack_table.array if events is None else None
+        sums = self.sumsq.ctypes.data if fused_norm else None
+        lib = _lib.load()
+        if self.ring_bytes:
+            _lib.check(lib.adt_host_to_device_ring(
+                self._host_segs, dev_segs, len(self.counts), self._stage_ptr, self.ring_bytes, self.slot_bytes,
+                self.packed.data_ptr(), self.layout.nbytes, sums, self.threads, int(s.cuda_stream)))
+        else:
+            _lib.check(lib.adt_host_to_device(
+                self._host_segs, dev_segs, len(self.counts), self._stage_ptr, self.packed.data_ptr(),
+                self.layout.nbytes, sums, self.threads, self.min_copy_bytes, int(s.cuda_stream)))
         if events is not None:
             events[1].record(s)
             engine.unpack(self.unpack_table, self.packed, s)

@@ -30,6 +30,10 @@ def best(fn, reps=5):
     return b
 
 
+def cudart_copy(dev_u8, host_u8, nbytes):
+    dev_u8[:nbytes].copy_(host_u8[:nbytes], non_blocking=True)
+
+
 def main():
     print(f"host threads {hostsync.host_threads()} simd {hostsync._lib.load().adt_host_simd()} "
           f"NT {os.environ.get('ADT_HOST_NT', '1')} prefetch {os.environ.get('ADT_HOST_PF', '8192')} B "
@@ -50,11 +54,16 @@ def main():
             def round_tos(self):
                 return list(rs)
 
-        sync = hostsync.HostWeightSync(host, Fixed(len(counts), 32))
+        ring_sync = hostsync.HostWeightSync(host, Fixed(len(counts), 32))
+        sync = hostsync.HostWeightSync(host, Fixed(len(counts), 32), ring_bytes=0)
         s = torch.cuda.current_stream()
 
         def adt_step():
             sync.launch(fused_norm=True)
+            s.synchronize()
+
+        def ring_step():
+            ring_sync.launch(fused_norm=True)
             s.synchronize()
 
         flat = torch.empty(sum(counts), dtype=torch.float32).pin_memory()
@@ -64,12 +73,29 @@ def main():
             dev.copy_(flat, non_blocking=True)
             s.synchronize()
 
-        t_adt, t_raw = best(adt_step), best(raw)
+        t_adt, t_raw, t_ring = best(adt_step), best(raw), best(ring_step)
+        print(f"   {name}: ring ({ring_sync.ring_bytes >> 20} MiB, {ring_sync.slot_bytes >> 10} KiB slots) "
+              f"{t_ring * 1e3:.2f} ms vs full staging {t_adt * 1e3:.2f} ms")
+        lib = hostsync._lib.load()
+        L = len(counts)
+
+        def pack_only():                       # the host pass alone, into the pinned staging buffer
+            lib.adt_pack_host(sync._host_segs, L, sync._stage_ptr, sync.sumsq.ctypes.data, 0)
+
+        dev_packed = sync.packed
+
+        def dma_only():                        # the packed stream's copy alone
+            cudart_copy(dev_packed, sync.staging, sync.layout.nbytes)
+            s.synchronize()
+
+        t_pack, t_dma = best(pack_only), best(dma_only)
+        print(f"   {name}: host pack alone {t_pack * 1e3:.2f} ms ({sum(counts) * 4 / t_pack / 1e9:.1f} GB/s of masters), "
+              f"packed DMA alone {t_dma * 1e3:.2f} ms ({sync.layout.nbytes / t_dma / 1e9:.1f} GB/s)")
         n = sum(counts)
         print(f"{name} r={sorted(set(rs))}: HostWeightSync {t_adt * 1e3:7.2f} ms ({sync.h2d_bytes / 1e6:.0f} MB over "
               f"PCIe) vs raw FP32 pinned H2D {t_raw * 1e3:7.2f} ms ({4 * n / 1e6:.0f} MB): "
               f"{t_raw / t_adt:.2f}x")
-        del sync, flat, dev
+        del sync, ring_sync, flat, dev
 
 
 if __name__ == "__main__":

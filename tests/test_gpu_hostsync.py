@@ -25,7 +25,8 @@ def adt():
     return adt
 
 
-def test_replicas_and_norms_mixed_widths(adt):
+@pytest.mark.parametrize("ring", [0, 48 * (384 << 10)])
+def test_replicas_and_norms_mixed_widths(adt, ring):
     rng = np.random.default_rng(3)
     counts = [20 * 25, 50 * 20 * 25, 4097, 0, 65536 * 3 + 11, 10 * 500, 3]
     rs = [1, 2, 3, 4, 4, 1, 3]
@@ -36,7 +37,7 @@ def test_replicas_and_norms_mixed_widths(adt):
         def round_tos(self):
             return list(rs)
 
-    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32))
+    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32), ring_bytes=ring)
     for _ in range(3):                        # repeated transfers reuse the staging buffer
         for r_ in sync.replicas:
             r_.fill_(float("nan"))
@@ -55,7 +56,8 @@ def test_replicas_and_norms_mixed_widths(adt):
     assert sync.h2d_bytes < 4 * sum(counts)
 
 
-def test_large_set_in_many_copies(adt):
+@pytest.mark.parametrize("ring", [0, 48 * (320 << 10), 17 * (320 << 10)])
+def test_large_set_in_many_copies(adt, ring):
     """A stream much larger than one copy batch: the DMA of early units overlaps
     the packing of later ones; every byte must still land once, in order."""
     rng = np.random.default_rng(8)
@@ -67,7 +69,8 @@ def test_large_set_in_many_copies(adt):
         def round_tos(self):
             return list(rs)
 
-    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32), min_copy_bytes=64 << 10)
+    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32), min_copy_bytes=64 << 10, ring_bytes=ring,
+                              slot_bytes=320 << 10)
     sync.launch(fused_norm=False)
     torch.cuda.synchronize()
     for i, (h, r) in enumerate(zip(hosts, rs)):
