@@ -527,7 +527,11 @@ def main_ours(args):
             roofline["dram_GBps"] = dram
             roofline["dram_frac"] = dram / hbm
         if world == 1 and not args.quiet_extra and not small:
-            roofline["cold"] = run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, not args.no_norm)
+            l2b = torch.cuda.get_device_properties(dev).L2_cache_size
+            if 4 * (8 * sum(counts) + sync.layout.nbytes) > 2 * l2b:
+                roofline["cold"] = run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, not args.no_norm)
+            else:
+                roofline["cold"] = {"note": "not applicable: four copies of the set fit in L2 (latency-bound set)"}
 
     # ---- e2e through the public API with host buffers (pinned H2D in the timed region)
     e2e = e2e_dropin = e2e_fp32_h2d = None

@@ -8,7 +8,8 @@ mkdir -p paper_2004_02297_b200/variants
 for v in "$@"; do
   name=${v%%=*}; defs=${v#*=}
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -shared \
-    -I include ${defs//,/ } -o paper_2004_02297_b200/variants/libadt_$name.so paper_2004_02297_b200/csrc/adt_kernels.cu &
+    -Xcompiler -pthread -lpthread -I include ${defs//,/ } -o paper_2004_02297_b200/variants/libadt_$name.so \
+    paper_2004_02297_b200/csrc/adt_kernels.cu paper_2004_02297_b200/csrc/adt_host.cpp &
 done
 wait
 ls paper_2004_02297_b200/variants
