@@ -89,6 +89,25 @@ def main():
     pl = torch.tensor(list(range(len(nz))) * 2, dtype=torch.int32, device="cuda")
     engine.awp_combine(tails, pl, len(nz), torch.empty(len(nz), dtype=torch.float64, device="cuda"))
     torch.cuda.synchronize()
+    # r02: peer-abort guard (a lone barrier times out, then every guarded kernel is a no-op),
+    # float64-input norm, one-launch small step, CPU-master transfer (staging and ring)
+    lone = torch.zeros(2, dtype=torch.int32, device="cuda")
+    lone_flags = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    engine.peer_barrier([f.data_ptr() for f in lone_flags], 0, lone, timeout_s=0.01)
+    engine.unpack_multi(engine.SegmentTable(outs, lay, sources=[0] * len(counts)), [a.data_ptr()], abort=lone[1:2])
+    engine.copy_multi(torch.zeros(32, dtype=torch.uint8, device="cuda"), [a.data_ptr()], 0, 32, abort=lone[1:2])
+    engine.reduce_sgd_pack(table, [b.flat.data_ptr() for b in buckets], [b.sample_count for b in buckets],
+                           0.01, 0.9, 5e-4, packed, norms, abort=lone[1:2])
+    x64 = torch.randn(100003, dtype=torch.float64, device="cuda")
+    engine.sumsq_f64(x64, torch.empty(1, dtype=torch.float64, device="cuda"))
+    small = adt.WeightSync([d.clone() for d in nz], fuse_small=True)
+    for _ in range(3):
+        small.launch(fused_norm=True)
+    hosts_nz = [h for h in hosts if h.size]
+    for ring in (0, 24 * (320 << 10)):
+        hs = adt.HostWeightSync([h.copy() for h in hosts_nz], ring_bytes=ring, slot_bytes=320 << 10)
+        hs.launch(fused_norm=True)
+    torch.cuda.synchronize()
     print("sanitize smoke ok")
 
 
