@@ -1,11 +1,15 @@
 #!/bin/bash
-# Copy one gpu_full.sh run (gpurun_out/<tag>) into the tracked profiles/: bench lines,
-# ncu summaries, launch lists, traffic table, Table-2, bench-codec, step overhead, training runs.
-# usage: bash scripts/refresh_profiles.sh r01g
+# Copy one evidence pass (gpurun_out/<tag>, from scripts/gpu_full.sh or gpu_r02.sh) into the
+# tracked profiles/: bench lines, ncu summaries, launch lists, traffic table, Table-2, step
+# overhead, host probes. Files a pass did not produce are skipped.
+# usage: bash scripts/refresh_profiles.sh <tag> [round-prefix, default r02]
 set -e
 O=gpurun_out/$1
-for f in bench bench_1b_16 bench_1b_24 bench_1b_32 bench_1b_8 bench_lenet bench_resnet50 bench_vgg16 bench_reference; do
-  python - "$O/$f.json" "profiles/r01_$f.json" <<'PY'
+P=${2:-r02}
+have() { [ -s "$1" ]; }
+for j in $O/bench*.json; do
+  f=$(basename $j .json)
+  python - "$j" "profiles/${P}_$f.json" <<'PY'
 import json, sys
 line = None
 for l in open(sys.argv[1]):
@@ -13,22 +17,25 @@ for l in open(sys.argv[1]):
         line = json.loads(l)
     except Exception:
         pass
-json.dump(line, open(sys.argv[2], "w")); open(sys.argv[2], "a").write("\n")
+if line is not None:
+    json.dump(line, open(sys.argv[2], "w")); open(sys.argv[2], "a").write("\n")
 PY
 done
-python scripts/ncu_summary.py launches $O/launches.csv > profiles/r01_alexnet_launches.md
-python scripts/ncu_summary.py launches $O/launches_resnet50.csv > profiles/r01_resnet50_launches.md
-python scripts/ncu_summary.py launches $O/launches_awp_device.csv > profiles/r01_awp_device_launches.md
-python scripts/ncu_summary.py report $O/prof_alexnet.ncu-rep > profiles/r01_alexnet_ncu_full.md
-python scripts/ncu_summary.py report $O/prof_resnet50.ncu-rep > profiles/r01_resnet50_ncu_full.md
-python scripts/ncu_summary.py report $O/prof_sgd.ncu-rep > profiles/r01_sgd_ncu_full.md
-python scripts/ncu_summary.py report $O/prof_reduce.ncu-rep > profiles/r01_reduce_ncu_full.md
-python scripts/ncu_summary.py traffic $O/prof_alexnet.ncu-rep alexnet > /dev/null
-python scripts/ncu_summary.py traffic $O/prof_resnet50.ncu-rep resnet50 > /dev/null
-cp $O/table2.md profiles/r01_table2.md
-cp $O/nvsmi.txt profiles/r01_nvsmi.txt
-tail -n 1 $O/bench_n2_gloo_p2p.log > profiles/r01_bench_n2_gloo_p2p.json
-python scripts/results_table.py $O > profiles/r01_results_table.md
-cp $O/step_overhead.txt profiles/r01_step_overhead.txt
-cat $O/train_fp32.json $O/train_awp.json $O/train_awp_device.json > profiles/r01_train_example.jsonl
-cp $O/reduce_sweep.md profiles/r01_reduce_sweep.md
+have $O/launches.csv && python scripts/ncu_summary.py launches $O/launches.csv > profiles/${P}_alexnet_launches.md
+have $O/launches_resnet50.csv && python scripts/ncu_summary.py launches $O/launches_resnet50.csv > profiles/${P}_resnet50_launches.md
+have $O/launches_awp_device.csv && python scripts/ncu_summary.py launches $O/launches_awp_device.csv > profiles/${P}_awp_device_launches.md
+for k in alexnet resnet50 sgd reduce vgg16_r1 vgg16_r2 vgg16_r3; do
+  have $O/prof_$k.ncu-rep && python scripts/ncu_summary.py report $O/prof_$k.ncu-rep > profiles/${P}_${k}_ncu_full.md
+done
+have $O/prof_alexnet.ncu-rep && python scripts/ncu_summary.py traffic $O/prof_alexnet.ncu-rep alexnet > /dev/null
+have $O/prof_resnet50.ncu-rep && python scripts/ncu_summary.py traffic $O/prof_resnet50.ncu-rep resnet50 > /dev/null
+have $O/table2.md && cp $O/table2.md profiles/${P}_table2.md
+have $O/nvsmi.txt && cp $O/nvsmi.txt profiles/${P}_nvsmi.txt
+have $O/step_overhead.txt && cp $O/step_overhead.txt profiles/${P}_step_overhead.txt
+have $O/host_probe.txt && cp $O/host_probe.txt profiles/${P}_host_probe.txt
+have $O/small_step.txt && cp $O/small_step.txt profiles/${P}_small_step.txt
+have $O/pytest_gpu.log && tail -n 30 $O/pytest_gpu.log > profiles/${P}_pytest_gpu_tail.txt
+for t in memcheck racecheck synccheck; do
+  have $O/sanitize_$t.log && tail -n 3 $O/sanitize_$t.log > profiles/${P}_sanitize_$t.txt
+done
+python scripts/results_table.py $O > profiles/${P}_results_table.md || true
