@@ -1035,38 +1035,55 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
             return list(rs)
 
     import numpy as np
-    sync = adt.HostWeightSync(host, Fixed(len(host), 32), device=dev)
+    # The masters live in page-locked host memory, as a CPU-master trainer
+    # allocates them (torch pin_memory): full-width layers then go to the GPU by
+    # DMA straight from the masters (HostWeightSync direct_full, the default).
+    pinned = []
+    for h in host:
+        t = torch.empty(h.size, dtype=torch.float32, pin_memory=True)
+        t.numpy()[:] = h
+        pinned.append(t.numpy())
     stream = torch.cuda.current_stream(dev)
-    # the step's result lives on the GPU (the replicas): each step reads back the
-    # last 4 words of the last replica (16 B D2H, which also completes the step)
-    # and checks them against the host masters truncated to their width
-    tail_dev = sync.replicas[-1][-4:]
-    tail_host = torch.empty(4, dtype=torch.float32, pin_memory=True)
-    want = (host[-1][-4:].view(np.uint32) & np.uint32((0xFFFFFFFF << (8 * (4 - rs[-1]))) & 0xFFFFFFFF))
 
-    def one():
-        sync.launch(fused_norm=True)
-        tail_host.copy_(tail_dev, non_blocking=True)
-        stream.synchronize()
-        if not np.array_equal(tail_host.numpy().view(np.uint32), want):
-            raise AssertionError("host-master e2e: the replica read back differs from the packed masters")
+    def measure(direct_full):
+        sync = adt.HostWeightSync(pinned, Fixed(len(host), 32), device=dev, direct_full=direct_full)
+        # the step's result lives on the GPU (the replicas): each step reads back the
+        # last 4 words of the last replica (16 B D2H, which also completes the step)
+        # and checks them against the host masters truncated to their width
+        tail_dev = sync.replicas[-1][-4:]
+        tail_host = torch.empty(4, dtype=torch.float32, pin_memory=True)
+        want = (host[-1][-4:].view(np.uint32) & np.uint32((0xFFFFFFFF << (8 * (4 - rs[-1]))) & 0xFFFFFFFF))
 
-    for _ in range(3):
-        one()
-    steps = max(args.e2e_steps, steps)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        one()
-    dt = (time.perf_counter() - t0) / steps
+        def one():
+            sync.launch(fused_norm=True)
+            tail_host.copy_(tail_dev, non_blocking=True)
+            stream.synchronize()
+            if not np.array_equal(tail_host.numpy().view(np.uint32), want):
+                raise AssertionError("host-master e2e: the replica read back differs from the packed masters")
+
+        for _ in range(3):
+            one()
+        n_steps = max(args.e2e_steps, steps)
+        t0 = time.perf_counter()
+        for _ in range(n_steps):
+            one()
+        dt = (time.perf_counter() - t0) / n_steps
+        ndirect = int(sync.direct[:len(host)].sum())
+        h2d = sync.h2d_bytes
+        del sync
+        return dt, n_steps, ndirect, h2d
+
+    dt, n_steps, ndirect, h2d = measure(True)
+    dt_packed, _, _, _ = measure(False) if ndirect else (dt, 0, 0, 0)
     # the same host arrays as one raw FP32 pinned copy would move: the baseline
     n = sum(h.size for h in host)
     byts = 2 * sum((4 + r) * h.size for h, r in zip(host, rs))
-    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": sync.h2d_bytes, "d2h_bytes_per_step": 16,
-            "ms_per_step": dt * 1e3, "steps": steps, "host_threads": host_threads(),
-            "raw_fp32_bytes": 4 * n,
-            "note": "HostWeightSync: host FP32 masters -> adt_pack_host (all host cores, norms fused) -> packed "
-                    "H2D overlapped with the packing -> adt_unpack -> 16 B read-back check; wall clock; the "
-                    "norms come from the host pass"}
+    return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16,
+            "ms_per_step": dt * 1e3, "steps": n_steps, "host_threads": host_threads(),
+            "raw_fp32_bytes": 4 * n, "direct_full_layers": ndirect, "all_packed_ms_per_step": dt_packed * 1e3,
+            "note": "HostWeightSync: pinned host FP32 masters -> adt_pack_host (all host cores, norms fused) -> "
+                    "packed H2D overlapped with the packing -> adt_unpack; full-width layers DMA'd straight from "
+                    "the masters (direct_full); 16 B read-back check; wall clock; the norms come from the host pass"}
 
 
 def run_e2e_weightsync(args, dev_masters, rs, dev):

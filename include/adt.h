@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ADT_ABI_VERSION 10
+#define ADT_ABI_VERSION 11
 
 /* status codes */
 #define ADT_OK 0
@@ -352,6 +352,31 @@ int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *se
 int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
                        uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
                        uint64_t min_copy_bytes, void *stream);
+
+/*
+ * adt_host_to_device with options. flags:
+ *   ADT_H2D_DIRECT_FULL — layers at round_to 4 whose host words are page-locked
+ *     (both ends of the range registered with CUDA) are not packed on the host:
+ *     the DMA copies their FP32 words straight into dev_segs[l].weights (the
+ *     replica equals the master at full width, so the result is identical;
+ *     4n bytes cross the link either way) before the packed stream, and their
+ *     unpack is skipped. Their seg_sumsq entries still come from a host pass
+ *     (read only; bit-identical to the packed path's sums). Host DRAM then
+ *     carries their 4n bytes once instead of three times. Needs dev_segs.
+ *   ADT_H2D_SKIP_DIRECT_NORMS — with DIRECT_FULL: no host norm pass over the
+ *     direct layers (their seg_sumsq entries are set to NaN); the caller takes
+ *     them from the replicas on the device (adt_sumsq: the replica IS the
+ *     master at full width). Measured on the B200 host: a host read of the
+ *     direct layers running beside their DMA slows the DMA by up to 40 %
+ *     (profiles/r02_host_direct.md).
+ * direct_out (nseg bytes, may be NULL) receives 1 for every layer sent that way.
+ * Everything else as adt_host_to_device (which is this call with flags 0).
+ */
+#define ADT_H2D_DIRECT_FULL 1u
+#define ADT_H2D_SKIP_DIRECT_NORMS 2u
+int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
+                          uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
+                          uint64_t min_copy_bytes, uint32_t flags, uint8_t *direct_out, void *stream);
 
 /*
  * adt_host_to_device through a small pinned RING instead of a staging buffer

@@ -23,7 +23,9 @@ ADT_ERR_ARG = -3
 ADT_ERR_NO_DEVICE = -4
 ADT_ERR_CUDA_BASE = -1000
 TILE_WEIGHTS = 4096
-ABI_VERSION = 10
+ABI_VERSION = 11
+H2D_DIRECT_FULL = 1      # adt_host_to_device_ex flags (include/adt.h)
+H2D_SKIP_DIRECT_NORMS = 2
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 
@@ -33,7 +35,7 @@ EXPORTS = ("adt_abi_version", "adt_strerror", "adt_partials_count", "adt_pack", 
            "adt_awp_observe", "adt_awp_fixup", "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces",
            "adt_awp_fixup_gather", "adt_device_sm_count", "adt_pack_host", "adt_host_to_device", "adt_host_threads",
            "adt_host_simd", "adt_sumsq_f64_partials", "adt_sumsq_f64", "adt_roundtrip", "adt_roundtrip_max_tiles",
-           "adt_host_to_device_ring")
+           "adt_host_to_device_ring", "adt_host_to_device_ex")
 
 
 class Segment(ctypes.Structure):
@@ -209,6 +211,9 @@ def load() -> ctypes.CDLL:
         lib.adt_host_to_device_ring.restype = ctypes.c_int
         lib.adt_host_to_device_ring.argtypes = [seg_p, seg_p, ctypes.c_int, vp, ctypes.c_uint64, ctypes.c_uint64, vp,
                                                 ctypes.c_uint64, vp, ctypes.c_int, vp]
+        lib.adt_host_to_device_ex.restype = ctypes.c_int
+        lib.adt_host_to_device_ex.argtypes = [seg_p, seg_p, ctypes.c_int, vp, vp, ctypes.c_uint64, vp, ctypes.c_int,
+                                              ctypes.c_uint64, ctypes.c_uint32, vp, vp]
         lib.adt_host_threads.restype = ctypes.c_int
         lib.adt_host_threads.argtypes = [P(ctypes.c_int)]
         lib.adt_host_simd.restype = ctypes.c_int

@@ -195,6 +195,44 @@ ADT_AVX512 double pack_avx512(const uint32_t *src, uint64_t n, uint8_t *dst) {
     return _mm512_reduce_add_pd(_mm512_add_pd(_mm512_add_pd(a0, a1), _mm512_add_pd(a2, a3)));
 }
 
+// The same float64 sum of squares as pack_avx512 (same accumulators, same
+// order: bit-identical), without the byte gather or any store — the norm of a
+// layer that is not packed on the host (adt_host_to_device_ex direct layers).
+ADT_AVX512 double sumsq_avx512(const uint32_t *src, uint64_t n) {
+    const int pf = prefetch_bytes();
+    __m512d a0 = _mm512_setzero_pd(), a1 = _mm512_setzero_pd(), a2 = _mm512_setzero_pd(), a3 = _mm512_setzero_pd();
+    for (uint64_t i = 0; i < n; i += kGroup) {
+        if (pf > 0) {
+            const char *p = reinterpret_cast<const char *>(src + i) + pf;
+            _mm_prefetch(p, _MM_HINT_T1);
+            _mm_prefetch(p + 64, _MM_HINT_T1);
+            _mm_prefetch(p + 128, _MM_HINT_T1);
+            _mm_prefetch(p + 192, _MM_HINT_T1);
+        }
+        const __m512i v0 = _mm512_loadu_si512(src + i), v1 = _mm512_loadu_si512(src + i + 16),
+                      v2 = _mm512_loadu_si512(src + i + 32), v3 = _mm512_loadu_si512(src + i + 48);
+        a0 = sq_acc(a0, _mm512_castps512_ps256(_mm512_castsi512_ps(v0)));
+        a1 = sq_acc(a1, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v0), 1)));
+        a2 = sq_acc(a2, _mm512_castps512_ps256(_mm512_castsi512_ps(v1)));
+        a3 = sq_acc(a3, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v1), 1)));
+        a0 = sq_acc(a0, _mm512_castps512_ps256(_mm512_castsi512_ps(v2)));
+        a1 = sq_acc(a1, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v2), 1)));
+        a2 = sq_acc(a2, _mm512_castps512_ps256(_mm512_castsi512_ps(v3)));
+        a3 = sq_acc(a3, _mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castsi512_pd(v3), 1)));
+    }
+    return _mm512_reduce_add_pd(_mm512_add_pd(_mm512_add_pd(a0, a1), _mm512_add_pd(a2, a3)));
+}
+
+double sumsq_scalar(const uint32_t *src, uint64_t n) {
+    double acc = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        float f;
+        memcpy(&f, src + i, 4);
+        acc += static_cast<double>(f) * static_cast<double>(f);
+    }
+    return acc;
+}
+
 using PackFn = double (*)(const uint32_t *, uint64_t, uint8_t *);
 
 ADT_AVX512 PackFn pick_avx512(int r, bool nt) {
@@ -237,6 +275,32 @@ double pack_unit_to(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *dst
     if (body < n) acc += pack_scalar(src + body, n - body, s.round_to, dst + body * s.round_to);
     return acc;
 }
+
+// pack_unit's sum of squares alone (same split into vector body + scalar tail)
+double sumsq_unit(const adt_segment &s, uint64_t lo, uint64_t hi) {
+    const uint32_t *src = static_cast<const uint32_t *>(s.weights) + lo;
+    const uint64_t n = hi - lo, body = have_vbmi() ? n / kGroup * kGroup : 0;
+    double acc = body ? sumsq_avx512(src, body) : 0.0;
+    if (body < n) acc += sumsq_scalar(src + body, n - body);
+    return acc;
+}
+
+// Host memory the DMA engine can read in place: [p, p + bytes) page-locked
+// (cudaHostAlloc / cudaHostRegister; both ends checked).
+bool page_locked(const void *p, uint64_t bytes) {
+    cudaPointerAttributes a;
+    const char *c = static_cast<const char *>(p);
+    for (const char *q : {c, c + (bytes ? bytes - 1 : 0)}) {
+        if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (a.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
+}
+
+constexpr uint64_t kRunMergeGap = 64;     // inter-layer pad (< 64 B with 64-B aligned payloads) ships with its run
 
 double pack_unit(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *packed) {
     return pack_unit_to(s, lo, hi, packed + s.offset + lo * static_cast<uint64_t>(s.round_to), true);
@@ -337,7 +401,7 @@ std::vector<Unit> make_units(const adt_segment *segs, int nseg) {
 // Pack every unit on `threads` threads; `on_progress(ready_prefix)` is called
 // by the caller thread between its own units with the count of leading units
 // that are complete (for the DMA pipeline). Per-unit sums go to unit_ss.
-void pack_units(const adt_segment *segs, const std::vector<Unit> &units, uint8_t *packed, int threads,
+void pack_units(const adt_segment *segs, const std::vector<Unit> &units, size_t nnorm, uint8_t *packed, int threads,
                 std::vector<double> &unit_ss, const std::function<void(size_t)> &on_progress) {
     const size_t nu = units.size();
     std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[nu == 0 ? 1 : nu]);
@@ -345,7 +409,7 @@ void pack_units(const adt_segment *segs, const std::vector<Unit> &units, uint8_t
     std::atomic<size_t> next{0};
     auto work_one = [&](size_t k) {
         const Unit &u = units[k];
-        unit_ss[k] = pack_unit(segs[u.seg], u.lo, u.hi, packed);
+        unit_ss[k] = k < nnorm ? sumsq_unit(segs[u.seg], u.lo, u.hi) : pack_unit(segs[u.seg], u.lo, u.hi, packed);
         done[k].store(1, std::memory_order_release);
     };
     const std::function<void(int)> job = [&](int) {
@@ -398,7 +462,7 @@ int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *se
     if (v != ADT_OK) return v;
     const std::vector<Unit> units = make_units(segs, nseg);
     std::vector<double> ss(units.size(), 0.0);
-    pack_units(segs, units, packed, resolve_threads(threads), ss, [](size_t) {});
+    pack_units(segs, units, 0, packed, resolve_threads(threads), ss, [](size_t) {});
     finish_sums(units, ss, nseg, seg_sumsq);
     return ADT_OK;
 }
@@ -406,9 +470,18 @@ int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *se
 int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
                        uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
                        uint64_t min_copy_bytes, void *stream) {
+    return adt_host_to_device_ex(host_segs, dev_segs, nseg, host_packed, dev_packed, packed_bytes, seg_sumsq, threads,
+                                 min_copy_bytes, 0u, nullptr, stream);
+}
+
+int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
+                          uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
+                          uint64_t min_copy_bytes, uint32_t flags, uint8_t *direct_out, void *stream) {
     int v = validate_host(host_segs, nseg, host_packed);
     if (v != ADT_OK) return v;
     if (nseg > 0 && dev_packed == nullptr) return ADT_ERR_ARG;
+    if ((flags & ~static_cast<uint32_t>(ADT_H2D_DIRECT_FULL | ADT_H2D_SKIP_DIRECT_NORMS)) != 0) return ADT_ERR_ARG;
+    if ((flags & ADT_H2D_DIRECT_FULL) && dev_segs == nullptr) return ADT_ERR_ARG;   // direct copies land in the replicas
     uint64_t end_prev = 0;                    // payloads in increasing, non-overlapping order (the DMA
     for (int i = 0; i < nseg; ++i) {          // ships the stream front to back as units complete)
         const adt_segment &h = host_segs[i];
@@ -421,29 +494,104 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
         if (h.offset < end_prev || end > packed_bytes) return ADT_ERR_ARG;
         end_prev = end;
     }
+    // Full-width layers (round_to 4: the replica is the master word for word)
+    // whose host words are page-locked skip the packer: the DMA reads them
+    // straight from the masters into the replicas (4n bytes on the link either
+    // way), so host DRAM carries their 4n once instead of read 4n + write 4n +
+    // DMA-read 4n; the device skips their unpack. Their norms still come from
+    // the host (a read-only pass). The packed stream keeps their (unused) span.
+    std::vector<uint8_t> direct(static_cast<size_t>(nseg > 0 ? nseg : 1), 0);
+    if (flags & ADT_H2D_DIRECT_FULL)
+        for (int i = 0; i < nseg; ++i)
+            direct[i] = host_segs[i].count > 0 && host_segs[i].round_to == 4 &&
+                        page_locked(host_segs[i].weights, host_segs[i].count * 4) &&
+                        reinterpret_cast<uintptr_t>(dev_segs[i].weights) % 16 == 0;
+    if (direct_out != nullptr)
+        for (int i = 0; i < nseg; ++i) direct_out[i] = direct[i];
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const std::vector<Unit> units = make_units(host_segs, nseg);
+    cudaError_t err = cudaSuccess;
+    // The direct copies go first (the DMA has work from t = 0 while the first
+    // units are packed); ADT_H2D_DIRECT_LAST=1 queues them after the packed
+    // stream instead (A/B: the packed runs then ship while the host packs, the
+    // direct layers once the host is idle).
+    static const bool direct_last = [] {
+        const char *e = getenv("ADT_H2D_DIRECT_LAST");
+        return e != nullptr && e[0] == '1';
+    }();
+    auto ship_direct = [&] {
+        for (int i = 0; i < nseg && err == cudaSuccess; ++i)
+            if (direct[i])
+                err = cudaMemcpyAsync(dev_segs[i].weights, host_segs[i].weights, host_segs[i].count * 4,
+                                      cudaMemcpyHostToDevice, st);
+    };
+    if (!direct_last) ship_direct();
+    // byte runs of the stream the DMA must carry: the packed layers' payloads,
+    // neighbours merged when only the inter-layer pad separates them
+    struct Run { uint64_t a, b; };
+    std::vector<Run> runs;
+    for (int i = 0; i < nseg; ++i) {
+        const adt_segment &h = host_segs[i];
+        if (h.count == 0 || direct[i]) continue;
+        const uint64_t a = h.offset, b = h.offset + h.count * static_cast<uint64_t>(h.round_to);
+        if (!runs.empty() && a - runs.back().b < kRunMergeGap) runs.back().b = b;
+        else runs.push_back({a, b});
+    }
+    // units: the direct layers' norm-only units first (while the DMA reads the
+    // same words), then the packed layers' units in stream order
+    std::vector<Unit> units;
+    const bool skip_direct_norms = (flags & ADT_H2D_SKIP_DIRECT_NORMS) != 0;
+    if (seg_sumsq != nullptr && !skip_direct_norms)
+        for (int s = 0; s < nseg; ++s)
+            if (direct[s])
+                for (uint64_t lo = 0; lo < host_segs[s].count; lo += kUnitWeights)
+                    units.push_back({s, lo, std::min(host_segs[s].count, lo + kUnitWeights)});
+    const size_t nnorm = units.size();
+    for (int s = 0; s < nseg; ++s)
+        if (!direct[s])
+            for (uint64_t lo = 0; lo < host_segs[s].count; lo += kUnitWeights)
+                units.push_back({s, lo, std::min(host_segs[s].count, lo + kUnitWeights)});
     std::vector<double> ss(units.size(), 0.0);
     // byte range of the packed stream that is final once units [0, k) are done:
-    // [0, start of unit k), the trailing pad included with the last unit
+    // [0, start of unit k) — nothing while the norm-only units run
     auto ready_bytes = [&](size_t k) -> uint64_t {
         if (k >= units.size()) return packed_bytes;
+        if (k < nnorm) return 0;
         const adt_segment &s = host_segs[units[k].seg];
         return s.offset + units[k].lo * static_cast<uint64_t>(s.round_to);
     };
+    size_t run = 0;
+    auto ship = [&](uint64_t a, uint64_t b) {      // copy the runs' bytes inside [a, b)
+        while (run < runs.size() && err == cudaSuccess) {
+            const uint64_t lo = std::max(a, runs[run].a), hi = std::min(b, runs[run].b);
+            if (lo < hi)
+                err = cudaMemcpyAsync(dev_packed + lo, host_packed + lo, hi - lo, cudaMemcpyHostToDevice, st);
+            if (runs[run].b > b) break;            // the rest of this run ships with a later range
+            ++run;
+        }
+    };
     uint64_t sent = 0;
-    cudaError_t err = cudaSuccess;
     const uint64_t batch = min_copy_bytes == 0 ? (1u << 20) : min_copy_bytes;
-    pack_units(host_segs, units, host_packed, resolve_threads(threads), ss, [&](size_t prefix) {
+    pack_units(host_segs, units, nnorm, host_packed, resolve_threads(threads), ss, [&](size_t prefix) {
         const uint64_t end = ready_bytes(prefix);
         if (err != cudaSuccess || end <= sent) return;
         if (end - sent < batch && prefix < units.size()) return;
-        err = cudaMemcpyAsync(dev_packed + sent, host_packed + sent, end - sent, cudaMemcpyHostToDevice, st);
+        ship(sent, end);
         sent = end;
     });
+    if (direct_last) ship_direct();
     finish_sums(units, ss, nseg, seg_sumsq);
+    if (seg_sumsq != nullptr && skip_direct_norms)
+        for (int i = 0; i < nseg; ++i)
+            if (direct[i]) seg_sumsq[i] = __builtin_nan("");     // the caller's to fill (device pass)
     if (err != cudaSuccess) return ADT_ERR_CUDA_BASE - static_cast<int>(err);
-    return dev_segs == nullptr ? ADT_OK : adt_unpack(dev_segs, nseg, dev_packed, stream);
+    if (dev_segs == nullptr) return ADT_OK;
+    bool any_direct = false;
+    for (int i = 0; i < nseg; ++i) any_direct = any_direct || direct[i];
+    if (!any_direct) return adt_unpack(dev_segs, nseg, dev_packed, stream);
+    std::vector<adt_segment> rest(dev_segs, dev_segs + nseg);     // the direct layers are complete already
+    for (int i = 0; i < nseg; ++i)
+        if (direct[i]) rest[i].count = 0;
+    return adt_unpack(rest.data(), nseg, dev_packed, stream);
 }
 
 int adt_host_to_device_ring(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *ring,

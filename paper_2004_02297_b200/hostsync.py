@@ -67,7 +67,7 @@ class HostWeightSync:
 
     def __init__(self, masters: Sequence, schedule=None, replicas: Sequence[torch.Tensor] | None = None,
                  device: torch.device | str | None = None, threads: int = 0, min_copy_bytes: int = 1 << 20,
-                 ring_bytes: int = 0, slot_bytes: int = 384 << 10):
+                 ring_bytes: int = 0, slot_bytes: int = 384 << 10, direct_full: bool = True):
         engine.require_cuda()
         self.masters = [_host_view(m, i) for i, m in enumerate(masters)]
         self.counts = [m.size for m in self.masters]
@@ -83,6 +83,13 @@ class HostWeightSync:
         if [r.numel() for r in self.replicas] != self.counts:
             raise ValueError("replica sizes differ from the masters")
         self.threads = int(threads)
+        # direct_full: layers at full width (round_to 4) whose masters are
+        # page-locked go to their replicas by DMA straight from the masters
+        # (adt_host_to_device_ex, ADT_H2D_DIRECT_FULL) instead of through the
+        # host packer and the device unpack: identical replicas and norms, the
+        # same bytes on the link, a third of the host DRAM traffic for them.
+        self.direct_full = bool(direct_full)
+        self.direct = np.zeros(max(1, L), dtype=np.uint8)   # which layers the last launch sent that way
         self.min_copy_bytes = int(min_copy_bytes)
         cap = PackedLayout.plan(self.counts, [4] * L, align=HOST_ALIGN).nbytes
         # ring_bytes = 0 (default): one pinned staging buffer as large as the
@@ -100,6 +107,11 @@ class HostWeightSync:
         self.sumsq = np.zeros(max(1, L), dtype=np.float64)
         self._dma_done = torch.cuda.Event()
         self._dma_pending = False
+        # device-side norms of the direct layers (their replica equals the master)
+        self._dn_idx: list[int] = []
+        self._dn_table = None
+        self._dn_done = torch.cuda.Event()
+        self._dn_pending = False
         self._plan(self.schedule.round_tos())
 
     def _plan(self, round_tos) -> None:
@@ -138,9 +150,15 @@ class HostWeightSync:
                 self._host_segs, dev_segs, len(self.counts), self._stage_ptr, self.ring_bytes, self.slot_bytes,
                 self.packed.data_ptr(), self.layout.nbytes, sums, self.threads, int(s.cuda_stream)))
         else:
-            _lib.check(lib.adt_host_to_device(
+            flags = (_lib.H2D_DIRECT_FULL | _lib.H2D_SKIP_DIRECT_NORMS) if (self.direct_full and dev_segs is not None) \
+                else 0
+            self._dn_pending = False
+            _lib.check(lib.adt_host_to_device_ex(
                 self._host_segs, dev_segs, len(self.counts), self._stage_ptr, self.packed.data_ptr(),
-                self.layout.nbytes, sums, self.threads, self.min_copy_bytes, int(s.cuda_stream)))
+                self.layout.nbytes, sums, self.threads, self.min_copy_bytes, flags, self.direct.ctypes.data,
+                int(s.cuda_stream)))
+            if fused_norm and flags and self.direct.any():
+                self._direct_norms(s)
         if events is not None:
             events[1].record(s)
             engine.unpack(self.unpack_table, self.packed, s)
@@ -148,8 +166,31 @@ class HostWeightSync:
         self._dma_done.record(s)
         self._dma_pending = True
 
+    def _direct_norms(self, s) -> None:
+        """The direct layers' sums of squares, on the device from their replicas
+        (bit-equal to the masters at full width): adt_sumsq on `s` behind the
+        copies, then an 8-B-per-layer device->host read that norms() waits for.
+        A host read of those masters beside their DMA would slow the DMA
+        (profiles/r02_host_direct.md)."""
+        idx = [i for i in range(len(self.counts)) if self.direct[i]]
+        if idx != self._dn_idx:
+            self._dn_idx = idx
+            lay = PackedLayout.plan([self.counts[i] for i in idx], [4] * len(idx))
+            self._dn_table = engine.SegmentTable([self.replicas[i] for i in idx], lay)
+            self._dn_dev = torch.empty(len(idx), dtype=torch.float64, device=self.device)
+            self._dn_host = torch.empty(len(idx), dtype=torch.float64, pin_memory=True)
+        engine.sumsq(self._dn_table, self._dn_dev, s)
+        self._dn_host.copy_(self._dn_dev, non_blocking=True)
+        self._dn_done.record(s)
+        self._dn_pending = True
+
     def norms(self) -> list[float]:
         """precision.l2_norm of every master as of the last launch with the norm fused."""
+        if self._dn_pending:
+            self._dn_done.synchronize()
+            for j, i in enumerate(self._dn_idx):
+                self.sumsq[i] = float(self._dn_host[j])
+            self._dn_pending = False
         return [math.sqrt(v) for v in self.sumsq[:len(self.counts)]]
 
     def step(self, batch: int = 0, observe: bool | None = None, events=None) -> SyncResult:

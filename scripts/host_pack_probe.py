@@ -54,17 +54,31 @@ def main():
             def round_tos(self):
                 return list(rs)
 
-        ring_sync = hostsync.HostWeightSync(host, Fixed(len(counts), 32))
         sync = hostsync.HostWeightSync(host, Fixed(len(counts), 32), ring_bytes=0)
         s = torch.cuda.current_stream()
 
-        def adt_step():
-            sync.launch(fused_norm=True)
-            s.synchronize()
+        def step_of(sy):
+            def f():
+                sy.launch(fused_norm=True)
+                s.synchronize()
+            return f
 
-        def ring_step():
-            ring_sync.launch(fused_norm=True)
-            s.synchronize()
+        adt_step = step_of(sync)
+        pinned = []
+        for h in host:
+            t = torch.empty(h.size, dtype=torch.float32, pin_memory=True)
+            t.numpy()[:] = h
+            pinned.append(t.numpy())
+        dsync = hostsync.HostWeightSync(pinned, Fixed(len(counts), 32))
+        t_direct = best(step_of(dsync))
+        print(f"   {name}: pinned masters, direct_full ({int(dsync.direct[:len(counts)].sum())} layers direct) "
+              f"{t_direct * 1e3:.2f} ms")
+        del dsync
+        for slot in (384 << 10, 2 << 20, 8 << 20):
+            ring = max(48 << 20, 20 * slot)
+            rsync = hostsync.HostWeightSync(host, Fixed(len(counts), 32), ring_bytes=ring, slot_bytes=slot)
+            print(f"   {name}: ring {ring >> 20} MiB, {slot >> 10} KiB slots: {best(step_of(rsync)) * 1e3:.2f} ms")
+            del rsync
 
         flat = torch.empty(sum(counts), dtype=torch.float32).pin_memory()
         dev = torch.empty_like(flat, device="cuda")
@@ -73,9 +87,7 @@ def main():
             dev.copy_(flat, non_blocking=True)
             s.synchronize()
 
-        t_adt, t_raw, t_ring = best(adt_step), best(raw), best(ring_step)
-        print(f"   {name}: ring ({ring_sync.ring_bytes >> 20} MiB, {ring_sync.slot_bytes >> 10} KiB slots) "
-              f"{t_ring * 1e3:.2f} ms vs full staging {t_adt * 1e3:.2f} ms")
+        t_adt, t_raw = best(adt_step), best(raw)
         lib = hostsync._lib.load()
         L = len(counts)
 
@@ -95,7 +107,7 @@ def main():
         print(f"{name} r={sorted(set(rs))}: HostWeightSync {t_adt * 1e3:7.2f} ms ({sync.h2d_bytes / 1e6:.0f} MB over "
               f"PCIe) vs raw FP32 pinned H2D {t_raw * 1e3:7.2f} ms ({4 * n / 1e6:.0f} MB): "
               f"{t_raw / t_adt:.2f}x")
-        del sync, ring_sync, flat, dev
+        del sync, flat, dev, pinned
 
 
 if __name__ == "__main__":

@@ -33,7 +33,7 @@ def test_header_declares_the_expected_surface():
          "adt_unpack_multi_dyn", "adt_awp_combine", "adt_awp_fixup_pieces", "adt_awp_fixup_gather",
          "adt_device_sm_count", "adt_pack_host", "adt_host_to_device", "adt_host_threads", "adt_host_simd",
          "adt_sumsq_f64_partials", "adt_sumsq_f64", "adt_roundtrip", "adt_roundtrip_max_tiles",
-         "adt_host_to_device_ring"])
+         "adt_host_to_device_ring", "adt_host_to_device_ex"])
 
 
 def test_library_exports_every_declared_symbol(lib):

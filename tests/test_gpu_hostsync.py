@@ -56,6 +56,71 @@ def test_replicas_and_norms_mixed_widths(adt, ring):
     assert sync.h2d_bytes < 4 * sum(counts)
 
 
+def _pinned_copy(h):
+    t = torch.empty(h.size, dtype=torch.float32, pin_memory=True)
+    t.numpy()[:] = h
+    return t
+
+
+def test_direct_full_width_layers_from_pinned_masters(adt):
+    """ADT_H2D_DIRECT_FULL: r = 4 layers with page-locked masters are DMA'd
+    straight into their replicas (no host pack, no device unpack); the other
+    layers take the packed path. Replicas and norms equal the all-packed path
+    bit for bit (norms: the direct layers' come from a device pass over the
+    replicas, within 1e-12 of the host pass); pageable masters never go direct."""
+    rng = np.random.default_rng(11)
+    counts = [5000, 65536 * 2 + 7, 4097, 0, 300000, 65, 3]
+    rs = [4, 1, 4, 4, 3, 4, 2]
+    hosts = [rng.standard_normal(n, dtype=np.float32) * np.float32(0.1) for n in counts]
+    hosts[2][:12] = np.array(O.SPECIAL_WORDS[:12], np.uint32).view(np.float32)
+    hosts[2][:12][~np.isfinite(hosts[2][:12])] = 1.0  # keep this layer's norm finite
+    pinned = [_pinned_copy(h) for h in hosts]
+
+    class Fixed(adt.FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    direct = adt.HostWeightSync(pinned, Fixed(len(counts), 32))
+    packed = adt.HostWeightSync(pinned, Fixed(len(counts), 32), direct_full=False)
+    pageable = adt.HostWeightSync(hosts, Fixed(len(counts), 32))
+    for sync in (direct, packed, pageable):
+        for _ in range(2):
+            for r_ in sync.replicas:
+                r_.fill_(float("nan"))
+            sync.launch(fused_norm=True)
+            torch.cuda.synchronize()
+            for i, (h, r) in enumerate(zip(hosts, rs)):
+                want = h.view(np.uint32) & np.uint32(O.keep_mask(r))
+                assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), i
+    assert list(direct.direct[:len(counts)]) == [1, 0, 1, 0, 0, 1, 0]
+    assert not packed.direct.any() and not pageable.direct.any()
+    assert packed.norms() == pageable.norms()                          # bit-identical host sums
+    for a, b, r in zip(direct.norms(), packed.norms(), rs):
+        assert (a == b) if r != 4 else abs(a - b) <= 1e-12 * max(b, 1e-30)
+    for i, h in enumerate(hosts):
+        ref = O.l2_norm(h)
+        assert abs(direct.norms()[i] - ref) <= NORM_RTOL * max(ref, 1e-30), i
+    # flags = DIRECT_FULL alone: the direct layers' norms from the host pass, bit-equal to the packed path's
+    from paper_2004_02297_b200 import _lib
+    ss = np.zeros(len(counts), dtype=np.float64)
+    flags_out = np.zeros(len(counts), dtype=np.uint8)
+    _lib.check(_lib.load().adt_host_to_device_ex(
+        direct._host_segs, direct.unpack_table.array, len(counts), direct._stage_ptr, direct.packed.data_ptr(),
+        direct.layout.nbytes, ss.ctypes.data, 0, 0, _lib.H2D_DIRECT_FULL, flags_out.ctypes.data,
+        torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert list(flags_out) == [1, 0, 1, 0, 0, 1, 0]
+    assert [math.sqrt(v) for v in ss] == packed.norms()
+    # masters updated in place on the host: the next launch carries the new words
+    for p_ in pinned:
+        p_.mul_(2.0)
+    direct.launch(fused_norm=True)
+    torch.cuda.synchronize()
+    for i, (p_, r) in enumerate(zip(pinned, rs)):
+        want = p_.numpy().view(np.uint32) & np.uint32(O.keep_mask(r))
+        assert np.array_equal(direct.replicas[i].cpu().numpy().view(np.uint32), want), i
+
+
 @pytest.mark.parametrize("ring", [0, 48 * (320 << 10), 17 * (320 << 10)])
 def test_large_set_in_many_copies(adt, ring):
     """A stream much larger than one copy batch: the DMA of early units overlaps
