@@ -666,9 +666,30 @@ def run_cold_roofline(sync, pack_bytes, unpack_bytes, hbm, fused_norm=True):
     pg, ug = pack_bytes / (p * 1e-3) / 1e9, unpack_bytes / (u * 1e-3) / 1e9
     del sets
     torch.cuda.empty_cache()
+    # Size-matched copy ceiling: one streaming kernel moving the pack's byte
+    # volume (pack_bytes / 2 read + the same written), same rotation (K
+    # source/destination pairs, one launch each): what a plain copy reaches on
+    # a stream of this size, launch ramp and drain included.
+    half = max(16, pack_bytes // 2 // 16 * 16)
+    pairs = [(torch.empty(half // 4, dtype=torch.float32, device=dev),
+              torch.empty(half // 4, dtype=torch.float32, device=dev)) for _ in range(K)]
+    for a, b in pairs:
+        a.fill_(1)
+
+    def copies():                                    # an SM streaming kernel (inside a CUDA graph a
+        for a, b in pairs:                           # copy_ becomes a copy-engine memcpy node: ~3 TB/s)
+            torch.neg(a, out=b)
+
+    c = _graph_ms([copies], reps=reps_per) / K
+    cg = 2 * half / (c * 1e-3) / 1e9
+    del pairs
+    torch.cuda.empty_cache()
     return {"pack_ms": p, "unpack_ms": u, "pack_GBps": pg, "unpack_GBps": ug, "pack_frac": pg / hbm,
             "unpack_frac": ug / hbm, "frac": min(pg, ug) / hbm, "frac_spec": min(pg, ug) / SPEC_HBM_GBPS,
-            "method": f"rotation over {K} buffer sets, CUDA graph of {reps_per * K} launches, median of 5 replays"}
+            "size_matched_copy_GBps": cg, "frac_of_size_matched_copy": min(pg, ug) / cg,
+            "method": f"rotation over {K} buffer sets, CUDA graph of {reps_per * K} launches, median of 5 replays; "
+                      f"size-matched copy: torch float32 elementwise kernel (neg) reading and writing {half} B each, "
+                      f"same rotation"}
 
 
 def traffic_of(kernel, args):

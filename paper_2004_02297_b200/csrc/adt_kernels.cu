@@ -417,6 +417,14 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
     __syncwarp();
 }
 
+#ifndef ADT_PDL
+// 1: pack triggers its dependents early and the unpack launches as a
+// programmatic dependent. Measured (profiles/r02_ab_pdl.md): ResNet-50 step
+// -0.6 us, but AlexNet +4.2 us and VGG-16 +12 us — the early-resident unpack
+// CTAs keep the side-stream finalize off the SMs and slow the unpack itself.
+// Off; with 1 the runtime switch ADT_PDL=0 disables the launch attribute.
+#define ADT_PDL 0
+#endif
 // WRITE=false is the norm-only pass (adt_sumsq).
 #ifndef ADT_PACK_MIN_BLOCKS
 #define ADT_PACK_MIN_BLOCKS 6   // resident CTAs/SM the register budget must allow (A/B: profiles/r01_ab_occupancy.md)
@@ -469,6 +477,13 @@ __global__ void __launch_bounds__(kThreads, ADT_PACK_MIN_BLOCKS)
 adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     uint32_t *ws = stage[threadIdx.x >> 5];
+#if ADT_PDL && __CUDA_ARCH__ >= 900
+    // Let a programmatic dependent (finalize, unpack) be scheduled as soon as
+    // every pack CTA has started: its launch and CTA rasterisation overlap the
+    // pack's last wave; it still reads nothing before griddepcontrol.wait,
+    // which waits for this whole grid and its memory operations.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     if (!ADT_PERSISTENT) {
         const uint32_t tile = blockIdx.x;
         pack_tile<MAXSEG, NORM, WRITE>(T, tile, find_segment(T, tile), ws);
@@ -569,6 +584,13 @@ __global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
 adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
     uint32_t *ws = stage[threadIdx.x >> 5];
+#if ADT_PDL && __CUDA_ARCH__ >= 900
+    // Launched as a programmatic dependent (launch_unpack): before touching the
+    // packed stream, the replicas or the abort word, wait for the preceding
+    // grid (the pack, a barrier, ...) to complete and flush. A no-op when the
+    // launch was an ordinary one.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     if (aborted(T.abort)) return;
     // Newest-first (ADT_UNPACK_REVERSE): CTAs are dispatched roughly in
     // blockIdx order, so walking the tiles backwards reads the payload the
@@ -765,6 +787,33 @@ cudaError_t launch_finalize(const Table<MAXSEG> &T, bool pdl, cudaStream_t strea
     return cudaLaunchKernelEx(&cfg, adt_norm_finalize_kernel<MAXSEG>, T);
 }
 
+// The unpack as a programmatic dependent of whatever precedes it on the
+// stream (the kernel's griddepcontrol.wait keeps it ordered after that grid):
+// behind the pack pass its launch overlaps the pack's last wave. Runtime A/B:
+// ADT_PDL=0 launches it as an ordinary kernel.
+bool pdl_unpack() {
+    static const bool v = [] {
+        const char *e = getenv("ADT_PDL");
+        return ADT_PDL && !(e != nullptr && e[0] == '0');
+    }();
+    return v;
+}
+
+template <int MAXSEG>
+cudaError_t launch_unpack(const Table<MAXSEG> &T, dim3 grid, uint32_t ntiles, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_unpack() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, adt_unpack_kernel<MAXSEG>, T, ntiles);
+}
+
 // nsrc == 0: `reserved` must be 0 (single packed buffer); otherwise it names
 // the source buffer (adt_unpack_multi) and must be < nsrc.
 int validate(const adt_segment *segs, int nseg, const void *packed, bool need_packed, int nsrc = 0) {
@@ -833,10 +882,10 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *co
                 case Pass::Pack: adt_pack_kernel<MAXSEG, false, true><<<grid, block, 0, stream>>>(T, ntiles); break;
                 case Pass::PackNorm: adt_pack_kernel<MAXSEG, true, true><<<grid, block, 0, stream>>>(T, ntiles); break;
                 case Pass::Norm: adt_pack_kernel<MAXSEG, true, false><<<grid, block, 0, stream>>>(T, ntiles); break;
-                case Pass::Unpack: adt_unpack_kernel<MAXSEG><<<grid, block, 0, stream>>>(T, ntiles); break;
+                case Pass::Unpack: e = launch_unpack<MAXSEG>(T, grid, ntiles, stream); break;
                 case Pass::Finalize: break;
             }
-            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaGetLastError();
         }
     }
     // PDL only directly behind this call's own pack pass; a standalone
