@@ -190,10 +190,11 @@ __device__ __forceinline__ double sq_acc(double acc, uint32_t w) {
 // every CTA resident ~1 us longer, profiles/r01_v1_*). adt_norm_finalize_kernel
 // sums a layer's partials in (tile, warp) order.
 constexpr int kWarpsPerTile = kThreads / 32;
-__device__ __forceinline__ void warp_partial(double *partials, uint32_t tile, double acc) {
+__device__ __forceinline__ void warp_partial(double *partials, uint32_t tile, double acc,
+                                             int warp = static_cast<int>(threadIdx.x >> 5)) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
-    if ((threadIdx.x & 31) == 0) partials[tile * kWarpsPerTile + (threadIdx.x >> 5)] = acc;
+    if ((threadIdx.x & 31) == 0) partials[tile * kWarpsPerTile + warp] = acc;
 }
 
 // Per layer (one CTA each): fixed-order sum of its partials -> seg_sumsq.
@@ -439,11 +440,12 @@ __device__ __forceinline__ void store_packed(uint8_t *dst, const uint4 (&v)[kVec
 #endif
 
 template <int MAXSEG, bool NORM, bool WRITE, bool BULK = (ADT_PACK_BULK_STORE != 0)>
-__device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
+__device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws,
+                                          int warp = static_cast<int>(threadIdx.x >> 5)) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
     const int r = width_of(T, s);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     const uint32_t g0 = warp * kWarpGroups + lane;                 // group of j = 0
     const uint4 *src = reinterpret_cast<const uint4 *>(T.weights[s]) + e0 / 4;
 
@@ -469,13 +471,25 @@ __device__ __forceinline__ void pack_tile(const Table<MAXSEG> &T, uint32_t tile,
 
     if (WRITE) store_packed<BULK>(T.packed_out + T.offset[s] + e0 * r, v, m, r, warp, lane, g0, ws);
 
-    if (NORM) warp_partial(T.partials, tile, sumsq16(v));
+    if (NORM) warp_partial(T.partials, tile, sumsq16(v), warp);
 }
 
+// Split CTAs (ADT_CTA_WARPS = 4 or 2): a CTA of kCtaWarps warps runs warps
+// [sub*kCtaWarps, (sub+1)*kCtaWarps) of tile blockIdx.x / kSplit — the same
+// per-warp slices, bytes and norm partials as one 8-warp CTA per tile, in
+// shorter-lived CTAs (a smaller drain tail at the end of the grid). A/B.
+#ifndef ADT_CTA_WARPS
+#define ADT_CTA_WARPS 8
+#endif
+constexpr int kCtaWarps = ADT_CTA_WARPS;
+constexpr int kCtaThreads = 32 * kCtaWarps;
+constexpr int kSplit = kWarpsPerTile / kCtaWarps;
+static_assert(kSplit * kCtaWarps == kWarpsPerTile, "CTA warps must divide the tile's warps");
+
 template <int MAXSEG, bool NORM, bool WRITE>
-__global__ void __launch_bounds__(kThreads, ADT_PACK_MIN_BLOCKS)
+__global__ void __launch_bounds__(kCtaThreads, ADT_PACK_MIN_BLOCKS * kSplit)
 adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
-    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    __shared__ __align__(16) uint32_t stage[kCtaWarps][kWarpStageWords];
     uint32_t *ws = stage[threadIdx.x >> 5];
 #if ADT_PDL && __CUDA_ARCH__ >= 900
     // Let a programmatic dependent (finalize, unpack) be scheduled as soon as
@@ -485,8 +499,9 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
     if (!ADT_PERSISTENT) {
-        const uint32_t tile = blockIdx.x;
-        pack_tile<MAXSEG, NORM, WRITE>(T, tile, find_segment(T, tile), ws);
+        const uint32_t tile = blockIdx.x / kSplit;
+        const int warp = static_cast<int>(blockIdx.x % kSplit) * kCtaWarps + static_cast<int>(threadIdx.x >> 5);
+        pack_tile<MAXSEG, NORM, WRITE>(T, tile, find_segment(T, tile), ws, warp);
         return;
     }
     int s = find_segment(T, blockIdx.x);
@@ -510,11 +525,12 @@ adt_pack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
 #define ADT_UNPACK_REVERSE 1   // A/B: AlexNet step 132.7 -> 127.2 us (profiles/r01_ab_unpack_order.md)
 #endif
 template <int MAXSEG>
-__device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws) {
+__device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t tile, int s, uint32_t *ws,
+                                            int warp = static_cast<int>(threadIdx.x >> 5)) {
     const uint64_t e0 = static_cast<uint64_t>(tile - T.tile_begin[s]) * kTile;
     const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), T.count[s] - e0));
     const int r = width_of(T, s);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     const uint32_t g0 = warp * kWarpGroups + lane;
     const uint8_t *src = T.srcs[T.src_idx[s]] + T.offset[s] + e0 * r;
     uint4 *dst = reinterpret_cast<uint4 *>(T.weights[s]) + e0 / 4;
@@ -580,9 +596,9 @@ __device__ __forceinline__ void unpack_tile(const Table<MAXSEG> &T, uint32_t til
 }
 
 template <int MAXSEG>
-__global__ void __launch_bounds__(kThreads, ADT_UNPACK_MIN_BLOCKS)
+__global__ void __launch_bounds__(kCtaThreads, ADT_UNPACK_MIN_BLOCKS * kSplit)
 adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
-    __shared__ __align__(16) uint32_t stage[kWarpsPerTile][kWarpStageWords];
+    __shared__ __align__(16) uint32_t stage[kCtaWarps][kWarpStageWords];
     uint32_t *ws = stage[threadIdx.x >> 5];
 #if ADT_PDL && __CUDA_ARCH__ >= 900
     // Launched as a programmatic dependent (launch_unpack): before touching the
@@ -600,9 +616,11 @@ adt_unpack_kernel(const __grid_constant__ Table<MAXSEG> T, uint32_t ntiles) {
         // Rotated walk (adt_unpack_multi_ex): each rank starts right before its
         // own pieces, so at any moment the ranks pull from different peers
         // instead of all draining the same owner's NVLink port in lockstep.
-        uint32_t tile = (ADT_UNPACK_REVERSE ? ntiles - 1 - blockIdx.x : blockIdx.x) + T.tile_rot;
+        const uint32_t b = blockIdx.x / kSplit;
+        const int warp = static_cast<int>(blockIdx.x % kSplit) * kCtaWarps + static_cast<int>(threadIdx.x >> 5);
+        uint32_t tile = (ADT_UNPACK_REVERSE ? ntiles - 1 - b : b) + T.tile_rot;
         if (tile >= ntiles) tile -= ntiles;
-        unpack_tile<MAXSEG>(T, tile, find_segment(T, tile), ws);
+        unpack_tile<MAXSEG>(T, tile, find_segment(T, tile), ws, warp);
         return;
     }
     if (ADT_UNPACK_REVERSE) {
@@ -803,7 +821,7 @@ template <int MAXSEG>
 cudaError_t launch_unpack(const Table<MAXSEG> &T, dim3 grid, uint32_t ntiles, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(ADT_PERSISTENT ? kThreads : kCtaThreads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -869,8 +887,10 @@ int launch_chunk(Pass pass, const adt_segment *segs, int nseg, const uint8_t *co
         if (use_tma_kernels() && dyn_r == nullptr) {
             e = launch_tma<MAXSEG>(pass, T, ntiles, stream);
         } else {
-            const dim3 block(kThreads);
-            uint32_t g = ntiles;
+            const bool split = !ADT_PERSISTENT && (pass == Pass::Pack || pass == Pass::PackNorm ||
+                                                   pass == Pass::Norm || pass == Pass::Unpack);
+            const dim3 block(split ? kCtaThreads : kThreads);
+            uint32_t g = split ? ntiles * kSplit : ntiles;
             if (ADT_PERSISTENT) {
                 int sms = 0;
                 if (sm_count_cached(&sms) != ADT_OK) return ADT_ERR_NO_DEVICE;
@@ -911,7 +931,7 @@ int run(Pass pass, const adt_segment *segs, int nseg, const uint8_t *const *srcs
         uint64_t tiles = 0;
         while (base + cnt < nseg && cnt < kLargeSeg) {
             const uint64_t t = (segs[base + cnt].count + kTile - 1) / kTile;
-            if (cnt > 0 && tiles + t > static_cast<uint64_t>(INT_MAX)) break;
+            if (cnt > 0 && tiles + t > static_cast<uint64_t>(INT_MAX / kSplit)) break;
             tiles += t;
             ++cnt;
         }
