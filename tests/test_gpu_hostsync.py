@@ -147,16 +147,20 @@ def test_large_set_in_many_copies(adt, ring):
         assert dev[lo:hi].tobytes() == O.pack_vectorized(h, r)
 
 
-def test_lenet_awp_walk_host_masters(adt, golden_lenet):
+@pytest.mark.parametrize("pinned", [False, True])
+def test_lenet_awp_walk_host_masters(adt, golden_lenet, pinned):
     """SURVEY §8d config 1 through the CPU-master path: the host arrays are the
     masters (updated in place), norms come from the host pass, widths / trace
-    rows / payloads / replicas equal the reference run's."""
+    rows / payloads / replicas equal the reference run's. pinned: page-locked
+    masters, so every layer AWP has widened to 32 bits goes by direct DMA with
+    its norm from the device (about half of the walk's layer-steps)."""
     steps = int(golden_lenet["steps"])
     walk = list(O.lenet_walk(steps, seed=7))
     L = len(walk[0][1])
     cfg = adt.PrecisionConfig(threshold=-2e-3, interval=int(golden_lenet["interval"]), step_bits=8, initial_bits=8)
-    masters = [w.copy() for w in walk[0][1]]
+    masters = [_pinned_copy(w.reshape(-1)).numpy().reshape(w.shape) if pinned else w.copy() for w in walk[0][1]]
     sync = adt.HostWeightSync(masters, adt.PrecisionController(L, cfg))
+    direct_steps = 0
     trace = []
     for t in range(steps):
         for m, w in zip(masters, walk[t][1]):
@@ -168,7 +172,10 @@ def test_lenet_awp_walk_host_masters(adt, golden_lenet):
         dev = sync.packed.cpu().numpy()
         for i in range(L):
             lo, hi = sync.layout.span(i)
-            assert hashlib.sha256(dev[lo:hi].tobytes()).digest() == golden_lenet["payload_sha"][t, i].tobytes()
+            if sync.direct[i]:                 # sent as FP32 straight into the replica: no packed payload
+                direct_steps += 1
+            else:
+                assert hashlib.sha256(dev[lo:hi].tobytes()).digest() == golden_lenet["payload_sha"][t, i].tobytes()
             rep = sync.replicas[i].cpu().numpy()
             assert hashlib.sha256(rep.tobytes()).digest() == golden_lenet["unpacked_sha"][t, i].tobytes()
     for m, w in zip(masters, walk[steps][1]):
@@ -180,6 +187,7 @@ def test_lenet_awp_walk_host_masters(adt, golden_lenet):
         assert (b, layer) == (t, i)
         assert bits == golden_lenet["bits"][t, i] and counter == golden_lenet["counter"][t, i], (t, i)
         assert abs(norm - golden_lenet["norms"][t, i]) <= NORM_RTOL * golden_lenet["norms"][t, i]
+    assert (direct_steps > 100) == pinned
 
 
 def test_rejects_device_and_strided_masters(adt):
