@@ -18,7 +18,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_
 for v in 1 2 3; do timeout 600 ncu --set full --clock-control none --import-source on -k regex:adt_ -s 6 -c 2 -o $OUT/prof_vgg16_r$v python bench.py --config vgg16 --bits $((8*v)) --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-reduce --no-awp-step --quiet-extra --eager > /dev/null 2>&1; done
 for t in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $t python scripts/sanitize_smoke.py > $OUT/sanitize_$t.log 2>&1; done
 ADT_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 --transport p2p > $OUT/bench_n2_gloo_p2p.json 2> $OUT/bench_n2_gloo_p2p.err
+ADT_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus 8 --steps 3 --warmup 3 --transport p2p --no-reduce > $OUT/bench_n8_gloo_p2p.json 2> $OUT/bench_n8_gloo_p2p.err
 PROBE_QUICK=1 timeout 900 python scripts/host_pack_probe.py > $OUT/host_probe.txt 2>&1
+timeout 900 python scripts/direct_probe.py > $OUT/direct_probe.txt 2>&1
 timeout 300 python scripts/small_step_probe.py > $OUT/small_step.txt 2>&1
 timeout 600 python scripts/step_overhead.py > $OUT/step_overhead.txt 2>&1
 timeout 600 python scripts/table2.py > $OUT/table2.md 2>&1
