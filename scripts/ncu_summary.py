@@ -90,32 +90,55 @@ def traffic(rep, config):
 
 
 def launches(path):
+    """Launch list: per kernel, launches, mean duration and share of the total;
+    when the capture also holds dram__bytes_read/write.sum, the mean DRAM bytes
+    per launch. Then each adt_ kernel's share of one step."""
     rows = list(csv.reader(open(path)))
     hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[hdr_i]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    tot = {}
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    ii = hdr.index("ID") if "ID" in hdr else None
+    dur, rd, wr = {}, {}, {}
+    dur_unit = "ns"
     for r in rows[hdr_i + 1:]:
         if len(r) <= vi:
             continue
         k = r[ki].split("(")[0]
+        metric = r[mi] if mi is not None else "gpu__time_duration.sum"
         v = float(r[vi].replace(",", ""))
-        tot.setdefault(k, []).append(v)
-    all_t = sum(sum(v) for v in tot.values())
-    print("| kernel | launches | mean | total share |\n|---|---|---|---|")
-    for k, v in sorted(tot.items(), key=lambda kv: -sum(kv[1])):
-        print(f"| `{k}` | {len(v)} | {sum(v) / len(v):.2f} {rows[hdr_i + 1][ui]} | {sum(v) / all_t:.1%} |")
+        if metric == "gpu__time_duration.sum":
+            dur.setdefault(k, []).append(v)
+            dur_unit = r[ui]
+        elif metric == "dram__bytes_read.sum":
+            rd.setdefault(k, []).append(v * _SCALE.get(r[ui], 1.0))
+        elif metric == "dram__bytes_write.sum":
+            wr.setdefault(k, []).append(v * _SCALE.get(r[ui], 1.0))
+    all_t = sum(sum(v) for v in dur.values())
+    has_dram = bool(rd)
+    extra_h = " DRAM read MB / launch | DRAM write MB / launch |" if has_dram else ""
+    print(f"| kernel | launches | mean duration | total share |{extra_h}\n|---|---|---|---|" + ("---|---|" if has_dram else ""))
+    for k, v in sorted(dur.items(), key=lambda kv: -sum(kv[1])):
+        extra = ""
+        if has_dram:
+            r_ = rd.get(k, [0.0])
+            w_ = wr.get(k, [0.0])
+            extra = f" {sum(r_) / len(r_) / 1e6:.1f} | {sum(w_) / len(w_) / 1e6:.1f} |"
+        print(f"| `{k}` | {len(v)} | {sum(v) / len(v):.2f} {dur_unit} | {sum(v) / all_t:.1%} |{extra}")
     # the ADT step alone (the process also launches setup kernels: input
     # generation, the L2-flush read): each adt_ kernel's share of the step
-    adt = {k: v for k, v in tot.items() if "adt_" in k}
+    adt = {k: v for k, v in dur.items() if "adt_" in k}
     step = sum(sum(v) / len(v) for v in adt.values())
     if adt:
         print("\nShare of one step (mean launch time of each adt_ kernel / their sum; ncu serialises launches, "
               "so the side-stream finalize is counted as if it ran alone):\n")
-        print("| kernel | mean | share of step |\n|---|---|---|")
+        print("| kernel | mean duration | share of step |\n|---|---|---|")
         for k, v in sorted(adt.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
             m = sum(v) / len(v)
-            print(f"| `{k}` | {m:.2f} {rows[hdr_i + 1][ui]} | {m / step:.1%} |")
+            print(f"| `{k}` | {m:.2f} {dur_unit} | {m / step:.1%} |")
+
+
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 if __name__ == "__main__":
