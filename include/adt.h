@@ -341,7 +341,8 @@ int adt_pack_host(const adt_segment *segs, int nseg, uint8_t *packed, double *se
  * The CPU-master transfer, pipelined: adt_pack_host of host_segs into the
  * pinned staging buffer host_packed; while the host threads pack, the calling
  * thread queues cudaMemcpyAsync (on `stream`) of every finished run of the
- * packed stream (>= min_copy_bytes, 0 = 1 MiB) into dev_packed, so the PCIe
+ * packed stream (>= min_copy_bytes; 0 = automatic: 1 MiB, or a quarter of a
+ * stream under 4 MiB but >= 64 KiB) into dev_packed, so the PCIe
  * DMA overlaps the packing; then adt_unpack of dev_segs (device replicas, the
  * same counts / offsets / round_to, payloads in increasing offset order) from
  * dev_packed — or no unpack when dev_segs is NULL (the caller queues it). Only Σ n·r (+ pad) bytes cross the link instead of 4n.
@@ -369,11 +370,17 @@ int adt_host_to_device(const adt_segment *host_segs, const adt_segment *dev_segs
  *     master at full width). Measured on the B200 host: a host read of the
  *     direct layers running beside their DMA slows the DMA by up to 40 %
  *     (profiles/r02_host_direct.md).
+ *   ADT_H2D_ZERO_COPY — no staging copies: host_packed must be page-locked
+ *     (device-mapped), and the unpack reads the packed stream from it across
+ *     the link once the host has packed it (dev_packed is not written). For
+ *     small streams, where one copy's fixed cost exceeds its transfer time
+ *     (profiles/r02_small_host.md). Needs dev_segs.
  * direct_out (nseg bytes, may be NULL) receives 1 for every layer sent that way.
  * Everything else as adt_host_to_device (which is this call with flags 0).
  */
 #define ADT_H2D_DIRECT_FULL 1u
 #define ADT_H2D_SKIP_DIRECT_NORMS 2u
+#define ADT_H2D_ZERO_COPY 4u
 int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *host_packed,
                           uint8_t *dev_packed, uint64_t packed_bytes, double *seg_sumsq, int threads,
                           uint64_t min_copy_bytes, uint32_t flags, uint8_t *direct_out, void *stream);

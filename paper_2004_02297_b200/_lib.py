@@ -26,6 +26,7 @@ TILE_WEIGHTS = 4096
 ABI_VERSION = 11
 H2D_DIRECT_FULL = 1      # adt_host_to_device_ex flags (include/adt.h)
 H2D_SKIP_DIRECT_NORMS = 2
+H2D_ZERO_COPY = 4
 MAX_SOURCES = 16
 PARTIALS_PER_TILE = 8
 

@@ -38,12 +38,14 @@
 #include <vector>
 
 #include <sched.h>
+#include <time.h>
 
 #include "adt.h"
 
 namespace {
 
-constexpr uint64_t kUnitWeights = 1u << 16;   // weights per work unit (multiple of 64)
+constexpr uint64_t kUnitWeights = 1u << 16;   // weights per work unit at most (multiple of 64)
+constexpr uint64_t kUnitMin = 1u << 12;       // ... and at least, for small sets
 constexpr uint64_t kGroup = 64;               // weights per vector iteration
 
 // ------------------------------------------------------------ scalar path
@@ -308,7 +310,27 @@ double pack_unit(const adt_segment &s, uint64_t lo, uint64_t hi, uint8_t *packed
 
 // ------------------------------------------------------------ worker pool
 // Persistent workers (affinity count - 1; the caller is the last worker).
-// One job at a time: concurrent callers queue on `submit_mu`.
+// One job at a time: concurrent callers queue on `submit_mu`. A job is
+// published as one atomic word (generation << 16 | participants), so a worker
+// decides from a single load whether and for which generation it works. After
+// a job, workers (and a caller waiting for them) spin for ADT_HOST_SPIN_US
+// before sleeping on the condition variable: a futex wake of 15 threads costs
+// tens of microseconds on the B200 host VM, more than a small layer set takes
+// to pack (profiles/r02_small_host.md).
+int spin_us() {
+    static const int v = [] {
+        const char *e = getenv("ADT_HOST_SPIN_US");
+        return e != nullptr ? atoi(e) : 200;
+    }();
+    return v;
+}
+
+inline uint64_t now_ns() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return static_cast<uint64_t>(t.tv_sec) * 1000000000ull + static_cast<uint64_t>(t.tv_nsec);
+}
+
 class Pool {
   public:
     static Pool &get() {
@@ -322,17 +344,28 @@ class Pool {
     void run(int nthreads, const std::function<void(int)> &job, const std::function<void()> &caller) {
         std::lock_guard<std::mutex> serial(submit_mu_);
         const int use = std::max(0, std::min(nthreads - 1, workers()));
+        if (use == 0) {
+            caller();
+            return;
+        }
+        job_ = &job;
+        active_.store(use, std::memory_order_relaxed);
         {
             std::lock_guard<std::mutex> g(mu_);
-            job_ = &job;
-            active_ = use;
-            want_ = use;
             ++gen_;
+            word_.store((gen_ << 16) | static_cast<uint64_t>(use), std::memory_order_release);
         }
-        cv_.notify_all();
+        if (sleepers_.load(std::memory_order_acquire) > 0) cv_.notify_all();
         caller();
-        std::unique_lock<std::mutex> g(mu_);
-        done_cv_.wait(g, [&] { return active_ == 0; });
+        const uint64_t t0 = now_ns(), budget = static_cast<uint64_t>(spin_us()) * 1000u;
+        for (unsigned k = 0; active_.load(std::memory_order_acquire) != 0; ++k) {
+            if ((k & 63) == 0 && now_ns() - t0 > budget) {
+                std::unique_lock<std::mutex> g(mu_);
+                done_cv_.wait(g, [&] { return active_.load(std::memory_order_acquire) == 0; });
+                break;
+            }
+            _mm_pause();
+        }
         job_ = nullptr;
     }
 
@@ -345,27 +378,39 @@ class Pool {
         for (auto &t : threads_) t.detach();
     }
     void loop(int idx) {
-        uint64_t seen = 0;
+        uint64_t seen = 0;                     // generation last looked at
         for (;;) {
-            const std::function<void(int)> *job = nullptr;
-            {
-                std::unique_lock<std::mutex> g(mu_);
-                cv_.wait(g, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (idx < want_) job = job_;
+            uint64_t w = word_.load(std::memory_order_acquire);
+            if ((w >> 16) == seen) {           // no new job: spin, then sleep
+                const uint64_t t0 = now_ns(), budget = static_cast<uint64_t>(spin_us()) * 1000u;
+                for (unsigned k = 0; ((w = word_.load(std::memory_order_acquire)) >> 16) == seen; ++k) {
+                    if ((k & 63) == 0 && now_ns() - t0 > budget) {
+                        std::unique_lock<std::mutex> g(mu_);
+                        sleepers_.fetch_add(1, std::memory_order_acq_rel);
+                        cv_.wait(g, [&] { return (word_.load(std::memory_order_acquire) >> 16) != seen; });
+                        sleepers_.fetch_sub(1, std::memory_order_acq_rel);
+                        w = word_.load(std::memory_order_acquire);
+                        break;
+                    }
+                    _mm_pause();
+                }
             }
-            if (job == nullptr) continue;
-            (*job)(idx);
-            std::lock_guard<std::mutex> g(mu_);
-            if (--active_ == 0) done_cv_.notify_all();
+            seen = w >> 16;
+            if (idx >= static_cast<int>(w & 0xFFFF)) continue;   // not a participant of this generation
+            (*job_)(idx);                      // job_ stays valid until every participant is done
+            if (active_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+                std::lock_guard<std::mutex> g(mu_);
+                done_cv_.notify_all();
+            }
         }
     }
     std::vector<std::thread> threads_;
     std::mutex mu_, submit_mu_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(int)> *job_ = nullptr;
-    uint64_t gen_ = 0;
-    int active_ = 0, want_ = 0;
+    uint64_t gen_ = 0;                         // guarded by mu_ (writers) / submit_mu_
+    std::atomic<uint64_t> word_{0};            // gen << 16 | participants
+    std::atomic<int> active_{0}, sleepers_{0};
 };
 
 struct Unit {
@@ -390,11 +435,32 @@ int validate_host(const adt_segment *segs, int nseg, const uint8_t *packed) {
     return ADT_OK;
 }
 
+// Weights per work unit for a set: 64K, or for a small set about 1/128 of
+// its weights (>= 4K, multiple of 64) so that its units spread over every
+// host thread (LeNet, 430K weights: 106 units instead of 10). A function of
+// the set alone, never of the thread count: the per-layer sums (summed unit
+// by unit in a fixed order) are the same on every host. ADT_HOST_UNIT pins it.
+uint64_t unit_weights(const adt_segment *segs, int nseg) {
+    static const uint64_t pinned = [] {
+        const char *e = getenv("ADT_HOST_UNIT");
+        const uint64_t v = e != nullptr ? strtoull(e, nullptr, 10) : 0;
+        return std::min(kUnitWeights, v / kGroup * kGroup);
+    }();
+    if (pinned) return pinned;
+    uint64_t total = 0;
+    for (int s = 0; s < nseg; ++s) total += segs[s].count;
+    const uint64_t u = (total / 128 + kGroup - 1) / kGroup * kGroup;
+    return std::max(kUnitMin, std::min(kUnitWeights, u));
+}
+
+void add_units(std::vector<Unit> &u, const adt_segment *segs, int s, uint64_t unit) {
+    for (uint64_t lo = 0; lo < segs[s].count; lo += unit) u.push_back({s, lo, std::min(segs[s].count, lo + unit)});
+}
+
 std::vector<Unit> make_units(const adt_segment *segs, int nseg) {
+    const uint64_t unit = unit_weights(segs, nseg);
     std::vector<Unit> u;
-    for (int s = 0; s < nseg; ++s)
-        for (uint64_t lo = 0; lo < segs[s].count; lo += kUnitWeights)
-            u.push_back({s, lo, std::min(segs[s].count, lo + kUnitWeights)});
+    for (int s = 0; s < nseg; ++s) add_units(u, segs, s, unit);
     return u;
 }
 
@@ -480,8 +546,22 @@ int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_s
     int v = validate_host(host_segs, nseg, host_packed);
     if (v != ADT_OK) return v;
     if (nseg > 0 && dev_packed == nullptr) return ADT_ERR_ARG;
-    if ((flags & ~static_cast<uint32_t>(ADT_H2D_DIRECT_FULL | ADT_H2D_SKIP_DIRECT_NORMS)) != 0) return ADT_ERR_ARG;
+    if ((flags & ~static_cast<uint32_t>(ADT_H2D_DIRECT_FULL | ADT_H2D_SKIP_DIRECT_NORMS | ADT_H2D_ZERO_COPY)) != 0)
+        return ADT_ERR_ARG;
     if ((flags & ADT_H2D_DIRECT_FULL) && dev_segs == nullptr) return ADT_ERR_ARG;   // direct copies land in the replicas
+    // ZERO_COPY: no staging copies; the unpack reads the packed stream from the
+    // page-locked staging buffer over the link (device-mapped host memory).
+    const bool zero_copy = (flags & ADT_H2D_ZERO_COPY) != 0;
+    const uint8_t *mapped = nullptr;
+    if (zero_copy) {
+        if (dev_segs == nullptr || !page_locked(host_packed, packed_bytes)) return ADT_ERR_ARG;
+        void *d = nullptr;
+        if (packed_bytes > 0 && cudaHostGetDevicePointer(&d, host_packed, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return ADT_ERR_ARG;
+        }
+        mapped = static_cast<const uint8_t *>(d);
+    }
     uint64_t end_prev = 0;                    // payloads in increasing, non-overlapping order (the DMA
     for (int i = 0; i < nseg; ++i) {          // ships the stream front to back as units complete)
         const adt_segment &h = host_segs[i];
@@ -529,7 +609,7 @@ int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_s
     // neighbours merged when only the inter-layer pad separates them
     struct Run { uint64_t a, b; };
     std::vector<Run> runs;
-    for (int i = 0; i < nseg; ++i) {
+    for (int i = 0; i < nseg && !zero_copy; ++i) {
         const adt_segment &h = host_segs[i];
         if (h.count == 0 || direct[i]) continue;
         const uint64_t a = h.offset, b = h.offset + h.count * static_cast<uint64_t>(h.round_to);
@@ -540,16 +620,13 @@ int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_s
     // same words), then the packed layers' units in stream order
     std::vector<Unit> units;
     const bool skip_direct_norms = (flags & ADT_H2D_SKIP_DIRECT_NORMS) != 0;
+    const uint64_t unit = unit_weights(host_segs, nseg);
     if (seg_sumsq != nullptr && !skip_direct_norms)
         for (int s = 0; s < nseg; ++s)
-            if (direct[s])
-                for (uint64_t lo = 0; lo < host_segs[s].count; lo += kUnitWeights)
-                    units.push_back({s, lo, std::min(host_segs[s].count, lo + kUnitWeights)});
+            if (direct[s]) add_units(units, host_segs, s, unit);
     const size_t nnorm = units.size();
     for (int s = 0; s < nseg; ++s)
-        if (!direct[s])
-            for (uint64_t lo = 0; lo < host_segs[s].count; lo += kUnitWeights)
-                units.push_back({s, lo, std::min(host_segs[s].count, lo + kUnitWeights)});
+        if (!direct[s]) add_units(units, host_segs, s, unit);
     std::vector<double> ss(units.size(), 0.0);
     // byte range of the packed stream that is final once units [0, k) are done:
     // [0, start of unit k) — nothing while the norm-only units run
@@ -570,7 +647,10 @@ int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_s
         }
     };
     uint64_t sent = 0;
-    const uint64_t batch = min_copy_bytes == 0 ? (1u << 20) : min_copy_bytes;
+    // 0 = automatic: 1 MiB copies, or for a small stream quarters of it (>= 64 KiB)
+    // so its DMA starts before the last unit is packed
+    const uint64_t batch = min_copy_bytes != 0 ? min_copy_bytes
+                                               : std::min<uint64_t>(1u << 20, std::max<uint64_t>(64u << 10, packed_bytes / 4));
     pack_units(host_segs, units, nnorm, host_packed, resolve_threads(threads), ss, [&](size_t prefix) {
         const uint64_t end = ready_bytes(prefix);
         if (err != cudaSuccess || end <= sent) return;
@@ -587,11 +667,12 @@ int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_s
     if (dev_segs == nullptr) return ADT_OK;
     bool any_direct = false;
     for (int i = 0; i < nseg; ++i) any_direct = any_direct || direct[i];
-    if (!any_direct) return adt_unpack(dev_segs, nseg, dev_packed, stream);
+    const uint8_t *src = zero_copy ? mapped : dev_packed;
+    if (!any_direct) return adt_unpack(dev_segs, nseg, src, stream);
     std::vector<adt_segment> rest(dev_segs, dev_segs + nseg);     // the direct layers are complete already
     for (int i = 0; i < nseg; ++i)
         if (direct[i]) rest[i].count = 0;
-    return adt_unpack(rest.data(), nseg, dev_packed, stream);
+    return adt_unpack(rest.data(), nseg, src, stream);
 }
 
 int adt_host_to_device_ring(const adt_segment *host_segs, const adt_segment *dev_segs, int nseg, uint8_t *ring,

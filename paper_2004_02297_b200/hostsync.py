@@ -37,6 +37,7 @@ from .layout import PackedLayout
 from .precision import FixedPrecision, PrecisionController
 from .sync import SyncResult, flat_views
 
+ZERO_COPY_BYTES = 2 << 20   # default HostWeightSync(zero_copy_bytes=): streams up to 2 MiB unpack from host memory
 HOST_ALIGN = 64        # payload offsets: full 64-B lines for the packer's non-temporal stores
 
 
@@ -66,8 +67,9 @@ class HostWeightSync:
     """
 
     def __init__(self, masters: Sequence, schedule=None, replicas: Sequence[torch.Tensor] | None = None,
-                 device: torch.device | str | None = None, threads: int = 0, min_copy_bytes: int = 1 << 20,
-                 ring_bytes: int = 0, slot_bytes: int = 384 << 10, direct_full: bool = True):
+                 device: torch.device | str | None = None, threads: int = 0, min_copy_bytes: int = 0,
+                 ring_bytes: int = 0, slot_bytes: int = 384 << 10, direct_full: bool = True,
+                 zero_copy_bytes: int = ZERO_COPY_BYTES):
         engine.require_cuda()
         self.masters = [_host_view(m, i) for i, m in enumerate(masters)]
         self.counts = [m.size for m in self.masters]
@@ -91,6 +93,11 @@ class HostWeightSync:
         self.direct_full = bool(direct_full)
         self.direct = np.zeros(max(1, L), dtype=np.uint8)   # which layers the last launch sent that way
         self.min_copy_bytes = int(min_copy_bytes)
+        # packed streams up to zero_copy_bytes skip the staging copy: the device
+        # unpack reads them from the pinned staging buffer across the link
+        # (ADT_H2D_ZERO_COPY). A copy's fixed cost (~10 us) exceeds its transfer
+        # time there (profiles/r02_small_host.md); 0 = always copy.
+        self.zero_copy_bytes = int(zero_copy_bytes)
         cap = PackedLayout.plan(self.counts, [4] * L, align=HOST_ALIGN).nbytes
         # ring_bytes = 0 (default): one pinned staging buffer as large as the
         # stream (adt_host_to_device). > 0: a small pinned ring of slot_bytes
@@ -105,6 +112,8 @@ class HostWeightSync:
         self._stage_ptr = self.staging.data_ptr() + base        # 64-B aligned stream start
         self.packed = torch.empty(max(64, cap), dtype=torch.uint8, device=self.device)
         self.sumsq = np.zeros(max(1, L), dtype=np.float64)
+        self._sumsq_ptr = self.sumsq.ctypes.data           # (ctypes attribute lookups cost ~1 us per launch)
+        self._direct_ptr = self.direct.ctypes.data
         self._dma_done = torch.cuda.Event()
         self._dma_pending = False
         # device-side norms of the direct layers (their replica equals the master)
@@ -126,6 +135,22 @@ class HostWeightSync:
         return list(self.layout.round_tos)
 
     @property
+    def zero_copy(self) -> bool:
+        """Whether the next launch's unpack reads the packed stream straight
+        from the pinned staging buffer (small streams) instead of a device copy."""
+        return self.ring_bytes == 0 and 0 < self.layout.nbytes <= self.zero_copy_bytes
+
+    def stream_bytes(self) -> np.ndarray:
+        """The packed stream the last launch's unpack read (a host copy, for
+        checks): the device buffer, or under zero copy the pinned staging
+        buffer itself. Call after the stream has passed the launch."""
+        n = self.layout.nbytes
+        if self.zero_copy:
+            base = self._stage_ptr - self.staging.data_ptr()
+            return self.staging.numpy()[base:base + n].copy()
+        return self.packed[:n].cpu().numpy()
+
+    @property
     def h2d_bytes(self) -> int:
         """Bytes one transfer moves over the link: the packed stream (payloads + < 64 B pad per layer)."""
         return self.layout.nbytes
@@ -143,7 +168,7 @@ class HostWeightSync:
         if events is not None:
             events[0].record(s)
         dev_segs = self.unpack_table.array if events is None else None
-        sums = self.sumsq.ctypes.data if fused_norm else None
+        sums = self._sumsq_ptr if fused_norm else None
         lib = _lib.load()
         if self.ring_bytes:
             _lib.check(lib.adt_host_to_device_ring(
@@ -152,10 +177,12 @@ class HostWeightSync:
         else:
             flags = (_lib.H2D_DIRECT_FULL | _lib.H2D_SKIP_DIRECT_NORMS) if (self.direct_full and dev_segs is not None) \
                 else 0
+            if dev_segs is not None and self.zero_copy:
+                flags |= _lib.H2D_ZERO_COPY
             self._dn_pending = False
             _lib.check(lib.adt_host_to_device_ex(
                 self._host_segs, dev_segs, len(self.counts), self._stage_ptr, self.packed.data_ptr(),
-                self.layout.nbytes, sums, self.threads, self.min_copy_bytes, flags, self.direct.ctypes.data,
+                self.layout.nbytes, sums, self.threads, self.min_copy_bytes, flags, self._direct_ptr,
                 int(s.cuda_stream)))
             if fused_norm and flags and self.direct.any():
                 self._direct_norms(s)

@@ -25,8 +25,8 @@ def adt():
     return adt
 
 
-@pytest.mark.parametrize("ring", [0, 48 * (384 << 10)])
-def test_replicas_and_norms_mixed_widths(adt, ring):
+@pytest.mark.parametrize("ring,zero_copy", [(0, False), (0, True), (48 * (384 << 10), False)])
+def test_replicas_and_norms_mixed_widths(adt, ring, zero_copy):
     rng = np.random.default_rng(3)
     counts = [20 * 25, 50 * 20 * 25, 4097, 0, 65536 * 3 + 11, 10 * 500, 3]
     rs = [1, 2, 3, 4, 4, 1, 3]
@@ -37,7 +37,9 @@ def test_replicas_and_norms_mixed_widths(adt, ring):
         def round_tos(self):
             return list(rs)
 
-    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32), ring_bytes=ring)
+    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32), ring_bytes=ring,
+                              zero_copy_bytes=(1 << 30) if zero_copy else 0)
+    assert sync.zero_copy == zero_copy
     for _ in range(3):                        # repeated transfers reuse the staging buffer
         for r_ in sync.replicas:
             r_.fill_(float("nan"))
@@ -46,6 +48,11 @@ def test_replicas_and_norms_mixed_widths(adt, ring):
         for i, (h, r) in enumerate(zip(hosts, rs)):
             want = h.view(np.uint32) & np.uint32(O.keep_mask(r))
             assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), i
+        if not ring:
+            stream = sync.stream_bytes()
+            for i, (h, r) in enumerate(zip(hosts, rs)):
+                lo, hi = sync.layout.span(i)
+                assert stream[lo:hi].tobytes() == O.pack_vectorized(h, r), i
     norms = sync.norms()
     for i, h in enumerate(hosts):
         if i == 4:
@@ -147,19 +154,22 @@ def test_large_set_in_many_copies(adt, ring):
         assert dev[lo:hi].tobytes() == O.pack_vectorized(h, r)
 
 
-@pytest.mark.parametrize("pinned", [False, True])
-def test_lenet_awp_walk_host_masters(adt, golden_lenet, pinned):
+@pytest.mark.parametrize("pinned,zero_copy", [(False, True), (True, True), (False, False)])
+def test_lenet_awp_walk_host_masters(adt, golden_lenet, pinned, zero_copy):
     """SURVEY §8d config 1 through the CPU-master path: the host arrays are the
     masters (updated in place), norms come from the host pass, widths / trace
     rows / payloads / replicas equal the reference run's. pinned: page-locked
     masters, so every layer AWP has widened to 32 bits goes by direct DMA with
-    its norm from the device (about half of the walk's layer-steps)."""
+    its norm from the device (about half of the walk's layer-steps). zero_copy:
+    the device unpack reads the packed stream from the pinned staging buffer
+    (the default for a stream this small) instead of a staged copy."""
     steps = int(golden_lenet["steps"])
     walk = list(O.lenet_walk(steps, seed=7))
     L = len(walk[0][1])
     cfg = adt.PrecisionConfig(threshold=-2e-3, interval=int(golden_lenet["interval"]), step_bits=8, initial_bits=8)
     masters = [_pinned_copy(w.reshape(-1)).numpy().reshape(w.shape) if pinned else w.copy() for w in walk[0][1]]
-    sync = adt.HostWeightSync(masters, adt.PrecisionController(L, cfg))
+    sync = adt.HostWeightSync(masters, adt.PrecisionController(L, cfg), zero_copy_bytes=(1 << 30) if zero_copy else 0)
+    assert sync.zero_copy == zero_copy
     direct_steps = 0
     trace = []
     for t in range(steps):
@@ -169,7 +179,7 @@ def test_lenet_awp_walk_host_masters(adt, golden_lenet, pinned):
         trace += res.trace
         assert res.round_tos == list(golden_lenet["widths"][t]), t
         torch.cuda.synchronize()
-        dev = sync.packed.cpu().numpy()
+        dev = sync.stream_bytes()
         for i in range(L):
             lo, hi = sync.layout.span(i)
             if sync.direct[i]:                 # sent as FP32 straight into the replica: no packed payload
