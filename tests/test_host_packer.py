@@ -105,3 +105,33 @@ def test_scalar_and_regular_store_paths_agree(env):
         all(np.isnan(a) == np.isnan(b) for a, b in zip(runs[0]["ss"], runs[1]["ss"]))
     if "ADT_HOST_SCALAR" in env:
         assert runs[1]["simd"] == 0
+
+
+def test_concurrent_callers_share_the_pool(hostpack):
+    """Several host threads call adt_pack_host at once (ctypes drops the GIL):
+    calls queue on the one worker pool and every result equals the
+    single-threaded one (bytes and bit-identical sums), whatever each call's
+    thread count and whether the workers were spinning or asleep."""
+    import threading
+    import time
+    rng = np.random.default_rng(12)
+    hosts = [rng.standard_normal(n, dtype=np.float32) for n in (500, 25000, 400000, 5000, 70001)]
+    rs = [1, 2, 3, 4, 1]
+    want_p, lay, want_ss = hostpack.pack_host(hosts, rs, threads=1)
+    spans = [lay.span(i) for i in range(len(hosts))]
+    bad = []
+
+    def caller(t):
+        for it in range(12):
+            p, _, ss = hostpack.pack_host(hosts, rs, threads=1 + (3 * it + t) % 8)
+            if any(not np.array_equal(p[a:b], want_p[a:b]) for a, b in spans) or not np.array_equal(ss, want_ss):
+                bad.append((t, it))
+            if it % 4 == 3:
+                time.sleep(0.002)                      # the workers fall asleep before the next call
+
+    ths = [threading.Thread(target=caller, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not bad
