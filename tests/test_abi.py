@@ -142,9 +142,14 @@ def test_host_entry_points_validate_arguments(lib):
     other = lib.segment_array([(16, 10, 0, 3)])                          # device side disagrees
     assert h.adt_host_to_device(one, other, 1, 64, 64, 1 << 20, None, 0, 0, None) == lib.ADT_ERR_ARG
     assert h.adt_host_to_device(one, one, 1, 64, 64, 8, None, 0, 0, None) == lib.ADT_ERR_ARG   # stream too short
-    # _ex: unknown flag bits, and DIRECT_FULL without device segments, are refused before any work
-    assert h.adt_host_to_device_ex(one, one, 1, 64, 64, 1 << 20, None, 0, 0, 4, None, None) == lib.ADT_ERR_ARG
+    # _ex: unknown flag bits, DIRECT_FULL or ZERO_COPY without device segments, and ZERO_COPY from
+    # staging that is not page-locked, are refused before any work
+    assert h.adt_host_to_device_ex(one, one, 1, 64, 64, 1 << 20, None, 0, 0, 8, None, None) == lib.ADT_ERR_ARG
     assert h.adt_host_to_device_ex(one, None, 1, 64, 64, 1 << 20, None, 0, 0, lib.H2D_DIRECT_FULL, None,
+                                   None) == lib.ADT_ERR_ARG
+    assert h.adt_host_to_device_ex(one, None, 1, 64, 64, 1 << 20, None, 0, 0, lib.H2D_ZERO_COPY, None,
+                                   None) == lib.ADT_ERR_ARG
+    assert h.adt_host_to_device_ex(one, one, 1, 64, 64, 1 << 20, None, 0, 0, lib.H2D_ZERO_COPY, None,
                                    None) == lib.ADT_ERR_ARG
     assert h.adt_sumsq_f64(None, 10, 16, 16, None) == lib.ADT_ERR_ARG
     assert h.adt_sumsq_f64(12, 10, 16, 16, None) == lib.ADT_ERR_ALIGN
