@@ -8,6 +8,8 @@ by __graft_entry__.install_reference() from /root/reference/pkg/tests;
 git-ignored like the reference install, shipped with the snapshot).
 
     python tests/refsuite/run.py <tests dir> test_codec.py test_precision.py [pytest args]
+    python tests/refsuite/run.py --plug <tests dir> test_training.py test_acceptance.py ...
+        (the whole reference package with only codec + precision replaced)
 """
 
 import os
@@ -28,11 +30,35 @@ def install_shim():
     sys.modules["weightpack.precision"] = precision
 
 
+def install_plugged(ref_root):
+    """The UNMODIFIED reference package (baseline/_ref/weightpack: training
+    loop, net, transfer ledger, config, CLI, report) with only its hot path
+    replaced by this package's codec and precision modules
+    (tests/refsuite/plug/weightpack). Set up for this process and, through
+    PYTHONPATH, for the suite's `python -m weightpack` children."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    os.environ["ADT_REFSUITE_REF"] = os.path.join(ref_root, "weightpack")
+    front = [os.path.join(here, "plug"), os.path.join(here, "stubs"), ROOT]     # stubs: matplotlib (absent)
+    os.environ["PYTHONPATH"] = os.pathsep.join(front + [p for p in os.environ.get("PYTHONPATH", "").split(os.pathsep) if p])
+    sys.path[:0] = front
+    from paper_2004_02297_b200 import codec, precision
+    import weightpack
+    from weightpack import training
+    assert weightpack.codec is codec and weightpack.precision is precision
+    assert training.pack_vectorized is codec.pack_vectorized and training.l2_norm is precision.l2_norm
+    assert training.__file__.startswith(os.environ["ADT_REFSUITE_REF"])
+
+
 def main(argv):
+    plug = "--plug" in argv
+    argv = [a for a in argv if a != "--plug"]
     tests_dir, rest = argv[0], argv[1:]
     files = [a for a in rest if a.endswith(".py")]
     extra = [a for a in rest if not a.endswith(".py")]
-    install_shim()
+    if plug:
+        install_plugged(os.path.dirname(os.path.abspath(tests_dir)))
+    else:
+        install_shim()
     sys.path.insert(0, tests_dir)            # oracle_precision, conftest helpers
     import pytest
     rc = pytest.main([os.path.join(tests_dir, f) for f in files] +
