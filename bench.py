@@ -259,6 +259,10 @@ def reference_kind(wp):
             "(baseline/_ref missing)")
 
 
+THREADS_NOTE = ("cores = the host threads the reference path may use: its NumPy codec calls "
+                "(pack_vectorized, unpack) run on one thread, OpenBLAS ddot (l2_norm) on up to all of them")
+
+
 def reference_threads():
     """Host threads the reference path may use: NumPy's codec ops are
     single-threaded; OpenBLAS's ddot (l2_norm) uses up to the affinity count."""
@@ -282,7 +286,7 @@ def run_cpu_baseline(counts, rs, budget_s=10.0, min_reps=2):
     mean = sum(times) / len(times)
     return {"value": byts / mean / 1e9, "unit": UNIT, "cores": reference_threads(), "kind": kind,
             "sample": f"{sample}; {what}; mean of {len(times)} passes ({sum(times):.1f} s)",
-            "seconds_per_pass": mean, "host_cpus": os.cpu_count()}
+            "threads_note": THREADS_NOTE, "seconds_per_pass": mean, "host_cpus": os.cpu_count()}
 
 
 def bench_config(args, counts, bits, rs, world=1, transport=None):
@@ -326,7 +330,7 @@ def main_reference(args):
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": reference_threads(), "kind": kind,
                          "sample": f"{sample}; {what}; each step one pass" + (f" with {world} worker unpacks" if world > 1 else ""),
-                         "host_cpus": os.cpu_count()},
+                         "threads_note": THREADS_NOTE, "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
