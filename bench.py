@@ -1106,10 +1106,15 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
     dflat = torch.empty(flat.numel(), dtype=torch.float32, device=dev)
     tail_raw = torch.empty(4, dtype=torch.float32, pin_memory=True)
 
-    def raw_one():
+    flat.numpy()[-4:] = host[-1][-4:]
+    want_raw = host[-1][-4:].view(np.uint32)
+
+    def raw_one():                                   # same read-back and check as one()
         dflat.copy_(flat, non_blocking=True)
         tail_raw.copy_(dflat[-4:], non_blocking=True)
         stream.synchronize()
+        if not np.array_equal(tail_raw.numpy().view(np.uint32), want_raw):
+            raise AssertionError("raw FP32 e2e: read-back differs")
 
     for _ in range(3):
         raw_one()
