@@ -122,13 +122,22 @@ adt_sgd_pack_kernel(const __grid_constant__ SgdTable<MAXSEG> T) {
         // contributions, two k-steps for a few more, one beyond (NC loads per
         // k-step are already in flight), within the register budget.
         constexpr int kH = sgd_hoist(NC);
+        // many contributions: address each load from the table's source base
+        // (a constant-bank operand) + one shared offset instead of keeping NC
+        // 64-bit pointers live (they pushed NC >= 14 past 128 registers: spills)
+        constexpr bool kLeanPtrs = NC > ADT_SGD_HOIST2_MAX_NC;
+        const uintptr_t goff = kLeanPtrs ? T.grad[s] + e0 * 4 : 0;
 #pragma unroll
         for (int kb = 0; kb < kVec; kb += kH) {
             uint4 g[kH][NG];
+            uintptr_t go = goff;
+            if (kLeanPtrs) asm volatile("" : "+l"(go));   // opaque per k-step: the NC addresses are not kept live
 #pragma unroll
             for (int h = 0; h < kH; ++h)
 #pragma unroll
-                for (int c = 0; c < NG; ++c) g[h][c] = __ldcs(gp[c] + g0 + 32 * (kb + h));
+                for (int c = 0; c < NG; ++c)
+                    g[h][c] = __ldcs((kLeanPtrs ? reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(T.srcs[c]) + go)
+                                                : gp[c]) + g0 + 32 * (kb + h));
 #pragma unroll
             for (int h = 0; h < kH; ++h) {
                 const int k = kb + h;

@@ -4,7 +4,7 @@
 OUT=${1:-gpurun_out/reduce_sweep}; mkdir -p $OUT
 echo "| contributions | fused µs | unfused µs | fused GB/s | % of copy peak | speedup |"
 echo "|---|---|---|---|---|---|"
-for k in 1 2 3 4 5 6 7 8 12 16; do
+for k in ${KS:-1 2 3 4 5 6 7 8 9 10 11 12 13 14 15 16}; do
   timeout 200 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-h2d --no-sgd --no-awp-step --quiet-extra --reduce-contribs $k > $OUT/red_$k.json 2>/dev/null
   python - $OUT/red_$k.json <<'PY'
 import json, sys
