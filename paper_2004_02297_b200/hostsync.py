@@ -193,6 +193,38 @@ class HostWeightSync:
         self._dma_done.record(s)
         self._dma_pending = True
 
+    def tune_threads(self, candidates=None, reps: int = 3) -> dict:
+        """Pick the packer thread count for this set on this host (setup-time,
+        like cudnn's benchmark mode): time whole transfers (launch -> stream
+        sync, best of `reps`) at a few thread counts and keep the fastest.
+        More threads are not always faster: the packers and the DMA share host
+        DRAM, and once the pack runs ahead of the link extra threads only take
+        bandwidth from the DMA (AlexNet mixed widths: 3.30 ms at 6 threads vs
+        3.47 ms at 16; VGG-16 r = 1 needs all 16, profiles/r02_small_host.md §3).
+        Replicas are rewritten with the same values; the masters are only read.
+        Returns {threads: seconds}."""
+        import time
+        total = host_threads()
+        if candidates is None:
+            candidates = sorted({total, max(1, (3 * total) // 4), max(1, total // 2), max(1, (3 * total) // 8)},
+                                reverse=True)
+        s = torch.cuda.current_stream(self.device)
+        keep = self.threads
+        timings = {}
+        for t in candidates:
+            self.threads = int(t)
+            self.launch(fused_norm=True)                  # warm
+            s.synchronize()
+            best = float("inf")
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                self.launch(fused_norm=True)
+                s.synchronize()
+                best = min(best, time.perf_counter() - t0)
+            timings[int(t)] = best
+        self.threads = min(timings, key=timings.get) if timings else keep
+        return timings
+
     def _direct_norms(self, s) -> None:
         """The direct layers' sums of squares, on the device from their replicas
         (bit-equal to the masters at full width): adt_sumsq on `s` behind the

@@ -205,3 +205,33 @@ def test_rejects_device_and_strided_masters(adt):
         adt.HostWeightSync([torch.zeros(8, device="cuda")])
     with pytest.raises(ValueError):
         adt.HostWeightSync([np.zeros((4, 6), np.float32).T])
+
+
+def test_tune_threads_keeps_results(adt):
+    """tune_threads() only picks the packer thread count: after it, transfers
+    still produce the reference's replicas and bit-identical host norms (the
+    sums never depend on the thread count)."""
+    from paper_2004_02297_b200.hostsync import host_threads
+    rng = np.random.default_rng(21)
+    counts = [300000, 5000, 65536 * 2 + 3]
+    rs = [1, 3, 2]
+    hosts = [rng.standard_normal(n, dtype=np.float32) for n in counts]
+
+    class Fixed(adt.FixedPrecision):
+        def round_tos(self):
+            return list(rs)
+
+    sync = adt.HostWeightSync(hosts, Fixed(len(counts), 32))
+    sync.launch(fused_norm=True)
+    torch.cuda.synchronize()
+    before = sync.norms()
+    timings = sync.tune_threads(reps=1)
+    assert sync.threads in timings and all(1 <= t <= host_threads() for t in timings)
+    for r_ in sync.replicas:
+        r_.fill_(float("nan"))
+    sync.launch(fused_norm=True)
+    torch.cuda.synchronize()
+    assert sync.norms() == before
+    for i, (h, r) in enumerate(zip(hosts, rs)):
+        want = h.view(np.uint32) & np.uint32(O.keep_mask(r))
+        assert np.array_equal(sync.replicas[i].cpu().numpy().view(np.uint32), want), i
