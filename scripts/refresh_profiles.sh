@@ -39,3 +39,6 @@ for t in memcheck racecheck synccheck; do
   have $O/sanitize_$t.log && tail -n 3 $O/sanitize_$t.log > profiles/${P}_sanitize_$t.txt
 done
 python scripts/results_table.py $O > profiles/${P}_results_table.md || true
+have $O/refsuite_plug.txt && { echo "# the reference's whole test suite on the unmodified reference package with codec + precision replaced by this repo (tests/refsuite/run.py --plug)"; cat $O/refsuite_plug.txt; } > profiles/${P}_reference_suite_plugged.txt
+have $O/small_host_breakdown.txt && cp $O/small_host_breakdown.txt profiles/${P}_small_host_breakdown.txt
+true

@@ -104,8 +104,9 @@ def main():
     for _ in range(3):
         small.launch(fused_norm=True)
     hosts_nz = [h for h in hosts if h.size]
-    for ring in (0, 24 * (320 << 10)):
-        hs = adt.HostWeightSync([h.copy() for h in hosts_nz], ring_bytes=ring, slot_bytes=320 << 10)
+    for ring, zc in ((0, 1 << 30), (0, 0), (24 * (320 << 10), 0)):    # zero-copy, staged, ring
+        hs = adt.HostWeightSync([h.copy() for h in hosts_nz], ring_bytes=ring, slot_bytes=320 << 10,
+                                zero_copy_bytes=zc)
         hs.launch(fused_norm=True)
     torch.cuda.synchronize()
     print("sanitize smoke ok")
