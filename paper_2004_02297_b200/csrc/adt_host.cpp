@@ -15,9 +15,10 @@
 //     written with non-temporal stores when the destination is 64-B aligned
 //     (no read-for-ownership of the pinned staging lines); the float64 sum of
 //     squares rides along (VCVTPS2PD + VFMADD, four accumulators);
-//   * work units of 64K weights (fixed: results do not depend on the thread
-//     count), claimed in order from an atomic counter by a persistent worker
-//     pool plus the calling thread;
+//   * work units of 64K weights (small sets: ~1/128 of the set; a function of
+//     the set, so results never depend on the thread count), claimed in order
+//     from an atomic counter by a persistent worker pool (spin, then sleep)
+//     plus the calling thread;
 //   * adt_host_to_device: the calling thread also issues cudaMemcpyAsync for
 //     every run of finished units (>= min batch), so the DMA of unit k overlaps
 //     the packing of unit k+16.., then queues the device unpack (adt_unpack).
