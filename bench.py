@@ -1074,11 +1074,11 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
 
     def measure(direct_full):
         sync = adt.HostWeightSync(pinned, Fixed(len(host), 32), device=dev, direct_full=direct_full)
-        if direct_full:                              # setup (untimed): packer threads for this set on this host
-            tuned["timings_ms"] = {t: v * 1e3 for t, v in sync.tune_threads().items()}
-            tuned["threads"] = sync.threads
+        if direct_full:                              # setup (untimed): packer threads + copy batch for this set/host
+            tuned["timings_ms"] = {k: v * 1e3 for k, v in sync.tune().items()}
+            tuned["threads"], tuned["batch"] = sync.threads, sync.min_copy_bytes
         else:
-            sync.threads = tuned.get("threads", 0)
+            sync.threads, sync.min_copy_bytes = tuned.get("threads", 0), tuned.get("batch", 0)
         # the step's result lives on the GPU (the replicas): each step reads back the
         # last 4 words of the last replica (16 B D2H, which also completes the step)
         # and checks them against the host masters truncated to their width
@@ -1135,11 +1135,12 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
     byts = 2 * sum((4 + r) * h.size for h, r in zip(host, rs))
     return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16,
             "ms_per_step": dt * 1e3, "steps": n_steps, "host_threads": tuned.get("threads") or host_threads(),
-            "host_threads_available": host_threads(), "thread_tuning_ms": tuned.get("timings_ms"),
+            "host_threads_available": host_threads(), "copy_batch_bytes": tuned.get("batch"),
+            "tuning_ms": tuned.get("timings_ms"),
             "raw_fp32_bytes": 4 * n, "raw_fp32_wall_ms_per_step": dt_raw * 1e3, "vs_raw_fp32": dt_raw / dt,
             "direct_full_layers": ndirect, "all_packed_ms_per_step": dt_packed * 1e3,
-            "note": "HostWeightSync: pinned host FP32 masters -> adt_pack_host (host_threads cores, picked at setup by "
-                    "HostWeightSync.tune_threads; norms fused) -> "
+            "note": "HostWeightSync: pinned host FP32 masters -> adt_pack_host (host_threads cores and the copy batch "
+                    "picked at setup by HostWeightSync.tune; norms fused) -> "
                     "packed H2D overlapped with the packing -> adt_unpack; full-width layers DMA'd straight from "
                     "the masters (direct_full); 16 B read-back check; wall clock; the norms come from the host pass"}
 

@@ -469,7 +469,8 @@ std::vector<Unit> make_units(const adt_segment *segs, int nseg) {
 // by the caller thread between its own units with the count of leading units
 // that are complete (for the DMA pipeline). Per-unit sums go to unit_ss.
 void pack_units(const adt_segment *segs, const std::vector<Unit> &units, size_t nnorm, uint8_t *packed, int threads,
-                std::vector<double> &unit_ss, const std::function<void(size_t)> &on_progress) {
+                std::vector<double> &unit_ss, const std::function<void(size_t)> &on_progress,
+                bool caller_packs = true) {
     const size_t nu = units.size();
     std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[nu == 0 ? 1 : nu]);
     for (size_t i = 0; i < nu; ++i) done[i].store(0, std::memory_order_relaxed);
@@ -488,7 +489,7 @@ void pack_units(const adt_segment *segs, const std::vector<Unit> &units, size_t 
         on_progress(prefix);
     };
     const std::function<void()> caller = [&] {
-        for (size_t k; (k = next.fetch_add(1, std::memory_order_relaxed)) < nu;) {
+        for (size_t k; caller_packs && (k = next.fetch_add(1, std::memory_order_relaxed)) < nu;) {
             work_one(k);
             advance();
         }
@@ -497,8 +498,18 @@ void pack_units(const adt_segment *segs, const std::vector<Unit> &units, size_t 
             if (prefix < nu) _mm_pause();
         }
     };
-    Pool::get().run(threads, job, caller);
+    // caller_packs = false: `threads` pool workers pack, the caller only follows
+    // the completed prefix (issuing the DMA of each finished run at once)
+    Pool::get().run(caller_packs ? threads : threads + 1, job, caller);
     on_progress(nu);
+}
+
+bool caller_packs_h2d() {            // A/B: ADT_H2D_CALLER_PACKS=0 -> the calling thread only issues copies
+    static const bool v = [] {
+        const char *e = getenv("ADT_H2D_CALLER_PACKS");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    return v;
 }
 
 void finish_sums(const std::vector<Unit> &units, const std::vector<double> &unit_ss, int nseg, double *seg_sumsq) {
@@ -658,7 +669,7 @@ int adt_host_to_device_ex(const adt_segment *host_segs, const adt_segment *dev_s
         if (end - sent < batch && prefix < units.size()) return;
         ship(sent, end);
         sent = end;
-    });
+    }, caller_packs_h2d());
     if (direct_last) ship_direct();
     finish_sums(units, ss, nseg, seg_sumsq);
     if (seg_sumsq != nullptr && skip_direct_norms)

@@ -193,37 +193,49 @@ class HostWeightSync:
         self._dma_done.record(s)
         self._dma_pending = True
 
-    def tune_threads(self, candidates=None, reps: int = 3) -> dict:
-        """Pick the packer thread count for this set on this host (setup-time,
-        like cudnn's benchmark mode): time whole transfers (launch -> stream
-        sync, best of `reps`) at a few thread counts and keep the fastest.
-        More threads are not always faster: the packers and the DMA share host
-        DRAM, and once the pack runs ahead of the link extra threads only take
-        bandwidth from the DMA (AlexNet mixed widths: 3.30 ms at 6 threads vs
-        3.47 ms at 16; VGG-16 r = 1 needs all 16, profiles/r02_small_host.md §3).
+    def tune(self, threads=None, batches=None, reps: int = 3) -> dict:
+        """Pick the packer thread count and the copy batch size for this set on
+        this host (setup-time, like cudnn's benchmark mode): time whole
+        transfers (launch -> stream sync, best of `reps`) over a small grid and
+        keep the fastest. More threads are not always faster: the packers and
+        the DMA share host DRAM, and once the pack runs ahead of the link extra
+        threads only take bandwidth from the DMA; larger copy batches cost the
+        calling thread (which also packs) fewer cudaMemcpyAsync calls (AlexNet
+        mixed widths: 3.3 ms at 16 threads / 1 MiB, 3.1-3.2 ms at 6-8 threads /
+        4-8 MiB; VGG-16 r = 1 needs all 16 threads; profiles/r02_small_host.md).
         Replicas are rewritten with the same values; the masters are only read.
-        Returns {threads: seconds}."""
+        Returns {"<threads>x<batch KiB>": seconds}."""
         import time
         total = host_threads()
-        if candidates is None:
-            candidates = sorted({total, max(1, (3 * total) // 4), max(1, total // 2), max(1, (3 * total) // 8)},
-                                reverse=True)
+        if threads is None:
+            threads = sorted({total, max(1, (3 * total) // 4), max(1, total // 2), max(1, (3 * total) // 8)},
+                             reverse=True)
+        if batches is None:
+            batches = [b for b in (1 << 20, 4 << 20, 8 << 20) if 2 * b <= self.layout.nbytes] or [0]
         s = torch.cuda.current_stream(self.device)
-        keep = self.threads
-        timings = {}
-        for t in candidates:
-            self.threads = int(t)
-            self.launch(fused_norm=True)                  # warm
-            s.synchronize()
-            best = float("inf")
-            for _ in range(reps):
-                t0 = time.perf_counter()
-                self.launch(fused_norm=True)
+        keep = (self.threads, self.min_copy_bytes)
+        timings, best = {}, None
+        for b in batches:
+            for t in threads:
+                self.threads, self.min_copy_bytes = int(t), int(b)
+                self.launch(fused_norm=True)              # warm
                 s.synchronize()
-                best = min(best, time.perf_counter() - t0)
-            timings[int(t)] = best
-        self.threads = min(timings, key=timings.get) if timings else keep
+                dt = float("inf")
+                for _ in range(reps):
+                    t0 = time.perf_counter()
+                    self.launch(fused_norm=True)
+                    s.synchronize()
+                    dt = min(dt, time.perf_counter() - t0)
+                timings[f"{int(t)}x{int(b) >> 10}K"] = dt
+                if best is None or dt < best[0]:
+                    best = (dt, int(t), int(b))
+        self.threads, self.min_copy_bytes = (best[1], best[2]) if best else keep
         return timings
+
+    def tune_threads(self, candidates=None, reps: int = 3) -> dict:
+        """tune() over thread counts only (copy batch unchanged); {threads: seconds}."""
+        t = self.tune(threads=candidates, batches=[self.min_copy_bytes], reps=reps)
+        return {int(k.split("x")[0]): v for k, v in t.items()}
 
     def _direct_norms(self, s) -> None:
         """The direct layers' sums of squares, on the device from their replicas

@@ -207,10 +207,10 @@ def test_rejects_device_and_strided_masters(adt):
         adt.HostWeightSync([np.zeros((4, 6), np.float32).T])
 
 
-def test_tune_threads_keeps_results(adt):
-    """tune_threads() only picks the packer thread count: after it, transfers
-    still produce the reference's replicas and bit-identical host norms (the
-    sums never depend on the thread count)."""
+def test_tune_keeps_results(adt):
+    """tune() / tune_threads() only pick the packer thread count and the copy
+    batch: after them, transfers still produce the reference's replicas and
+    bit-identical host norms (the sums never depend on the thread count)."""
     from paper_2004_02297_b200.hostsync import host_threads
     rng = np.random.default_rng(21)
     counts = [300000, 5000, 65536 * 2 + 3]
@@ -225,6 +225,8 @@ def test_tune_threads_keeps_results(adt):
     sync.launch(fused_norm=True)
     torch.cuda.synchronize()
     before = sync.norms()
+    grid = sync.tune(batches=[0, 256 << 10], reps=1)
+    assert f"{sync.threads}x{sync.min_copy_bytes >> 10}K" in grid and len(grid) >= 2
     timings = sync.tune_threads(reps=1)
     assert sync.threads in timings and all(1 <= t <= host_threads() for t in timings)
     for r_ in sync.replicas:
