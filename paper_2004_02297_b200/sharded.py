@@ -236,7 +236,7 @@ class ShardedWeightSync:
 
     def __init__(self, masters: Sequence[torch.Tensor], schedule=None, replicas=None, group=None,
                  transport: str = "auto", awp_on_device: bool = False, trace_ring: int = 256,
-                 nccl_chunks: int = 4, barrier_timeout_s: float = 30.0):
+                 nccl_chunks: int = 4, barrier_timeout_s: float = 30.0, collectives_at_world1: bool = False):
         """awp_on_device (p2p transport): every rank runs the AWP decision on
         its GPU from the gathered per-piece sums (identical inputs, so
         identical decisions), pieces keep capacity offsets in the send
@@ -252,7 +252,13 @@ class ShardedWeightSync:
         for the other ranks. On timeout every kernel behind it that reads peer
         memory skips its work (abort guard) and the next call on this object
         raises PeerTimeout: each call first waits for the previous step to
-        finish on the device, so the failure surfaces within one step."""
+        finish on the device, so the failure surfaces within one step.
+
+        collectives_at_world1 (nccl transport, tests): with a single rank, still
+        run the chunked all-gather and the gradient all_to_all through the
+        process group instead of short-cutting them (a one-rank NCCL group
+        exercises the real NCCL calls, stream waits and chunk bookkeeping on a
+        one-GPU box, where NCCL refuses two ranks on one device)."""
         import torch.distributed as dist
         engine.require_cuda()
         if transport not in ("nccl", "p2p", "auto"):
@@ -261,6 +267,7 @@ class ShardedWeightSync:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._collect = self.world > 1 or bool(collectives_at_world1)
         self.transport = peer_transport(dist, group) if transport == "auto" else transport
         from .sync import flat_views
         self.masters = flat_views(masters, "master")
@@ -460,7 +467,7 @@ class ShardedWeightSync:
         self._graphs = None
         self.unpack_table = engine.SegmentTable(outs, self.unpack_layout,
                                                 sources=srcs if self.transport == "p2p" else None)
-        if self.transport == "nccl" and self.world > 1:
+        if self.transport == "nccl" and self._collect:
             self._chunked = ChunkedGather.cut(self.plan, self.nccl_chunks)
             self._chunk_tables = []
             for segs in self._chunked.segments:
@@ -482,8 +489,8 @@ class ShardedWeightSync:
         self.send = [torch.zeros(cap, dtype=torch.uint8, device=self.device) for _ in range(nslots)]
         if self.transport == "nccl":
             # one rank: unpack straight from the send buffer (no gather, no copy)
-            self.recv = self.send[0] if self.world == 1 else torch.zeros(cap * self.world, dtype=torch.uint8,
-                                                                          device=self.device)
+            self.recv = self.send[0] if not self._collect else torch.zeros(cap * self.world, dtype=torch.uint8,
+                                                                            device=self.device)
             return
         handles = [engine.ipc_handle(b) for b in self.send]
         everyone = [None] * self.world
@@ -621,7 +628,7 @@ class ShardedWeightSync:
         gather completes: the unpack of chunk c overlaps the gather of c+1.
         mid_event (if given) is recorded once the gathers are queued."""
         stream = torch.cuda.current_stream()
-        if self.world == 1:                      # recv is the send buffer
+        if not self._collect:                    # one rank: recv is the send buffer
             if mid_event is not None:
                 mid_event.record(stream)
             engine.unpack(self.unpack_table, self.recv)
@@ -683,7 +690,7 @@ class ShardedWeightSync:
         self.check_barrier()
         S, base, m = self.plan.send_bytes, self.plan.payload_cap, self.plan.max_pieces
         if self.transport == "nccl":
-            g = (self._chunked.tails(self.recv, self.plan) if self.world > 1
+            g = (self._chunked.tails(self.recv, self.plan) if self._collect
                  else self.recv[:S].view(1, S)[:, base:base + 8 * m]).contiguous()
         else:
             g = self.tails[:self.world * 8 * m].view(self.world, 8 * m)
@@ -735,7 +742,7 @@ class ShardedWeightSync:
         mine = b1 - b0
         if self._grecv is None or self._grecv.numel() < max(4, mine * self.world):
             self._grecv = torch.empty(max(4, mine * self.world), dtype=torch.float32, device=self.device)
-        if self.world > 1:
+        if self._collect:
             splits = [e - b for b, e in self.grad_ranges]
             self.dist.all_to_all_single(self._grecv[:mine * self.world], bucket.flat[:sum(splits)],
                                         output_split_sizes=[mine] * self.world, input_split_sizes=splits,

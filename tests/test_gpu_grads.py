@@ -185,7 +185,12 @@ def _rank_main(rank, world, port, q, transport="p2p"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
         torch.cuda.set_device(0)
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+        extra = {}
+        if transport == "nccl-real":             # one rank on a real NCCL communicator, collectives kept
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+            transport, extra = "nccl", dict(collectives_at_world1=True, nccl_chunks=3)
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_2004_02297_b200 as adt
         from paper_2004_02297_b200.grads import GradBucket
         from paper_2004_02297_b200.sharded import ShardedWeightSync
@@ -201,7 +206,8 @@ def _rank_main(rank, world, port, q, transport="p2p"):
         masters = [torch.from_numpy(w.copy()).cuda() for w in w_ref]
         kw = dict(threshold=-2e-3, interval=2, step_bits=8, initial_bits=8)
         octl = O.OracleController(L, **kw)
-        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport=transport)
+        sync = ShardedWeightSync(masters, adt.PrecisionController(L, adt.PrecisionConfig(**kw)), transport=transport,
+                                 **extra)
         bucket = GradBucket(counts)
         ok, notes, seen = True, [], []
         for b in range(8):
@@ -237,10 +243,13 @@ def _rank_main(rank, world, port, q, transport="p2p"):
 
 
 @pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (8, "p2p"), (2, "nccl"), (3, "nccl"),
-                                             (3, "p2p-tiny"), (3, "nccl-tiny")])
+                                             (3, "p2p-tiny"), (3, "nccl-tiny"), (1, "nccl-real")])
 def test_sharded_update_processes_sharing_one_gpu(world, transport):
     """transport="nccl": the all_to_all gradient exchange + all-gather path,
-    run over gloo with CUDA tensors (NCCL refuses two ranks on one device)."""
+    run over gloo with CUDA tensors (NCCL refuses two ranks on one device).
+    "nccl-real": the same path on a real one-rank NCCL communicator
+    (collectives_at_world1: all_to_all_single and the chunked
+    all_gather_into_tensor go through NCCL, its streams and work.wait())."""
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
