@@ -162,9 +162,35 @@ def _pack_device(flat: torch.Tensor, r: int) -> torch.Tensor:
 
 
 # -------------------------------------------------------------- per layer
+def _host_words(weights) -> np.ndarray | None:
+    """codec.py:110-113 for a host input: the flat float32 words, or None for
+    a CUDA tensor."""
+    if isinstance(weights, torch.Tensor):
+        if weights.is_cuda:
+            return None
+        weights = weights.detach().numpy()
+    return np.ascontiguousarray(weights, dtype=np.float32).reshape(-1)
+
+
+def _pack_host_small(host: np.ndarray, r: int) -> PackedBlock:
+    """A small host array (< hostio.SMALL bytes): one H2D, the pack kernel and
+    one D2H queued back to back, one stream sync (hostio.small_call)."""
+    n = host.size
+    layout = PackedLayout.plan([n], [r])
+
+    def fn(d_in, d_out):
+        engine.pack(engine.SegmentTable([d_in[:4 * n].view(torch.float32)], layout), d_out)
+
+    return PackedBlock(r, n, hostio.small_call(host, n * r, fn).tobytes())
+
+
 def pack(weights, round_to: int) -> PackedBlock:
     """codec.py:116-130 (scalar reference) — here one multi-tensor kernel launch."""
     r = check_round_to(round_to)
+    engine.require_cuda()
+    host = _host_words(weights)
+    if host is not None and 0 < host.nbytes < hostio.SMALL:
+        return _pack_host_small(host, r)
     flat, on_dev = _device_words(weights)
     payload = _pack_device(flat, r)
     if on_dev:
@@ -199,9 +225,15 @@ def unpack(block: PackedBlock):
         raise MalformedBlock(f"payload holds {size} bytes, expected {n * r}")
     engine.require_cuda()
     layout = PackedLayout.plan([n], [r])
-    out = torch.empty(n, dtype=torch.float32, device="cuda")
     if n == 0:
-        return out if block.on_device else np.zeros(0, dtype=np.float32)
+        return torch.empty(0, dtype=torch.float32, device="cuda") if block.on_device else np.zeros(0, dtype=np.float32)
+    if not block.on_device and 4 * n < hostio.SMALL:
+        def fn(d_in, d_out):     # one H2D of the payload, the unpack, one D2H of the words, one sync
+            engine.unpack(engine.SegmentTable([d_out[:4 * n].view(torch.float32)], layout), d_in)
+
+        words = hostio.small_call(np.frombuffer(block.payload, dtype=np.uint8), 4 * n, fn)
+        return words.view(np.float32).copy()            # a fresh writable array (codec.py:186)
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
     if block.on_device:
         src = block.payload
         if src.data_ptr() % 16:

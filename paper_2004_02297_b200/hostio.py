@@ -88,6 +88,57 @@ class _Stage:
             _staging[self.idx].append(self.bufs)
 
 
+class _SmallStage:
+    """Per (thread, device) pinned + device scratch for one small call (< SMALL
+    bytes each way): the host bytes are copied into pinned memory, the H2D,
+    the kernels and the D2H are queued back to back on the current stream,
+    and ONE stream sync ends the call — instead of a synchronous pageable
+    H2D, the launch, and a second synchronous pageable D2H."""
+
+    _local = threading.local()
+
+    def __init__(self, device: torch.device):
+        self.h_in = torch.empty(SMALL, dtype=torch.uint8, pin_memory=True)
+        self.h_out = torch.empty(SMALL, dtype=torch.uint8, pin_memory=True)
+        self.d_in = torch.empty(SMALL, dtype=torch.uint8, device=device)
+        self.d_out = torch.empty(SMALL, dtype=torch.uint8, device=device)
+        self.h_in_np, self.h_out_np = self.h_in.numpy(), self.h_out.numpy()
+
+    @classmethod
+    def get(cls, device: torch.device) -> "_SmallStage":
+        stages = getattr(cls._local, "stages", None)
+        if stages is None:
+            stages = cls._local.stages = {}
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        st = stages.get(idx)
+        if st is None:
+            st = stages[idx] = _SmallStage(torch.device("cuda", idx))
+        return st
+
+
+def small_call(host_in: np.ndarray, out_nbytes: int, fn, device: torch.device | str = "cuda") -> np.ndarray:
+    """One small host -> device -> host call: host_in (contiguous, < SMALL
+    bytes) lands in a device uint8 buffer `d_in`, fn(d_in, d_out) queues the
+    device work on the current stream writing d_out[:out_nbytes] (< SMALL),
+    and the result comes back as a view of a reused pinned buffer — valid
+    until this thread's next small call (callers copy it out)."""
+    dev = torch.device(device)
+    src = np.ascontiguousarray(host_in).reshape(-1).view(np.uint8)
+    n = src.size
+    if n > SMALL or out_nbytes > SMALL:
+        raise ValueError("small_call: more than SMALL bytes")
+    st = _SmallStage.get(dev)
+    stream = torch.cuda.current_stream(st.d_in.device)
+    st.h_in_np[:n] = src
+    if n:
+        st.d_in[:n].copy_(st.h_in[:n], non_blocking=True)
+    fn(st.d_in, st.d_out)
+    if out_nbytes:
+        st.h_out[:out_nbytes].copy_(st.d_out[:out_nbytes], non_blocking=True)
+    stream.synchronize()
+    return st.h_out_np[:out_nbytes]
+
+
 def _parallel_memmove(dst: int, src: int, nbytes: int) -> None:
     n = max(1, min(THREADS, nbytes >> 22))     # >= 4 MiB per thread
     step = -(-nbytes // n)
