@@ -1102,6 +1102,41 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
         dt = (time.perf_counter() - t0) / n_steps
         ndirect = int(sync.direct[:len(host)].sum())
         h2d = sync.h2d_bytes
+        if direct_full:
+            # the pipeline's two legs alone (best of 5, wall clock): the host pass (adt_pack_host
+            # of the layers the packer handles, the tuned thread count) and the DMA of the link
+            # bytes (the staging stream, direct layers' spans included); the step cannot beat
+            # the slower one, and both share host DRAM
+            from paper_2004_02297_b200 import _lib
+            lib = _lib.load()
+            L = len(host)
+            segs = _lib.segment_array([(sync._host_segs[i].weights, 0 if sync.direct[i] else sync._host_segs[i].count,
+                                        sync._host_segs[i].offset, sync._host_segs[i].round_to) for i in range(L)])
+            nb = sync.layout.nbytes
+            base = sync._stage_ptr - sync.staging.data_ptr()
+
+            def best(fn, k=5):
+                fn()
+                b = float("inf")
+                for _ in range(k):
+                    t1 = time.perf_counter()
+                    fn()
+                    b = min(b, time.perf_counter() - t1)
+                return b
+
+            def pack_leg():
+                _lib.check(lib.adt_pack_host(segs, L, sync._stage_ptr, sync._sumsq_ptr, sync.threads))
+
+            def dma_leg():
+                sync.packed[:nb].copy_(sync.staging[base:base + nb], non_blocking=True)
+                stream.synchronize()
+
+            tuned["legs_ms"] = {"host_pack": best(pack_leg) * 1e3, "dma": best(dma_leg) * 1e3}
+            # host DRAM bytes a step moves (both legs share it): masters read by the packer,
+            # staging written (non-temporal) and read again by the DMA, direct layers read by the DMA
+            tuned["host_dram_bytes"] = sum(
+                4 * sync._host_segs[i].count if sync.direct[i]
+                else (4 + 2 * sync._host_segs[i].round_to) * sync._host_segs[i].count for i in range(L))
         del sync
         return dt, n_steps, ndirect, h2d
 
@@ -1136,6 +1171,9 @@ def run_e2e_host_master(args, host, rs, dev, steps=20):
     return {"value": byts / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 16,
             "ms_per_step": dt * 1e3, "steps": n_steps, "host_threads": tuned.get("threads") or host_threads(),
             "host_threads_available": host_threads(), "copy_batch_bytes": tuned.get("batch"),
+            "legs_ms": tuned.get("legs_ms"), "host_dram_bytes_per_step": tuned.get("host_dram_bytes"),
+            "host_dram_GBps": (tuned["host_dram_bytes"] / dt / 1e9) if tuned.get("host_dram_bytes") else None,
+            "frac_of_legs_floor": (max(tuned["legs_ms"].values()) / (dt * 1e3)) if tuned.get("legs_ms") else None,
             "tuning_ms": tuned.get("timings_ms"),
             "raw_fp32_bytes": 4 * n, "raw_fp32_wall_ms_per_step": dt_raw * 1e3, "vs_raw_fp32": dt_raw / dt,
             "direct_full_layers": ndirect, "all_packed_ms_per_step": dt_packed * 1e3,
