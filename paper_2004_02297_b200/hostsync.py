@@ -287,7 +287,10 @@ class HostWeightSync:
 
     def observe_final(self, batch: int) -> list[tuple]:
         """The observation after the last update (training.py:246-254): the
-        norms of the masters as they are now, from a host pass (no transfer)."""
+        norms of the masters as they are now, from a host pass (no transfer).
+        A fixed schedule observes nothing (training.py:246): no rows."""
+        if not self.adaptive:
+            return []
         segs = self._host_segs
         scratch = np.empty(self.layout.nbytes + 64, dtype=np.uint8)
         base = (-scratch.ctypes.data) % 64

@@ -528,7 +528,11 @@ class WeightSync:
 
     def observe_final(self, batch: int) -> list[tuple]:
         """Norm-only pass over the masters (the observation after the last
-        update, training.py:246-254); returns its trace rows labelled `batch`."""
+        update, training.py:246-254); returns its trace rows labelled `batch`.
+        A fixed schedule observes nothing (the reference only observes in
+        adaptive mode, training.py:246): no rows."""
+        if not self.adaptive:
+            return []
         if self.awp_on_device:
             d = self._dawp
             rows = self.drain_trace()

@@ -83,3 +83,22 @@ def test_dp_training_over_ranks_matches_simulated_workers(example, transport):
     assert dp["final_loss"] == pytest.approx(sim["final_loss"], rel=1e-6)
     assert dp["val_accuracy"] == pytest.approx(sim["val_accuracy"], abs=1e-3)
     assert dp["weight_bytes_vs_fp32"] == pytest.approx(sim["weight_bytes_vs_fp32"])
+
+
+def test_cpu_master_training_loop():
+    """examples/train_mlp_cpu_master.py — the paper's CPU-master setting as a
+    training loop: host masters updated by the CPU, packed on the host at the
+    AWP widths (HostWeightSync), unpacked on the GPU for the workers, FP32
+    gradients back. The loss falls, AWP widens layers, the weight stream stays
+    below FP32 and the accuracy matches the uncompressed run."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    sys.path.insert(0, os.path.join(ROOT, "examples"))
+    import train_mlp_cpu_master as ex
+    fp32 = ex.main(["--steps", "120", "--fp32", "--sizes", "64,512,512,10"])
+    assert fp32["weight_bytes_vs_fp32"] == 1.0 and fp32["final_loss"] < 0.5 * fp32["first_loss"]
+    awp = ex.main(["--steps", "120", "--interval", "5", "--threshold", "1e-3", "--sizes", "64,512,512,10"])
+    assert awp["final_loss"] < 0.5 * awp["first_loss"]
+    assert abs(awp["val_accuracy"] - fp32["val_accuracy"]) < 0.03
+    assert awp["weight_bytes_vs_fp32"] < 1.0 and max(awp["final_bits"]) > 8
+    assert awp["trace_rows"] == 120 * 3
