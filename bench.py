@@ -203,6 +203,29 @@ def reference_package():
     return weightpack
 
 
+def reference_parallel_pack_GBps(wp, layers, rs, reps=2):
+    """The reference's own threaded packer, codec.pack_parallel (codec.py:156-180)
+    with one worker per host thread, in place of pack_vectorized in the same
+    step (unpack + l2_norm unchanged): the host-thread-parallel form of the
+    reference path, reported beside the training-path number. None without
+    baseline/_ref."""
+    if wp is None:
+        return None
+    th = reference_threads()
+    byts = 2 * sum((4 + r) * w.size for w, r in zip(layers, rs))
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        blocks = [wp.pack_parallel(w, r, th) for w, r in zip(layers, rs)]
+        for b in blocks:
+            wp.unpack(b)
+        for w in layers:
+            wp.l2_norm(w)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": byts / best / 1e9, "unit": UNIT, "pack": f"codec.pack_parallel(w, r, {th})",
+            "seconds_per_pass": best}
+
+
 def reference_step(wp, layers, rs, workers=1):
     """One step of the reference's own CPU path, the calls its training loop
     makes per batch (training.py:209-213 pack every layer once with
@@ -286,7 +309,8 @@ def run_cpu_baseline(counts, rs, budget_s=10.0, min_reps=2):
     mean = sum(times) / len(times)
     return {"value": byts / mean / 1e9, "unit": UNIT, "cores": reference_threads(), "kind": kind,
             "sample": f"{sample}; {what}; mean of {len(times)} passes ({sum(times):.1f} s)",
-            "threads_note": THREADS_NOTE, "seconds_per_pass": mean, "host_cpus": os.cpu_count()}
+            "threads_note": THREADS_NOTE, "seconds_per_pass": mean, "host_cpus": os.cpu_count(),
+            "with_pack_parallel": reference_parallel_pack_GBps(wp, layers, rs)}
 
 
 def bench_config(args, counts, bits, rs, world=1, transport=None):
@@ -330,7 +354,8 @@ def main_reference(args):
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": reference_threads(), "kind": kind,
                          "sample": f"{sample}; {what}; each step one pass" + (f" with {world} worker unpacks" if world > 1 else ""),
-                         "threads_note": THREADS_NOTE, "host_cpus": os.cpu_count()},
+                         "threads_note": THREADS_NOTE, "host_cpus": os.cpu_count(),
+                         "with_pack_parallel": reference_parallel_pack_GBps(wp, layers, rs)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
