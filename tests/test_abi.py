@@ -157,3 +157,26 @@ def test_host_entry_points_validate_arguments(lib):
     assert h.adt_sumsq_f64_partials(10 ** 9, ctypes.byref(n)) == lib.ADT_OK and 1 <= n.value <= 1184
     t = ctypes.c_int(0)
     assert h.adt_host_threads(ctypes.byref(t)) == lib.ADT_OK and t.value == len(os.sched_getaffinity(0))
+
+
+def test_reference_plug_binds_the_hot_path_modules(tmp_path):
+    """tests/refsuite/plug: the UNMODIFIED reference package (baseline/_ref)
+    imports with weightpack.codec / weightpack.precision bound to this
+    package and every other module from the reference — checked without a
+    GPU (nothing is called); the GPU run of the suite is
+    tests/test_gpu_reference_suite.py."""
+    import subprocess
+    import sys
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "weightpack")):
+        pytest.skip("baseline/_ref not installed (run __graft_entry__.build() where /root/reference exists)")
+    code = (
+        "import sys; sys.path.insert(0, %r); import run; run.install_plugged(%r)\n"
+        "import weightpack, weightpack.training as t, weightpack.cli as c, weightpack.transfer as tr\n"
+        "import paper_2004_02297_b200.codec as oc, paper_2004_02297_b200.precision as op\n"
+        "assert weightpack.pack_vectorized is oc.pack_vectorized and weightpack.l2_norm is op.l2_norm\n"
+        "assert t.unpack is oc.unpack and c.codec is oc and tr.PackedBlock is oc.PackedBlock\n"
+        "assert t.__file__.startswith(%r)\n"
+        "print('plug ok')\n") % (os.path.join(ROOT, "tests", "refsuite"), ref, os.path.join(ref, "weightpack"))
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=tmp_path)
+    assert p.returncode == 0 and "plug ok" in p.stdout, p.stdout[-2000:] + p.stderr[-4000:]
