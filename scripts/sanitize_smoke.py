@@ -108,6 +108,13 @@ def main():
         hs = adt.HostWeightSync([h.copy() for h in hosts_nz], ring_bytes=ring, slot_bytes=320 << 10,
                                 zero_copy_bytes=zc)
         hs.launch(fused_norm=True)
+    # drop-in per-call host API: small arrays (one staged round trip) and a large one
+    for n in (1, 300, 4097, 300000):
+        w = rng.standard_normal(n, dtype=np.float32)
+        for r in (1, 3, 4):
+            blk = adt.pack_vectorized(w, r)
+            adt.unpack(blk)
+        adt.l2_norm(w)
     torch.cuda.synchronize()
     print("sanitize smoke ok")
 
