@@ -23,7 +23,7 @@ for l in open(sys.argv[1]):
     except Exception:
         continue
     fp, ex = d.get("fp32_allgather") or {}, d.get("exchange") or {}
-    print(f"N={d['n_gpus']} {d['config']['transport']:<4} value {d['value']:9.1f} GB/s  sync {d['ms_per_step'] * 1e3:8.1f} us"
+    print(f"N={d['n_gpus']} {d['setup']['transport']:<4} value {d['value']:9.1f} GB/s  sync {d['ms_per_step'] * 1e3:8.1f} us"
           f"  busbw {ex.get('busbw_GBps', float('nan')):7.1f} GB/s  fp32 all-gather {fp.get('ms', float('nan')) * 1e3:8.1f} us"
           f" ({fp.get('busbw_GBps', float('nan')):7.1f} GB/s)  e2e {(d.get('e2e') or {}).get('value', 0):8.1f}")
 PY
